@@ -1,0 +1,302 @@
+#!/usr/bin/env python
+"""Tree-ensemble inference benchmark (BASELINE.json metric: rows/s at 1/2/4/8 B200).
+
+One step = one pass of the whole hot path (lowering is done
+once at load; per step: feature gather + compare / traversal, leaf-value gather,
+per-tree reduction, finalize) over one batch of synthetic rows.  Default
+workload = BASELINE.json configs[1] (C2: random forest, 100 trees, depth 8,
+1M rows x 28 features, binary classification; predict -> int32 labels).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config C2]
+  python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N   (row shards, weak scaling)
+
+Timing: W untimed warm-ups, then K steps each bracketed by CUDA events on the
+launching stream; L2 is flushed (256 MiB write) before every step, outside the
+events; barrier + synchronize on both sides of the timed region; max over
+ranks.  `e2e` re-times the same metric through the public host-buffer API
+(bridger_predict_host: H2D of the pinned input + predict + D2H of the labels
+inside the timed region).  `roofline` reports the dominant kernel (traversal)
+against the shared-memory pipe, its binding resource.
+`cpu_baseline` is the oracle (oracle/) timed on this host's cores on a bounded
+sample (a reported baseline, not the target).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], None, set()
+        for l in getattr(self, "lines", []):
+            p = [x.strip() for x in l.split(",")]
+            if len(p) < 6:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, p[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_baseline(m, cfg, target_s=10.0):
+    """The oracle as it stands, on this host's cores, on a bounded row sample."""
+    import oracle
+    from synth import gen_x
+    cores = oracle.n_cores()
+    n = 4096
+    X = gen_x(cfg.seed, 0, n, cfg.n_features)
+    t = time.perf_counter()
+    oracle.run(m, X, n_threads=cores, want=("label", "pred"))
+    dt = time.perf_counter() - t
+    n2 = int(min(cfg.n_rows, max(n, n * (target_s * 0.8) / max(dt, 1e-6))))
+    X = gen_x(cfg.seed, 0, n2, cfg.n_features)
+    t = time.perf_counter()
+    oracle.run(m, X, n_threads=cores, want=("label", "pred"))
+    dt = time.perf_counter() - t
+    return {"value": n2 / dt, "unit": "rows/s", "cores": cores, "kind": "oracle",
+            "sample": f"rows [0, {n2}) of the {cfg.name} input ({n2}/{cfg.n_rows} rows), all {cfg.n_trees} trees, "
+                      f"{dt:.1f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle timed on host cores, same metric/config."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    from synth import gen_x, make_config
+    cfg, m = make_config(args.config)
+    cores = oracle.n_cores()
+    # per step: a bounded sample sized so warmup+steps finish in ~2 minutes
+    probe = gen_x(cfg.seed, 0, 2048, cfg.n_features)
+    t = time.perf_counter()
+    oracle.run(m, probe, n_threads=cores, want=("label", "pred"))
+    rate = 2048 / (time.perf_counter() - t)
+    per_step_s = min(8.0, 120.0 / max(1, args.steps + args.warmup))
+    n = int(max(2048, min(cfg.n_rows, rate * per_step_s)))
+    X = gen_x(cfg.seed, 0, n, cfg.n_features)
+    for _ in range(args.warmup):
+        oracle.run(m, X[: min(n, 4096)], n_threads=cores, want=("label", "pred"))
+    times = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        oracle.run(m, X, n_threads=cores, want=("label", "pred"))
+        times.append(time.perf_counter() - t)
+    tot = sum(times)
+    value = n * args.steps / tot
+    line = {
+        "impl": "reference", "metric": "tree-ensemble inference rows/sec", "value": value, "unit": "rows/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 compare, f64 accumulate",
+        "data": "synthetic", "config": workload_config(cfg, world),
+        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{n} rows per step (bounded sample of the {cfg.n_rows}-row workload)"},
+        "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(cfg, world):
+    return {"workload": f"{cfg.name}: {cfg.describe}", "n_rows_per_gpu": cfg.n_rows, "n_trees": cfg.n_trees,
+            "depth": cfg.depth, "n_features": cfg.n_features, "n_outputs": cfg.n_classes,
+            "sharding": f"rows x{world}" if world > 1 else "single GPU",
+            "l2": "flushed before every timed step (256 MiB write)", "output": "predict (int32 labels)"
+            if cfg.kind == "classification" else "predict (fp32 scores)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--variant", default=None, choices=[None, "auto", "traverse", "gemm"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2405_12491_b200 as B
+    from synth import gen_x, gen_x_torch, make_config
+
+    world, rank, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg, m = make_config(args.config)
+    n = cfg.n_rows
+    row0 = rank * n
+    X = gen_x_torch(cfg.seed, row0, n, cfg.n_features, device=dev)
+    model = B.Model(m, device=local, variant=args.variant)
+    classif = cfg.kind == "classification"
+    out = torch.empty(n, dtype=torch.int32, device=dev) if classif else torch.empty((n, 1), device=dev)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+    st = torch.cuda.current_stream(dev)
+
+    for _ in range(args.warmup):
+        flush.fill_(1.0)
+        model.predict(X, out=out)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    B.hot_kernel_timing(True)
+    B.hot_kernel_time()
+    l0 = B.launch_count()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        t_wall = time.perf_counter()
+        for e0, e1 in ev:
+            flush.fill_(1.0)
+            e0.record(st)
+            model.predict(X, out=out)
+            e1.record(st)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        t_wall = time.perf_counter() - t_wall
+    launches = B.launch_count() - l0
+    hot_ms, hot_n = B.hot_kernel_time()
+    B.hot_kernel_timing(False)
+    step_ms = sum(e0.elapsed_time(e1) for e0, e1 in ev)
+    t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = t.item() / args.steps
+    value = n * world / (ms_per_step / 1e3)
+
+    # ---- e2e through the public host-buffer API (pinned input, labels back to host)
+    Xh = torch.from_numpy(gen_x(cfg.seed, row0, n, cfg.n_features)).pin_memory()
+    oh = torch.empty(n, dtype=torch.int32).pin_memory() if classif else torch.empty((n, 1)).pin_memory()
+    model.predict_host(Xh, out=oh)
+    e2e_times = []
+    for _ in range(max(1, args.e2e_steps)):
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        model.predict_host(Xh, out=oh)
+        e2e_times.append(time.perf_counter() - t0)
+    te = torch.tensor([sum(e2e_times) / len(e2e_times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e = {"value": n * world / te.item(), "unit": "rows/s", "h2d_bytes_per_step": n * cfg.n_features * 4,
+           "d2h_bytes_per_step": int(oh.numel() * oh.element_size()),
+           "api": "bridger_predict_host (2-stream chunked H2D/compute/D2H pipeline)"}
+
+    # ---- roofline of the dominant kernel
+    peaks, src = _peaks()
+    info = model.info()
+    clocks = clk.summary()
+    variant = info["variant"]
+    hot_avg = hot_ms / max(1, hot_n)
+    if variant == "traverse":
+        # algorithmic shared-memory bytes per launch: per (row, tree) D node records (8 B) +
+        # D feature values (4 B) + K leaf values (4 B)
+        alg = n * cfg.n_trees * (12 * cfg.depth + 4 * cfg.n_classes)
+        sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+        peak = sm_count * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e9   # GB/s
+        achieved = alg / (hot_avg / 1e3) / 1e9
+        roof = {"bound": "alu", "resource": "shared-memory (LSU) pipe: 128 B/clk/SM x SMs x max SM clock",
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                "kernel": "trav_kernel", "kernel_ms": hot_avg,
+                "hbm_frac": (n * cfg.n_features * 4 + n * 4) / (hot_avg / 1e3) / 1e9 / peaks["hbm_gbs"],
+                "peak_source": f"derived from guide unit counts ({src} sm_max_mhz)"}
+    else:
+        roof = {"bound": "tensor", "achieved": None, "peak": None, "unit": "TOP/s", "frac": None, "traffic": None,
+                "kernel": "path_contract", "kernel_ms": hot_avg}
+    tr = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tr):
+        try:
+            roof["traffic"] = json.load(open(tr)).get(f"{cfg.name}:{variant}")
+        except Exception:
+            pass
+
+    line = {
+        "metric": "tree-ensemble inference rows/sec", "value": value, "unit": "rows/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 compare, int64 fixed-point accumulate" if info["acc_is_int64"] else "f32 compare, f64 accumulate",
+        "data": "synthetic (counter-based generator, seeded; random calibrated trees)",
+        "config": workload_config(cfg, world), "variant": variant, "exact_tier": info["exact_tier"],
+        "gpu_launches": launches, "wall_s_timed": t_wall, "roofline": roof, "e2e": e2e, "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(m, cfg)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

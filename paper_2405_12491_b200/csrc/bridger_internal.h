@@ -1,0 +1,141 @@
+// Internal declarations shared by the library's translation units (host
+// lowering, kernels, C ABI).  Not installed; the public surface is
+// include/bridger.h.
+#pragma once
+
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/bridger.h"
+
+namespace bridger {
+
+// ---------------------------------------------------------------- errors ----
+void set_error(const std::string& msg);
+bridger_status fail(bridger_status s, const std::string& msg);
+
+// ------------------------------------------------------------ lowering -------
+// One tree padded to a perfect tree of depth D in heap order (step a0,
+// SURVEY.md §8(a)): children of heap node i are 2i+1 / 2i+2; leaves are heap
+// nodes I..2I (I = 2^D - 1) and leaf index l = heap - I.  A leaf of the
+// original tree at depth d < D is REPLICATED into all 2^(D-d) heap leaves under
+// its heap position, and the internal heap nodes below it get a dummy split
+// (feature 0, threshold 0): both subtrees are identical, so any routing of a
+// dummy (NaN included) reaches the same value and the same original leaf id
+// (reading c11; the leaf self-loop of SPEC.md:283 made static).
+struct PaddedTree {
+  int32_t depth = 0;
+  std::vector<int32_t> feature;   // [I]
+  std::vector<float> threshold;   // [I]
+  std::vector<uint8_t> missing;   // [I] (0 when the desc has no missing_left)
+  std::vector<int32_t> leaf_id;   // [L] original tree-local node id
+  std::vector<float> leaf_value;  // [L*K]
+};
+
+bridger_status validate_desc(const bridger_model_desc* d);
+int32_t tree_depth(const bridger_model_desc* d, int32_t t);  // desc must be valid
+void pad_tree(const bridger_model_desc* d, int32_t t, int32_t D, PaddedTree* out);
+
+struct Exactness {
+  int32_t q = 0;        // every leaf value is an integer multiple of 2^q
+  int32_t tier = BRIDGER_EXACT_E53;
+  double log2_M = -1.0; // log2 of max_k sum_t max_leaf |v| 2^-q  (-1 when M == 0)
+};
+Exactness analyze_exactness(const bridger_model_desc* d);
+
+// Universal path matrix of depth D (step a0/a3): C[i][l] in {+1,-1,0},
+// Dv[l] = number of left turns on leaf l's root path.
+void path_matrix(int32_t D, int32_t i_pad, int32_t l_pad, int8_t* C, int32_t* Dv);
+inline int32_t gemm_i_pad(int32_t D) { int32_t I = (1 << D) - 1; return ((I + 31) / 32) * 32; }
+inline int32_t gemm_l_pad(int32_t D) { int32_t L = 1 << D; int32_t p = ((L + 15) / 16) * 16; return p < 16 ? 16 : p; }
+
+// ----------------------------------------------- traversal (K4) layout -------
+// A chunk is a contiguous set of trees (same padded depth) resident in one
+// CTA's shared memory for the whole kernel.  In global memory (and SMEM) a
+// chunk is:  nodes  [n_trees][I] {float threshold; int32 feature | missing<<31}
+//            leaves [n_trees][L][K] float (fixed-point scaled when exact)
+struct TravChunk {
+  int64_t offset;      // byte offset of the chunk inside the packed buffer
+  int32_t bytes;       // total bytes (multiple of 16)
+  int32_t n_trees;
+  int32_t depth;
+  int32_t leaf_offset; // byte offset of the leaves inside the chunk
+  int32_t first_slot;  // index of the chunk's first tree slot (slot -> original tree)
+  int32_t pad_;
+};
+
+struct TravLayout {
+  int32_t n_warps = 8;          // warps per CTA (each owns a 32-row X block)
+  int32_t smem_bytes = 0;       // dynamic shared memory per CTA
+  int32_t chunk_budget = 0;     // max bytes of one chunk
+  bool has_missing = false;
+  std::vector<TravChunk> chunks;
+  std::vector<uint8_t> data;        // packed chunks
+  std::vector<int32_t> slot_tree;   // [slots] original tree index
+  std::vector<int64_t> slot_leafid_off; // [slots] offset into leaf_ids
+  std::vector<int32_t> leaf_ids;    // concatenated [L] per slot (original ids)
+};
+
+// DSMEM reduction slots of the cluster mode: [NW][2][n_chunks-1][32 rows][K] x 8 B
+inline int32_t trav_slot_bytes(int32_t n_warps, int32_t n_chunks, int32_t K) {
+  return (n_chunks >= 2 && n_chunks <= 8) ? n_warps * 2 * (n_chunks - 1) * 32 * K * 8 : 0;
+}
+
+// Builds the resident-chunk layout; returns false (with reason) when a single
+// tree does not fit the shared-memory budget.
+bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& depth,
+                       const Exactness& ex, bool acc_int, TravLayout* out, std::string* why);
+
+// --------------------------------------------------- GEMM-path layout -------
+struct GemmClass {
+  int32_t depth, i_pad, l_pad;
+  int32_t first_tree, n_trees;   // trees of this depth class (in sorted order)
+};
+
+// ------------------------------------------------------------- finalize -----
+struct FinalizeArgs {
+  int32_t task, agg, post, K;
+  int32_t total_trees;
+  int32_t q;          // raw = acc * 2^q
+  int32_t acc_int;    // accumulators are int64 fixed point (else double)
+  int32_t want;       // 0 predict, 1 proba, 2 raw
+  double leaf_scale;
+  const double* base; // device [K] or nullptr
+  void* out;
+};
+
+}  // namespace bridger
+
+struct bridger_model {
+  int device = 0;
+  int32_t T = 0, F = 0, K = 0, task = 0, agg = 0, post = 0;
+  double leaf_scale = 1.0;
+  std::vector<double> base;
+  bridger::Exactness ex;
+  bool acc_int = true;
+  int32_t max_depth = 0;
+  int32_t variant = BRIDGER_VARIANT_AUTO;
+  int32_t resolved_variant = BRIDGER_VARIANT_TRAVERSE;
+
+  // traversal layout on device
+  bridger::TravLayout trav;
+  bool trav_ok = false;
+  void* d_trav_data = nullptr;
+  void* d_trav_chunks = nullptr;
+  int32_t* d_slot_tree = nullptr;
+  int64_t* d_slot_leafid_off = nullptr;
+  int32_t* d_leaf_ids = nullptr;
+  double* d_base = nullptr;
+
+  // GEMM-path layout on device (filled by gemm_path.cu)
+  bool gemm_ok = false;
+  std::vector<bridger::GemmClass> gemm_classes;
+  void* d_gemm = nullptr;   // opaque device block owned by gemm_path.cu
+  void* gemm_host = nullptr;
+
+  // bridger_predict_host pipeline context (streams + staging buffers), lazily built
+  std::mutex host_mu;
+  void* host_ctx = nullptr;
+};

@@ -1,0 +1,327 @@
+// Host-side lowering (step a0): validation, padding to
+// perfect heap-ordered trees, exactness analysis (reading c9), the universal
+// path matrix C_D / D_D, and the packed device layouts of the traversal
+// kernels.  The COR view of a tree becomes five tensors per
+// tree: A (feature index), B (threshold), C_D/D_D (per depth, universal) and E
+// (leaf values); CML "data type rewriting" and "redundant operator
+// elimination" (Table 2) show up as the int8 path matrix and the
+// exact gather that replaces a one-hot feature-selection matmul.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "bridger_internal.h"
+
+namespace bridger {
+
+static inline bool finite_f(float v) { return std::isfinite(v); }
+
+bridger_status validate_desc(const bridger_model_desc* d) {
+  if (!d) return fail(BRIDGER_E_NULL_ARG, "desc is NULL");
+  if (!d->tree_offsets || !d->feature || !d->threshold || !d->left || !d->right || !d->value)
+    return fail(BRIDGER_E_NULL_ARG, "desc has a NULL required array");
+  if (d->n_trees < 1) return fail(BRIDGER_E_SHAPE, "n_trees must be >= 1");
+  if (d->n_features < 1) return fail(BRIDGER_E_SHAPE, "n_features must be >= 1");
+  if (d->n_outputs < 1 || d->n_outputs > 64) return fail(BRIDGER_E_SHAPE, "n_outputs must be in [1,64]");
+  if (d->task != BRIDGER_TASK_REGRESSION && d->task != BRIDGER_TASK_CLASSIFICATION)
+    return fail(BRIDGER_E_UNSUPPORTED, "unknown task");
+  if (d->agg != BRIDGER_AGG_MEAN && d->agg != BRIDGER_AGG_SUM) return fail(BRIDGER_E_UNSUPPORTED, "unknown agg");
+  if (d->post != BRIDGER_POST_IDENTITY && d->post != BRIDGER_POST_SIGMOID)
+    return fail(BRIDGER_E_UNSUPPORTED, "unknown post");
+  if (d->post == BRIDGER_POST_SIGMOID && (d->task != BRIDGER_TASK_CLASSIFICATION || d->n_outputs != 1))
+    return fail(BRIDGER_E_UNSUPPORTED, "sigmoid post-transform needs a K == 1 classifier");
+  if (!std::isfinite(d->leaf_scale)) return fail(BRIDGER_E_SHAPE, "leaf_scale not finite");
+  if (d->tree_offsets[0] != 0) return fail(BRIDGER_E_INVALID_TREE, "tree_offsets[0] != 0");
+  const int32_t F = d->n_features, K = d->n_outputs;
+  std::vector<int32_t> parents;
+  std::vector<uint8_t> seen;
+  std::vector<int32_t> stack;
+  for (int32_t t = 0; t < d->n_trees; ++t) {
+    const int64_t a = d->tree_offsets[t], b = d->tree_offsets[t + 1];
+    if (b <= a) return fail(BRIDGER_E_INVALID_TREE, "tree_offsets not strictly increasing at tree " + std::to_string(t));
+    if (b - a > (int64_t)1 << 30) return fail(BRIDGER_E_UNSUPPORTED, "tree too large");
+    const int32_t n = (int32_t)(b - a);
+    parents.assign(n, 0);
+    for (int32_t i = 0; i < n; ++i) {
+      const int32_t l = d->left[a + i], r = d->right[a + i];
+      if ((l == -1) != (r == -1))
+        return fail(BRIDGER_E_INVALID_TREE, "tree " + std::to_string(t) + " node " + std::to_string(i) + ": exactly one child is -1");
+      if (l == -1) {
+        for (int32_t k = 0; k < K; ++k)
+          if (!finite_f(d->value[(a + i) * K + k]))
+            return fail(BRIDGER_E_INVALID_TREE, "tree " + std::to_string(t) + " leaf " + std::to_string(i) + ": non-finite value");
+        continue;
+      }
+      if (l <= 0 || r <= 0 || l >= n || r >= n || l == i || r == i || l == r)
+        return fail(BRIDGER_E_INVALID_TREE, "tree " + std::to_string(t) + " node " + std::to_string(i) + ": child out of range");
+      const int32_t f = d->feature[a + i];
+      if (f < 0 || f >= F)
+        return fail(BRIDGER_E_INVALID_TREE, "tree " + std::to_string(t) + " node " + std::to_string(i) + ": feature out of [0,F)");
+      if (std::isnan(d->threshold[a + i]))
+        return fail(BRIDGER_E_INVALID_TREE, "tree " + std::to_string(t) + " node " + std::to_string(i) + ": NaN threshold");
+      parents[l]++;
+      parents[r]++;
+    }
+    for (int32_t i = 1; i < n; ++i)
+      if (parents[i] != 1)
+        return fail(BRIDGER_E_INVALID_TREE, "tree " + std::to_string(t) + " node " + std::to_string(i) + ": must have exactly one parent");
+    seen.assign(n, 0);
+    stack.clear();
+    stack.push_back(0);
+    int32_t count = 0;
+    while (!stack.empty()) {
+      const int32_t i = stack.back();
+      stack.pop_back();
+      if (seen[i]) return fail(BRIDGER_E_INVALID_TREE, "tree " + std::to_string(t) + ": cycle");
+      seen[i] = 1;
+      ++count;
+      if (d->left[a + i] != -1) {
+        stack.push_back(d->left[a + i]);
+        stack.push_back(d->right[a + i]);
+      }
+    }
+    if (count != n) return fail(BRIDGER_E_INVALID_TREE, "tree " + std::to_string(t) + ": unreachable nodes");
+  }
+  return BRIDGER_OK;
+}
+
+int32_t tree_depth(const bridger_model_desc* d, int32_t t) {
+  const int64_t a = d->tree_offsets[t];
+  int32_t best = 0;
+  std::vector<std::pair<int32_t, int32_t>> st{{0, 0}};
+  while (!st.empty()) {
+    auto [i, dep] = st.back();
+    st.pop_back();
+    if (d->left[a + i] == -1) {
+      best = std::max(best, dep);
+    } else {
+      st.push_back({d->left[a + i], dep + 1});
+      st.push_back({d->right[a + i], dep + 1});
+    }
+  }
+  return best;
+}
+
+void pad_tree(const bridger_model_desc* d, int32_t t, int32_t D, PaddedTree* out) {
+  const int64_t a = d->tree_offsets[t];
+  const int32_t K = d->n_outputs;
+  const int32_t I = (1 << D) - 1, L = 1 << D;
+  out->depth = D;
+  out->feature.assign(I, 0);
+  out->threshold.assign(I, 0.0f);
+  out->missing.assign(I, 0);
+  out->leaf_id.assign(L, -1);
+  out->leaf_value.assign((size_t)L * K, 0.0f);
+  struct E { int32_t n; int32_t h; int32_t dep; };
+  std::vector<E> st{{0, 0, 0}};
+  while (!st.empty()) {
+    E e = st.back();
+    st.pop_back();
+    const int64_t g = a + e.n;
+    if (d->left[g] == -1) {
+      const int32_t span = 1 << (D - e.dep);
+      const int32_t first = e.h * span + (span - 1) - I;  // leftmost heap leaf under h, as leaf index
+      for (int32_t j = 0; j < span; ++j) {
+        out->leaf_id[first + j] = e.n;
+        for (int32_t k = 0; k < K; ++k) out->leaf_value[(size_t)(first + j) * K + k] = d->value[g * K + k];
+      }
+    } else {
+      out->feature[e.h] = d->feature[g];
+      out->threshold[e.h] = d->threshold[g];
+      out->missing[e.h] = d->missing_left ? (d->missing_left[g] != 0) : 0;
+      st.push_back({d->left[g], 2 * e.h + 1, e.dep + 1});
+      st.push_back({d->right[g], 2 * e.h + 2, e.dep + 1});
+    }
+  }
+}
+
+// exponent of the lowest set bit of a non-zero finite float
+static int32_t lsb_exp(float v) {
+  uint32_t u;
+  std::memcpy(&u, &v, 4);
+  const uint32_t E = (u >> 23) & 0xFF, M = u & 0x7FFFFF;
+  if (E == 0) return -149 + __builtin_ctz(M);
+  return (int32_t)E - 150 + __builtin_ctz(M | 0x800000u);
+}
+
+Exactness analyze_exactness(const bridger_model_desc* d) {
+  Exactness ex;
+  const int32_t K = d->n_outputs;
+  int32_t q = INT32_MAX;
+  for (int32_t t = 0; t < d->n_trees; ++t)
+    for (int64_t g = d->tree_offsets[t]; g < d->tree_offsets[t + 1]; ++g)
+      if (d->left[g] == -1)
+        for (int32_t k = 0; k < K; ++k) {
+          const float v = d->value[g * K + k];
+          if (v != 0.0f) q = std::min(q, lsb_exp(v));
+        }
+  if (q == INT32_MAX) {  // every leaf value is zero
+    ex.q = 0;
+    ex.tier = BRIDGER_EXACT_E53;
+    ex.log2_M = -1.0;
+    return ex;
+  }
+  ex.q = q;
+  bool overflow = false;
+  unsigned __int128 worst = 0;
+  std::vector<unsigned __int128> sum(K, 0);
+  for (int32_t t = 0; t < d->n_trees && !overflow; ++t)
+    for (int32_t k = 0; k < K && !overflow; ++k) {
+      float mx = 0.0f;
+      for (int64_t g = d->tree_offsets[t]; g < d->tree_offsets[t + 1]; ++g)
+        if (d->left[g] == -1) mx = std::max(mx, std::fabs(d->value[g * K + k]));
+      const long double term = std::ldexp((long double)mx, -q);  // exact: an integer
+      if (term >= std::ldexp(1.0L, 63)) { overflow = true; break; }
+      sum[k] += (unsigned __int128)(uint64_t)term;
+    }
+  if (overflow) {
+    ex.tier = BRIDGER_EXACT_F64;
+    ex.log2_M = 64.0;
+    return ex;
+  }
+  for (int32_t k = 0; k < K; ++k) worst = std::max(worst, sum[k]);
+  const long double Mf = (long double)worst;
+  ex.log2_M = worst == 0 ? -1.0 : (double)std::log2(Mf);
+  if (worst < ((unsigned __int128)1 << 53)) ex.tier = BRIDGER_EXACT_E53;
+  else if (worst < ((unsigned __int128)1 << 63)) ex.tier = BRIDGER_EXACT_E63;
+  else ex.tier = BRIDGER_EXACT_F64;
+  return ex;
+}
+
+void path_matrix(int32_t D, int32_t i_pad, int32_t l_pad, int8_t* C, int32_t* Dv) {
+  const int32_t I = (1 << D) - 1, L = 1 << D;
+  std::memset(C, 0, (size_t)i_pad * l_pad);
+  for (int32_t l = 0; l < L; ++l) {
+    // walk the root path of leaf l: bit (D-1-k) of l is the turn at depth k (1 = right)
+    int32_t h = 0, lefts = 0;
+    for (int32_t k = 0; k < D; ++k) {
+      const int32_t right = (l >> (D - 1 - k)) & 1;
+      C[(size_t)h * l_pad + l] = right ? -1 : +1;
+      lefts += !right;
+      h = 2 * h + 1 + right;
+    }
+    if (Dv) Dv[l] = lefts;
+    (void)I;
+  }
+}
+
+// ------------------------------------------------------ traversal layout ----
+static constexpr int32_t kSmemMax = 232448;  // 227 KB opt-in per block (sm_100)
+
+bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& depth,
+                       const Exactness& ex, bool acc_int, TravLayout* out, std::string* why) {
+  const int32_t T = d->n_trees, F = d->n_features, K = d->n_outputs;
+  out->has_missing = d->missing_left != nullptr;
+  // per-warp X blocks: feature-major working block + dense staging block, 32 rows each
+  const int32_t xw = 2 * 32 * F * 4;
+  int32_t nw = 8;
+  while (nw > 1 && nw * xw > 96 * 1024) --nw;
+  const int32_t misc = 1024 + ((1 + 5 * nw) * 8 + 15) / 16 * 16;
+  const int32_t base_budget = kSmemMax - misc - nw * xw;
+  out->n_warps = nw;
+  auto tree_bytes = [&](int32_t D) -> int64_t {
+    return (int64_t)((1 << D) - 1) * 8 + (int64_t)(1 << D) * K * 4;
+  };
+  auto chunk_bytes = [&](int32_t n, int32_t D) -> int64_t {
+    const int64_t nodes = (int64_t)n * ((1 << D) - 1) * 8;
+    const int64_t nodes_al = (nodes + 15) / 16 * 16;
+    return nodes_al + ((int64_t)n * (1 << D) * K * 4 + 15) / 16 * 16;
+  };
+  std::vector<int32_t> order(T);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return depth[a] < depth[b]; });
+  const int32_t Dmax = depth[order.back()];
+  // greedy chunking over depth-sorted trees, then even re-balancing inside runs
+  // of equal depth.  The cluster-mode reduction slots depend on the chunk
+  // count, so iterate until the budget is consistent.
+  struct Run { int32_t start, n, D; };
+  std::vector<Run> bal;
+  int32_t budget = base_budget, n_prev = 1;
+  for (int iter = 0; iter < 4; ++iter) {
+    budget = base_budget - trav_slot_bytes(nw, n_prev, K);
+    if (chunk_bytes(1, Dmax) > budget) {
+      if (why) *why = "one tree of depth " + std::to_string(Dmax) + " (" + std::to_string(tree_bytes(Dmax)) +
+                      " B) exceeds the shared-memory chunk budget " + std::to_string(budget);
+      return false;
+    }
+    std::vector<Run> runs;
+    int32_t s = 0;
+    while (s < T) {
+      int32_t Dc = depth[order[s]], n = 1;
+      while (s + n < T) {
+        const int32_t Dn = std::max(Dc, depth[order[s + n]]);
+        if (chunk_bytes(n + 1, Dn) > budget) break;
+        Dc = Dn;
+        ++n;
+      }
+      runs.push_back({s, n, Dc});
+      s += n;
+    }
+    bal.clear();
+    for (size_t i = 0; i < runs.size();) {
+      size_t j = i;
+      int32_t total = 0;
+      while (j < runs.size() && runs[j].D == runs[i].D) total += runs[j++].n;
+      const int32_t nc = (int32_t)(j - i);
+      int32_t st = runs[i].start;
+      for (int32_t c = 0; c < nc; ++c) {
+        const int32_t n = total / nc + (c < total % nc ? 1 : 0);
+        bal.push_back({st, n, runs[i].D});
+        st += n;
+      }
+      i = j;
+    }
+    if ((int32_t)bal.size() == n_prev || (int32_t)bal.size() < n_prev) break;
+    n_prev = (int32_t)bal.size();
+  }
+  out->chunk_budget = budget;
+  out->chunks.clear();
+  out->data.clear();
+  out->slot_tree.assign(T, 0);
+  out->slot_leafid_off.assign(T, 0);
+  out->leaf_ids.clear();
+  PaddedTree pt;
+  int64_t off = 0;
+  for (const Run& r : bal) {
+    const int32_t D = r.D, I = (1 << D) - 1, L = 1 << D;
+    TravChunk c{};
+    c.offset = off;
+    c.n_trees = r.n;
+    c.depth = D;
+    c.first_slot = r.start;
+    const int64_t nodes = (int64_t)r.n * I * 8;
+    c.leaf_offset = (int32_t)((nodes + 15) / 16 * 16);
+    c.bytes = (int32_t)chunk_bytes(r.n, D);
+    out->data.resize(off + c.bytes, 0);
+    uint8_t* base = out->data.data() + off;
+    for (int32_t j = 0; j < r.n; ++j) {
+      const int32_t t = order[r.start + j];
+      pad_tree(d, t, D, &pt);
+      uint32_t* nd = reinterpret_cast<uint32_t*>(base) + (size_t)j * I * 2;
+      for (int32_t i = 0; i < I; ++i) {
+        uint32_t tb;
+        std::memcpy(&tb, &pt.threshold[i], 4);
+        nd[2 * i] = tb;
+        nd[2 * i + 1] = (uint32_t)pt.feature[i] | ((uint32_t)pt.missing[i] << 31);
+      }
+      float* lv = reinterpret_cast<float*>(base + c.leaf_offset) + (size_t)j * L * K;
+      for (int32_t l = 0; l < L * K; ++l) {
+        const float v = pt.leaf_value[l];
+        lv[l] = acc_int ? std::ldexp(v, -ex.q) : v;  // exact: integer-valued float < 2^63
+      }
+      out->slot_tree[r.start + j] = t;
+      out->slot_leafid_off[r.start + j] = (int64_t)out->leaf_ids.size();
+      out->leaf_ids.insert(out->leaf_ids.end(), pt.leaf_id.begin(), pt.leaf_id.end());
+    }
+    out->chunks.push_back(c);
+    off += (c.bytes + 127) / 128 * 128;
+    out->data.resize(off, 0);
+  }
+  int32_t maxc = 0;
+  for (auto& c : out->chunks) maxc = std::max(maxc, c.bytes);
+  out->smem_bytes = maxc + nw * xw + misc;
+  return true;
+}
+
+}  // namespace bridger

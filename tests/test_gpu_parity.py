@@ -1,0 +1,168 @@
+"""CUDA path vs the oracle, element by element, through the C ABI.
+
+Bar (BASELINE.json north_star): labels and leaf indices bit-exact; scores and
+probabilities bit-exact under exactness tier E53 (reading c9), else rtol 1e-5;
+sigmoid probabilities rtol 1e-5 (reading c10).  Sizes span many 32-row blocks,
+several tree chunks and a ragged tail; the full-size C2 run (bench launch
+configuration) is checked on a seeded row sample the oracle computes one by one.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from synth import gen_x, gen_x_torch, inject_specials, make_config, perfect_ensemble, prune_ensemble
+from synth.trees import ModelDesc
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+import paper_2405_12491_b200 as B  # noqa: E402
+
+
+def dev(X):
+    return torch.from_numpy(np.ascontiguousarray(X)).cuda()
+
+
+def check(m, X, variant=None, exact=True, apply=True):
+    g = B.Model(m, variant=variant)
+    o = oracle.run(m, X)
+    Xd = dev(X)
+    torch.cuda.synchronize()
+    if m.task == 1:
+        lab = g.predict(Xd).cpu().numpy()
+        np.testing.assert_array_equal(lab, o["label"])
+        pr = g.predict_proba(Xd).cpu().numpy()
+        if exact and m.post == 0:
+            np.testing.assert_array_equal(pr, o["proba"])
+        else:
+            np.testing.assert_allclose(pr, o["proba"], rtol=1e-5, atol=1e-7)
+    else:
+        pred = g.predict(Xd).cpu().numpy()
+        if exact:
+            np.testing.assert_array_equal(pred, o["pred"])
+        else:
+            np.testing.assert_allclose(pred, o["pred"], rtol=1e-5, atol=1e-6)
+    if apply:
+        np.testing.assert_array_equal(g.apply(Xd).cpu().numpy(), o["leaf"])
+    info = g.info()
+    raw = g.predict_raw(Xd).cpu().numpy()
+    a = raw.astype(np.float64) * 2.0 ** info["acc_scale_exp"] if info["acc_is_int64"] else raw
+    if exact:
+        np.testing.assert_array_equal(a, o["acc"])
+    else:
+        np.testing.assert_allclose(a, o["acc"], rtol=1e-9, atol=1e-12)
+    return g, o
+
+
+def test_c1_iris_decision_tree():
+    c, m = make_config("C1")
+    from synth import iris_like_x
+    check(m, iris_like_x(1))
+
+
+@pytest.mark.parametrize("n_rows", [1, 31, 33, 20011])
+def test_c2_random_forest_rows(n_rows):
+    c, m = make_config("C2")
+    check(m, gen_x(2, 0, n_rows, 28), apply=n_rows < 5000)
+
+
+def test_c3_gbdt_regression():
+    c, m = make_config("C3")
+    check(m, gen_x(3, 0, 30011, 90))
+
+
+def test_c5_shaped_deep_wide():
+    c, m = make_config("C5", n_trees=24)
+    check(m, gen_x(5, 0, 3001, 200))
+
+
+@pytest.mark.parametrize("ml", [False, True])
+def test_pruned_trees_specials_missing(ml):
+    m = perfect_ensemble(7, 70, 7, 13, kind="classification", n_classes=5, calib_rows=1024)
+    m = prune_ensemble(m, 7, p=0.15, with_missing=ml)
+    X = inject_specials(gen_x(8, 0, 5003, 13), 8, rate=0.02)
+    check(m, X)
+
+
+def test_binary_gbdt_sigmoid():
+    m = perfect_ensemble(9, 150, 6, 17, kind="regression", lr=0.1)
+    m.task, m.post = 1, 1
+    check(m, gen_x(10, 0, 4099, 17), exact=False)
+
+
+def test_f64_tier_tolerance():
+    m = perfect_ensemble(11, 40, 5, 9, kind="regression", lr=0.1)
+    v = m.value.copy()
+    v[np.nonzero(m.left == -1)[0][0]] = np.float32(1.4e-45)      # subnormal leaf -> q = -149 -> F64 tier
+    m = ModelDesc(**{**m.__dict__, "value": v})
+    assert B.analyze_exactness(m)[1] == "F64"
+    check(m, gen_x(12, 0, 2000, 9), exact=False)
+
+
+def test_zero_rows_and_shape_errors():
+    c, m = make_config("C2", n_trees=10)
+    g = B.Model(m)
+    out = g.predict(torch.empty((0, 28), device="cuda"))
+    assert out.shape == (0,)
+    bad = torch.zeros((4, 27), device="cuda")
+    out4 = torch.zeros(4, dtype=torch.int32, device="cuda")
+    with pytest.raises(B.BridgerError) as ei:
+        B._check(B.lib().bridger_predict(g._h, bad.data_ptr(), 4, 27, out4.data_ptr(), None))
+    assert ei.value.status == B.E_SHAPE
+    c3, r = make_config("C3", n_trees=5)
+    with pytest.raises(B.BridgerError):
+        B.Model(r).predict_proba(torch.zeros((4, 90), device="cuda"))
+
+
+def test_predict_host_matches_device():
+    c, m = make_config("C2", n_trees=30)
+    X = gen_x(2, 0, 70001, 28)
+    g = B.Model(m)
+    a = g.predict(dev(X)).cpu().numpy()
+    b = g.predict_host(torch.from_numpy(X).pin_memory()).numpy()
+    np.testing.assert_array_equal(a, b)
+    p = g.predict_host(X, proba=True).numpy()
+    np.testing.assert_array_equal(p, g.predict_proba(dev(X)).cpu().numpy())
+
+
+def test_tree_shards_add_exactly():
+    """raw(A) + raw(B) finalised == predict(A u B), bitwise (reading c9, tree sharding)."""
+    c, m = make_config("C3", n_trees=120)
+    q, tier, _ = B.analyze_exactness(m)
+    tiers = {"E53": 0, "E63": 1, "F64": 2}
+    X = dev(gen_x(3, 0, 9001, 90))
+    full = B.Model(m).predict(X)
+    ga = B.Model(m.subset(range(0, 50)), force_fixed_point=(q, tiers[tier]))
+    gb = B.Model(m.subset(range(50, 120)), force_fixed_point=(q, tiers[tier]))
+    acc = ga.predict_raw(X) + gb.predict_raw(X)
+    out = ga.finalize(acc, total_trees=120)
+    assert torch.equal(out, full)
+
+
+def test_c2_full_size_sampled():
+    """BASELINE configs[1] at full size in the bench launch configuration;
+    a seeded sample of rows is checked against the oracle row by row."""
+    c, m = make_config("C2")
+    Xd = gen_x_torch(2, 0, c.n_rows, c.n_features, device="cuda")
+    g = B.Model(m)
+    lab = g.predict(Xd).cpu().numpy()
+    pr = g.predict_proba(Xd).cpu().numpy()
+    rows = np.sort(np.random.default_rng(0).choice(c.n_rows, 4096, replace=False))
+    rows = np.unique(np.concatenate([rows, [0, 31, 32, c.n_rows - 1]]))
+    X = np.concatenate([gen_x(2, int(r), 1, 28) for r in rows])
+    o = oracle.run(m, X)
+    np.testing.assert_array_equal(lab[rows], o["label"])
+    np.testing.assert_array_equal(pr[rows], o["proba"])
+
+
+@pytest.mark.parametrize("n_trees", [40, 150, 270, 300])
+def test_chunk_counts_cluster_and_partial_paths(n_trees):
+    """2..8 chunks -> one cluster launch with the DSMEM reduction; >8 chunks ->
+    per-chunk partials + combine kernel.  Both must match the oracle bitwise."""
+    m = perfect_ensemble(13, n_trees, 8, 28, kind="classification", n_classes=2, calib_rows=1024)
+    check(m, gen_x(14, 0, 7001, 28), apply=False)
+
+
+def test_many_deep_chunks_regression():
+    m = perfect_ensemble(15, 150, 10, 20, kind="regression", lr=0.01, calib_rows=2048)
+    check(m, gen_x(16, 0, 3001, 20), apply=False)

@@ -67,7 +67,9 @@ struct TravChunk {
 };
 
 struct TravLayout {
-  int32_t n_warps = 8;          // warps per CTA (each owns a 32-row X block)
+  int32_t n_warps = 16;         // warps per CTA
+  int32_t group = 2;            // warps sharing one 32-row X block (they split the chunk's trees)
+  bool use_cluster = false;     // cross-chunk reduction over DSMEM (else global partials)
   int32_t smem_bytes = 0;       // dynamic shared memory per CTA
   int32_t chunk_budget = 0;     // max bytes of one chunk
   bool has_missing = false;
@@ -78,9 +80,13 @@ struct TravLayout {
   std::vector<int32_t> leaf_ids;    // concatenated [L] per slot (original ids)
 };
 
-// DSMEM reduction slots of the cluster mode: [NW][2][n_chunks-1][32 rows][K] x 8 B
-inline int32_t trav_slot_bytes(int32_t n_warps, int32_t n_chunks, int32_t K) {
-  return (n_chunks >= 2 && n_chunks <= 8) ? n_warps * 2 * (n_chunks - 1) * 32 * K * 8 : 0;
+// Shared-memory carve-up of the traversal kernel after the chunk:
+//   [NB row blocks x (feature-major X + staging) = NB*256*F][mbarriers]
+//   [intra-group partials NB*(G-1)*32*K*8][cluster DSMEM slots NB*2*(nC-1)*32*K*8]
+inline int32_t trav_bar_bytes(int32_t nb) { return ((1 + 5 * nb) * 8 + 15) / 16 * 16; }
+inline int32_t trav_red_bytes(int32_t nb, int32_t g, int32_t K) { return nb * (g - 1) * 32 * K * 8; }
+inline int32_t trav_slot_bytes(int32_t nb, int32_t n_chunks, int32_t K) {
+  return (n_chunks >= 2 && n_chunks <= 8) ? nb * 2 * (n_chunks - 1) * 32 * K * 8 : 0;
 }
 
 // Builds the resident-chunk layout; returns false (with reason) when a single

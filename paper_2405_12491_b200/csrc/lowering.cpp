@@ -8,6 +8,7 @@
 // exact gather that replaces a one-hot feature-selection matmul.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -213,13 +214,23 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
                        const Exactness& ex, bool acc_int, TravLayout* out, std::string* why) {
   const int32_t T = d->n_trees, F = d->n_features, K = d->n_outputs;
   out->has_missing = d->missing_left != nullptr;
-  // per-warp X blocks: feature-major working block + dense staging block, 32 rows each
+  // 16 warps per CTA; NB row blocks of 32 rows (feature-major X + staging,
+  // 256*F bytes each) with G = 16/NB warps per block splitting the chunk's
+  // trees.  NB is the largest power of two whose X blocks fit in 120 KB
+  // (measured on B200: C2 best at NB=16/G=1, C3 at NB=4/G=4).
   const int32_t xw = 2 * 32 * F * 4;
-  int32_t nw = 8;
-  while (nw > 1 && nw * xw > 96 * 1024) --nw;
-  const int32_t misc = 1024 + ((1 + 5 * nw) * 8 + 15) / 16 * 16;
-  const int32_t base_budget = kSmemMax - misc - nw * xw;
+  int32_t nw = 16, nb = 16;
+  while (nb > 1 && nb * xw > 120 * 1024) nb /= 2;
+  if (const char* e = std::getenv("BRIDGER_WARPS")) nw = std::max(1, std::min(16, std::atoi(e)));  // experiments
+  if (const char* e = std::getenv("BRIDGER_BLOCKS")) nb = std::max(1, std::min(16, std::atoi(e)));
+  nb = std::min(nb, nw);
+  while (nw % nb) --nb;
+  const int32_t G = nw / nb;
+  out->use_cluster = std::getenv("BRIDGER_CLUSTER") != nullptr;
+  const int32_t misc = 1024 + trav_bar_bytes(nb) + trav_red_bytes(nb, G, K);
+  const int32_t base_budget = kSmemMax - misc - nb * xw;
   out->n_warps = nw;
+  out->group = G;
   auto tree_bytes = [&](int32_t D) -> int64_t {
     return (int64_t)((1 << D) - 1) * 8 + (int64_t)(1 << D) * K * 4;
   };
@@ -239,7 +250,7 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
   std::vector<Run> bal;
   int32_t budget = base_budget, n_prev = 1;
   for (int iter = 0; iter < 4; ++iter) {
-    budget = base_budget - trav_slot_bytes(nw, n_prev, K);
+    budget = base_budget - (out->use_cluster ? trav_slot_bytes(nb, n_prev, K) : 0);
     if (chunk_bytes(1, Dmax) > budget) {
       if (why) *why = "one tree of depth " + std::to_string(Dmax) + " (" + std::to_string(tree_bytes(Dmax)) +
                       " B) exceeds the shared-memory chunk budget " + std::to_string(budget);
@@ -320,7 +331,7 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
   }
   int32_t maxc = 0;
   for (auto& c : out->chunks) maxc = std::max(maxc, c.bytes);
-  out->smem_bytes = maxc + nw * xw + misc;
+  out->smem_bytes = maxc + nb * xw + misc;
   return true;
 }
 

@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "bridger_internal.h"
 #include "finalize.cuh"
@@ -59,6 +60,8 @@ struct TravParams {
   const int64_t* slot_leafid_off;
   const int32_t* leaf_ids;
   int32_t T;
+  int32_t group;      // warps sharing one 32-row block (tree split)
+  int32_t red_off;    // byte offset of the intra-group partials
   int32_t slot_off;   // byte offset of the DSMEM reduction slots (TRAV_CLUSTER)
   FinalizeArgs fin;   // (TRAV_FINAL, TRAV_CLUSTER)
 };
@@ -114,6 +117,25 @@ __device__ __forceinline__ void walk_trees(const TravParams& p, const TravChunk&
     }
     return;
   }
+  if (KT == K && (KT == 2 || KT == 4)) {
+    // K == KT: one vector load per tree (8/16-byte aligned leaf records)
+#pragma unroll
+    for (int u = 0; u < NI; ++u) {
+      const float* e = leaves + ((size_t)(j + u) * L + (idx[u] - I)) * KT;
+      if (KT == 2) {
+        const float2 v = *reinterpret_cast<const float2*>(e);
+        acc[0] += leaf_to_acc<ACC>(v.x);
+        acc[KT > 1 ? 1 : 0] += leaf_to_acc<ACC>(v.y);
+      } else {
+        const float4 v = *reinterpret_cast<const float4*>(e);
+        acc[0] += leaf_to_acc<ACC>(v.x);
+        acc[KT > 1 ? 1 : 0] += leaf_to_acc<ACC>(v.y);
+        acc[KT > 2 ? 2 : 0] += leaf_to_acc<ACC>(v.z);
+        acc[KT > 3 ? 3 : 0] += leaf_to_acc<ACC>(v.w);
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int u = 0; u < NI; ++u) {
     const float* e = leaves + ((size_t)(j + u) * L + (idx[u] - I)) * K;
@@ -123,31 +145,59 @@ __device__ __forceinline__ void walk_trees(const TravParams& p, const TravChunk&
   }
 }
 
+// one pass over r (<= 12) trees with ILP = r
+template <int KT, typename ACC, bool ML, int MAXNI>
+__device__ __forceinline__ void walk_tail(int r, const TravParams& p, const TravChunk& c, const uint2* nodes,
+                                          const float* leaves, const float* xl, int j, int I, int L, int D, int K,
+                                          int64_t row, ACC (&acc)[KT]) {
+  switch (r) {
+#define BRIDGER_TAIL(N) \
+  case N: if (N <= MAXNI) walk_trees<(N <= MAXNI ? N : 1), KT, ACC, ML>(p, c, nodes, leaves, xl, j, I, L, D, K, row, acc); break;
+    BRIDGER_TAIL(1) BRIDGER_TAIL(2) BRIDGER_TAIL(3) BRIDGER_TAIL(4) BRIDGER_TAIL(5) BRIDGER_TAIL(6)
+    BRIDGER_TAIL(7) BRIDGER_TAIL(8) BRIDGER_TAIL(9) BRIDGER_TAIL(10) BRIDGER_TAIL(11) BRIDGER_TAIL(12)
+#undef BRIDGER_TAIL
+    default: break;
+  }
+}
+
+// Barrier among the G warps that share one row block (named barrier 1+group).
+__device__ __forceinline__ void group_sync(int group, int G) {
+  if (G == 1) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + group), "r"(G * 32) : "memory");
+  }
+}
+
 template <int KT, typename ACC, bool ML>
-__global__ void __launch_bounds__(256, 1) trav_kernel(const TravParams p) {
+__global__ void __launch_bounds__(512, 1) trav_kernel(const TravParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
+  const int G = p.group, NB = NW / G;          // G warps share each of NB row blocks
+  const int grp = warp / G, gw = warp % G;     // row-block group, warp within the group
   const int chunk_id = blockIdx.x % p.n_chunks;
   const int cta_in_chunk = blockIdx.x / p.n_chunks;
   const TravChunk c = p.chunks[chunk_id];
   const int F = p.F;
+  const int K = p.K;
 
   uint8_t* cdata = smem;
-  float* Xs = reinterpret_cast<float*>(smem + p.chunk_cap) + (size_t)warp * 64 * F;  // [F][32]
-  float* St = Xs + 32 * F;                                                           // [32][F]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.chunk_cap + (size_t)NW * 256 * F);
+  float* Xs = reinterpret_cast<float*>(smem + p.chunk_cap) + (size_t)grp * 64 * F;  // [F][32]
+  float* St = Xs + 32 * F;                                                          // [32][F]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.chunk_cap + (size_t)NB * 256 * F);
+  uint64_t* red = reinterpret_cast<uint64_t*>(smem + p.red_off);  // [NB][G-1][32][K] intra-group partials
 
   const bool clustered = p.mode == TRAV_CLUSTER;
   const int nC = p.n_chunks;
-  uint64_t* full_bar = bars + 1 + NW;        // [NW][2] (leader): peers' partials landed
-  uint64_t* empty_bar = bars + 1 + 3 * NW;   // [NW][2] (peers): leader consumed the slot
+  uint64_t* full_bar = bars + 1 + NB;        // [NB][2] (leader): peers' partials landed
+  uint64_t* empty_bar = bars + 1 + 3 * NB;   // [NB][2] (peers): leader consumed the slot
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bars[0], 1);
-    for (int w = 0; w < NW; ++w) ptx::mbar_init(&bars[1 + w], 1);
+    for (int b = 0; b < NB; ++b) ptx::mbar_init(&bars[1 + b], 1);
     if (clustered)
-      for (int w = 0; w < 2 * NW; ++w) {
-        ptx::mbar_init(&full_bar[w], 32 * (nC - 1));
-        ptx::mbar_init(&empty_bar[w], 32);
+      for (int b = 0; b < 2 * NB; ++b) {
+        ptx::mbar_init(&full_bar[b], 32 * (nC - 1));
+        ptx::mbar_init(&empty_bar[b], 32);
       }
     ptx::fence_barrier_init();
     ptx::fence_proxy_async();
@@ -165,60 +215,74 @@ __global__ void __launch_bounds__(256, 1) trav_kernel(const TravParams p) {
 
   const int64_t n_rows = p.n_rows;
   const int64_t n_blocks = (n_rows + 31) / 32;
-  const int64_t stride = (int64_t)p.cpc * NW;
-  int64_t blk = (int64_t)cta_in_chunk * NW + warp;
-  uint64_t* wbar = &bars[1 + warp];
-  uint32_t wphase = 0;
+  const int64_t stride = (int64_t)p.cpc * NB;
+  int64_t blk = (int64_t)cta_in_chunk * NB + grp;
+  uint64_t* sbar = &bars[1 + grp];
+  uint32_t sphase = 0;
   const uint32_t block_bytes = 32u * (uint32_t)F * 4u;
-  const int lane_mod_F = lane % F;
 
-  auto issue = [&](int64_t b) {
-    if (b < n_blocks && (b + 1) * 32 <= n_rows && lane == 0) {
+  auto issue = [&](int64_t b) {  // warp 0 of the group, lane 0: next block -> staging
+    if (gw == 0 && lane == 0 && b < n_blocks && (b + 1) * 32 <= n_rows) {
       ptx::fence_proxy_async();
-      ptx::mbar_arrive_expect_tx(wbar, block_bytes);
-      ptx::bulk_g2s(St, p.X + b * 32 * (int64_t)F, block_bytes, wbar);
+      ptx::mbar_arrive_expect_tx(sbar, block_bytes);
+      ptx::bulk_g2s(St, p.X + b * 32 * (int64_t)F, block_bytes, sbar);
     }
   };
   issue(blk);
-
   ptx::mbar_wait(&bars[0], 0);  // chunk resident
 
   const int D = c.depth;
   const int I = (1 << D) - 1, L = 1 << D;
-  const int K = p.K;
-  const int nt = c.n_trees;
   const uint2* nodes = reinterpret_cast<const uint2*>(cdata);
   const float* leaves = reinterpret_cast<const float*>(cdata + c.leaf_offset);
   const float* xl = Xs + lane;
-  uint64_t* slots = reinterpret_cast<uint64_t*>(smem + p.slot_off);  // [NW][2][nC-1][32][K]
+  // this warp's share of the chunk's trees
+  const int t0 = (int)((int64_t)c.n_trees * gw / G), t1 = (int)((int64_t)c.n_trees * (gw + 1) / G);
+  const int nt = t1 - t0;
+  // feature share of the transpose
+  const int f_lo = F * gw / G, f_hi = F * (gw + 1) / G;
+  uint64_t* slots = reinterpret_cast<uint64_t*>(smem + p.slot_off);  // [NB][2][nC-1][32][K]
   uint32_t it = 0;
 
   while (blk < n_blocks) {
     const int64_t row0 = blk * 32;
     const bool full = row0 + 32 <= n_rows;
     if (full) {
-      ptx::mbar_wait(wbar, wphase);
-      wphase ^= 1;
+      ptx::mbar_wait(sbar, sphase);
+      sphase ^= 1;
     } else {
       const int rows = (int)(n_rows - row0);
       const float* src = p.X + row0 * F;
-      for (int e = lane; e < rows * F; e += 32) St[e] = src[e];
-      __syncwarp();
+      if (gw == 0)
+        for (int e = lane; e < rows * F; e += 32) St[e] = src[e];
+      group_sync(grp, G);
     }
-    // transpose staging [32][F] -> feature-major [F][32].  Lane l walks the
-    // features of row l starting at (l mod F) and wrapping, so one staging read
-    // instruction touches 32 different (row, feature) words spread over the
-    // banks; every write hits bank `lane`.
-    {
+    // transpose staging [32][F] -> feature-major [F][32] (features split over
+    // the group's warps).  Every write hits bank `lane`; reads of row `lane`
+    // start at a lane-dependent feature so one instruction spreads over banks.
+    if ((F & 3) == 0 && G == 1) {
+      const float4* srow = reinterpret_cast<const float4*>(St + lane * F);
+#pragma unroll 2
+      for (int f4 = 0; f4 < F / 4; ++f4) {
+        const float4 v = srow[f4];
+        Xs[(4 * f4 + 0) * 32 + lane] = v.x;
+        Xs[(4 * f4 + 1) * 32 + lane] = v.y;
+        Xs[(4 * f4 + 2) * 32 + lane] = v.z;
+        Xs[(4 * f4 + 3) * 32 + lane] = v.w;
+      }
+    } else {
       const float* srow = St + lane * F;
-      int f = lane_mod_F;
+      const int span = f_hi - f_lo;
+      if (span > 0) {
+        int f = f_lo + lane % span;
 #pragma unroll 4
-      for (int f0 = 0; f0 < F; ++f0) {
-        Xs[f * 32 + lane] = srow[f];
-        f = (f + 1 == F) ? 0 : f + 1;
+        for (int f0 = 0; f0 < span; ++f0) {
+          Xs[f * 32 + lane] = srow[f];
+          f = (f + 1 == f_hi) ? f_lo : f + 1;
+        }
       }
     }
-    __syncwarp();
+    group_sync(grp, G);  // Xs ready, staging free
     const int64_t next = blk + stride;
     issue(next);
 
@@ -227,46 +291,78 @@ __global__ void __launch_bounds__(256, 1) trav_kernel(const TravParams p) {
 #pragma unroll
     for (int k = 0; k < KT; ++k) acc[k] = ACC(0);
 
-    int j = 0;
-    for (; j + 8 <= nt; j += 8) walk_trees<8, KT, ACC, ML>(p, c, nodes, leaves, xl, j, I, L, D, K, row, acc);
-    for (; j + 4 <= nt; j += 4) walk_trees<4, KT, ACC, ML>(p, c, nodes, leaves, xl, j, I, L, D, K, row, acc);
-    for (; j < nt; ++j) walk_trees<1, KT, ACC, ML>(p, c, nodes, leaves, xl, j, I, L, D, K, row, acc);
+    // ceil(nt / NI_MAX) passes of (nearly) equal size: each pass walks its
+    // trees as independent dependency chains (ILP); a pass costs about the same
+    // latency whatever its width, so the pass count is what matters.  Full ILP
+    // range for the common int64 / no-missing / K <= 8 kernels, passes of <= 4
+    // for the rare variants (compile time).
+    {
+      constexpr int NI_MAX = (!ML && KT <= 8 && !std::is_same<ACC, double>::value) ? 12 : 4;
+      const int n_pass = (nt + NI_MAX - 1) / NI_MAX;
+      int j = t0;
+      for (int q = 0; q < n_pass; ++q) {
+        const int sz = nt / n_pass + (q < nt % n_pass ? 1 : 0);
+        walk_tail<KT, ACC, ML, NI_MAX>(sz, p, c, nodes, leaves, xl, j, I, L, D, K, row, acc);
+        j += sz;
+      }
+    }
 
-    if (clustered) {
-      const int s = it & 1;
-      const uint32_t ph = (it >> 1) & 1;
-      ++it;
-      uint64_t* slot = slots + (size_t)(warp * 2 + s) * (nC - 1) * 32 * K;
-      if (chunk_id != 0) {
-        ptx::mbar_wait_cluster(&empty_bar[warp * 2 + s], ph ^ 1);
-        const uint32_t dst = ptx::mapa(ptx::s2u(slot + ((size_t)(chunk_id - 1) * 32 + lane) * K), 0);
+    if (p.mode != TRAV_APPLY) {
+      // combine the group's warps (exact int64 / fixed order)
+      uint64_t* gred = red + (size_t)grp * (G - 1) * 32 * K;
+      if (gw > 0) {
+        uint64_t* dst = gred + ((size_t)(gw - 1) * 32 + lane) * K;
 #pragma unroll
         for (int k = 0; k < KT; ++k)
-          if (k < K) ptx::st_cluster_u64(dst + 8 * k, reinterpret_cast<const uint64_t&>(acc[k]));
-        ptx::mbar_arrive_remote(ptx::mapa(ptx::s2u(&full_bar[warp * 2 + s]), 0));
-      } else {
-        ptx::mbar_wait_cluster(&full_bar[warp * 2 + s], ph);
-        for (int q = 0; q < nC - 1; ++q) {
-          const uint64_t* src = slot + ((size_t)q * 32 + lane) * K;
+          if (k < K) dst[k] = reinterpret_cast<const uint64_t&>(acc[k]);
+      }
+      group_sync(grp, G);
+      if (gw == 0) {
+        for (int q = 0; q < G - 1; ++q) {
+          const uint64_t* src = gred + ((size_t)q * 32 + lane) * K;
 #pragma unroll
           for (int k = 0; k < KT; ++k)
             if (k < K) acc[k] += reinterpret_cast<const ACC&>(src[k]);
         }
-        for (int q = 1; q < nC; ++q) ptx::mbar_arrive_remote(ptx::mapa(ptx::s2u(&empty_bar[warp * 2 + s]), q));
-        if (row < n_rows) finalize_row<KT, ACC>(p.fin, row, acc);
-      }
-    } else if (row < n_rows) {
-      if (p.mode == TRAV_PARTIAL) {
-        ACC* o = static_cast<ACC*>(p.partial) + ((size_t)chunk_id * n_rows + row) * K;
+        if (clustered) {
+          const int s = it & 1;
+          const uint32_t ph = (it >> 1) & 1;
+          ++it;
+          uint64_t* slot = slots + (size_t)(grp * 2 + s) * (nC - 1) * 32 * K;
+          if (chunk_id != 0) {
+            ptx::mbar_wait_cluster(&empty_bar[grp * 2 + s], ph ^ 1);
+            const uint32_t dst = ptx::mapa(ptx::s2u(slot + ((size_t)(chunk_id - 1) * 32 + lane) * K), 0);
 #pragma unroll
-        for (int k = 0; k < KT; ++k)
-          if (k < K) o[k] = acc[k];
-      } else if (p.mode == TRAV_FINAL) {
-        finalize_row<KT, ACC>(p.fin, row, acc);
+            for (int k = 0; k < KT; ++k)
+              if (k < K) ptx::st_cluster_u64(dst + 8 * k, reinterpret_cast<const uint64_t&>(acc[k]));
+            ptx::mbar_arrive_remote(ptx::mapa(ptx::s2u(&full_bar[grp * 2 + s]), 0));
+          } else {
+            ptx::mbar_wait_cluster(&full_bar[grp * 2 + s], ph);
+            for (int q = 0; q < nC - 1; ++q) {
+              const uint64_t* src = slot + ((size_t)q * 32 + lane) * K;
+#pragma unroll
+              for (int k = 0; k < KT; ++k)
+                if (k < K) acc[k] += reinterpret_cast<const ACC&>(src[k]);
+            }
+            for (int q = 1; q < nC; ++q)
+              ptx::mbar_arrive_remote(ptx::mapa(ptx::s2u(&empty_bar[grp * 2 + s]), q));
+            if (row < n_rows) finalize_row<KT, ACC>(p.fin, row, acc);
+          }
+        } else if (row < n_rows) {
+          if (p.mode == TRAV_PARTIAL) {
+            ACC* o = static_cast<ACC*>(p.partial) + ((size_t)chunk_id * n_rows + row) * K;
+#pragma unroll
+            for (int k = 0; k < KT; ++k)
+              if (k < K) o[k] = acc[k];
+          } else {
+            finalize_row<KT, ACC>(p.fin, row, acc);
+          }
+        }
       }
+    } else {
+      group_sync(grp, G);  // keep the group's barrier sequence uniform
     }
     blk = next;
-    __syncwarp();
   }
   if (clustered) ptx::cluster_sync();  // no CTA leaves while peers may touch its shared memory
 }
@@ -327,8 +423,13 @@ static cudaError_t launch_trav_t(const TravParams& p, int grid_ctas, int block, 
     cfg.gridDim = dim3(cluster);
     int max_clusters = 0;
     e = cudaOccupancyMaxActiveClusters(&max_clusters, (void*)kern, &cfg);
-    if (e != cudaSuccess) return e;
-    if (max_clusters < 1) return cudaErrorNotSupported;  // caller falls back to partials
+    if (std::getenv("BRIDGER_DEBUG"))
+      std::fprintf(stderr, "[bridger] cluster=%d smem=%d max_active_clusters=%d (%s)\n", cluster, smem,
+                   max_clusters, cudaGetErrorString(e));
+    if (e != cudaSuccess || max_clusters < 1) {
+      cudaGetLastError();
+      return cudaErrorNotSupported;  // caller falls back to partials
+    }
     grid = std::min(grid_ctas, max_clusters * cluster);
     grid = std::max(cluster, grid / cluster * cluster);
   }
@@ -381,10 +482,11 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
   fin.base = m->d_base;
   fin.out = out;
   p.fin = fin;
-  const int NW = L.n_warps;
+  const int NW = L.n_warps, G = L.group, NB = NW / G;
   const int block = NW * 32;
-  const int bars_bytes = ((1 + 5 * NW) * 8 + 15) / 16 * 16;
-  p.slot_off = p.chunk_cap + NW * 256 * m->F + bars_bytes;
+  p.group = G;
+  p.red_off = p.chunk_cap + NB * 256 * m->F + trav_bar_bytes(NB);
+  p.slot_off = p.red_off + trav_red_bytes(NB, G, m->K);
   int smem = p.slot_off;
   int cluster = 1;
   void* partial = nullptr;
@@ -393,10 +495,10 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
     p.out_leaf = static_cast<int32_t*>(out);
   } else if (n_chunks == 1) {
     p.mode = TRAV_FINAL;
-  } else if (n_chunks <= 8) {
+  } else if (L.use_cluster && n_chunks <= 8 && smem + trav_slot_bytes(NB, n_chunks, m->K) <= 232448) {
     p.mode = TRAV_CLUSTER;
     cluster = n_chunks;
-    smem += trav_slot_bytes(NW, n_chunks, m->K);
+    smem += trav_slot_bytes(NB, n_chunks, m->K);
   } else {
     p.mode = TRAV_PARTIAL;
     cudaError_t e = cudaMallocAsync(&partial, (size_t)n_chunks * n_rows * m->K * 8, st);
@@ -415,12 +517,13 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
                            : launch_trav_t<KT, double, false>(p, grid, block, smem, cluster, st);
     };
     err = launch();
-    if (err == cudaErrorNotSupported && p.mode == TRAV_CLUSTER) {
+    if (err != cudaSuccess && p.mode == TRAV_CLUSTER) {
       // clusters of this size cannot be co-resident at this shared-memory
       // footprint: fall back to per-chunk partials + combine
       cudaGetLastError();
       p.mode = TRAV_PARTIAL;
       cluster = 1;
+      smem = p.slot_off;
       err = cudaMallocAsync(&partial, (size_t)n_chunks * n_rows * m->K * 8, st);
       p.partial = partial;
       if (err == cudaSuccess) err = launch();

@@ -14,7 +14,8 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbridger.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["api.cu", "traverse.cu", "gemm_path.cu", "lowering.cpp"]
+SOURCES = ["api.cu", "traverse.cu", "trav_inst_i64.cu", "trav_inst_i64_ml.cu", "trav_inst_f64.cu",
+           "trav_inst_gt_i64.cu", "trav_inst_gt_f64.cu", "gemm_path.cu", "lowering.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-ftz=false", "-prec-div=true", "-prec-sqrt=true",
           "-fmad=true", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
@@ -34,7 +35,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
+    objs, cmds = [], []
     for s in SOURCES:
         src = os.path.join(CSRC, s)
         obj = os.path.join(objdir, s + ".o")
@@ -46,8 +47,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
                    "-I", os.path.join(HERE, "..", "include"), "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
-        subprocess.check_call(cmd)
+        cmds.append(cmd)
         objs.append(obj)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 4))) as ex:
+        for r in ex.map(lambda c: subprocess.run(c).returncode, cmds):
+            if r != 0:
+                raise subprocess.CalledProcessError(r, "nvcc")
     cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static"]
     subprocess.check_call(cmd)
     return LIB

@@ -70,6 +70,7 @@ struct TravLayout {
   int32_t n_warps = 16;         // warps per CTA
   int32_t group = 2;            // warps sharing one 32-row X block (they split the chunk's trees)
   bool use_cluster = false;     // cross-chunk reduction over DSMEM (else global partials)
+  bool global_trees = false;    // trees too large for shared memory: walked from global memory
   int32_t smem_bytes = 0;       // dynamic shared memory per CTA
   int32_t chunk_budget = 0;     // max bytes of one chunk
   bool has_missing = false;

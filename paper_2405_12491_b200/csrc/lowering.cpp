@@ -252,9 +252,14 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
   for (int iter = 0; iter < 4; ++iter) {
     budget = base_budget - (out->use_cluster ? trav_slot_bytes(nb, n_prev, K) : 0);
     if (chunk_bytes(1, Dmax) > budget) {
-      if (why) *why = "one tree of depth " + std::to_string(Dmax) + " (" + std::to_string(tree_bytes(Dmax)) +
-                      " B) exceeds the shared-memory chunk budget " + std::to_string(budget);
-      return false;
+      // global-tree mode: chunks are runs of equal depth of any size, read from
+      // global memory by every CTA (no shared-memory residency, no partials)
+      out->global_trees = true;
+      budget = INT32_MAX / 2;
+      if (chunk_bytes(T, Dmax) > (int64_t)1 << 40) {
+        if (why) *why = "model too large";
+        return false;
+      }
     }
     std::vector<Run> runs;
     int32_t s = 0;
@@ -262,7 +267,7 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
       int32_t Dc = depth[order[s]], n = 1;
       while (s + n < T) {
         const int32_t Dn = std::max(Dc, depth[order[s + n]]);
-        if (chunk_bytes(n + 1, Dn) > budget) break;
+        if (out->global_trees ? (Dn != Dc || chunk_bytes(n + 1, Dn) > (1 << 30)) : (chunk_bytes(n + 1, Dn) > budget)) break;
         Dc = Dn;
         ++n;
       }
@@ -283,7 +288,7 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
       }
       i = j;
     }
-    if ((int32_t)bal.size() == n_prev || (int32_t)bal.size() < n_prev) break;
+    if (out->global_trees || (int32_t)bal.size() == n_prev || (int32_t)bal.size() < n_prev) break;
     n_prev = (int32_t)bal.size();
   }
   out->chunk_budget = budget;

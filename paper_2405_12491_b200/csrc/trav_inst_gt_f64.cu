@@ -1,0 +1,7 @@
+// Explicit instantiations of the traversal kernel (see traverse.cuh).
+#include "traverse.cuh"
+
+namespace bridger {
+BRIDGER_TRAV_INSTANTIATE(double, false, true)
+BRIDGER_TRAV_INSTANTIATE(double, true, true)
+}  // namespace bridger

@@ -1,0 +1,7 @@
+// Explicit instantiations of the traversal kernel (see traverse.cuh).
+#include "traverse.cuh"
+
+namespace bridger {
+BRIDGER_TRAV_INSTANTIATE(long long, false, true)
+BRIDGER_TRAV_INSTANTIATE(long long, true, true)
+}  // namespace bridger

@@ -1,0 +1,6 @@
+// Explicit instantiations of the traversal kernel (see traverse.cuh).
+#include "traverse.cuh"
+
+namespace bridger {
+BRIDGER_TRAV_INSTANTIATE(long long, true, false)
+}  // namespace bridger

@@ -1,0 +1,463 @@
+#pragma once
+// Traversal kernel templates (K4); instantiated in trav_inst_*.cu.
+// K4 traversal kernel (step a4' + a5 + a6 [+ a7 fused]).
+//
+// The COR form of a tree executed as the SPEC.md:283 template:
+//   idx <- 0; repeat D: idx <- 2 idx + 1 + [not (X[r, feat[idx]] <= thr[idx])]
+//   leaf = idx - I;  acc += E[leaf]
+// on perfect, heap-ordered trees (lowering.cpp).  B200 mapping:
+//  * A chunk of trees (nodes {thr, feature} 8 B + leaf values) is copied ONCE
+//    into a CTA's shared memory by the TMA engine (cp.async.bulk) and stays
+//    resident; the grid is persistent, n_chunks x ctas_per_chunk ~= #SMs.
+//  * lane = row.  Each warp streams its own 32-row blocks of X: a bulk copy
+//    lands the dense [32][F] block in a staging buffer (double buffering: the
+//    next block is in flight while the current one is walked), then the warp
+//    transposes it to a feature-major [F][32] block, so x = Xs[f*32 + lane]
+//    hits bank `lane` for ANY per-lane feature: the data-dependent feature
+//    gather is bank-conflict free.  Node loads are broadcast at the top levels
+//    and random-but-narrow below.
+//  * Each thread walks 4 trees at once (ILP) and accumulates leaf values in
+//    int64 fixed point (exact, order-free; reading c9) or fp64.
+//  * One chunk: finalize fused (a7).  Several chunks: per-chunk partials
+//    [chunk][row][K], combined in chunk order by trav_combine_kernel.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <type_traits>
+
+#include "bridger_internal.h"
+#include "finalize.cuh"
+#include "ptx.cuh"
+
+namespace bridger {
+
+void count_launch();
+void hot_begin(cudaStream_t st, cudaEvent_t* ev);
+void hot_end(cudaStream_t st, cudaEvent_t start);
+
+// FINAL: one chunk, finalize fused.  PARTIAL: per-chunk partials to global.
+// APPLY: leaf ids.  CLUSTER: the n_chunks CTAs of a thread-block cluster hold
+// the n chunks of the model and walk the SAME row blocks; peers push their
+// per-row partial sums into the leader CTA's shared memory over DSMEM
+// (st.shared::cluster + remote mbarrier arrive), the leader adds them in rank
+// order and finalizes -- no global partials, no second kernel.
+enum TravMode : int32_t { TRAV_FINAL = 0, TRAV_PARTIAL = 1, TRAV_APPLY = 2, TRAV_CLUSTER = 3 };
+
+struct TravParams {
+  const float* X;
+  int64_t n_rows;
+  int32_t F;
+  int32_t K;
+  const uint8_t* data;
+  const TravChunk* chunks;
+  int32_t n_chunks;
+  int32_t n_chunks_grid;  // chunks the grid is split over (1 in global-tree mode)
+  int32_t cpc;        // CTAs per chunk
+  int32_t chunk_cap;  // bytes reserved for the chunk in shared memory
+  int32_t mode;
+  void* partial;      // [n_chunks][n_rows][K] ACC   (TRAV_PARTIAL)
+  int32_t* out_leaf;  // [n_rows][T]                 (TRAV_APPLY)
+  const int32_t* slot_tree;
+  const int64_t* slot_leafid_off;
+  const int32_t* leaf_ids;
+  int32_t T;
+  int32_t group;      // warps sharing one 32-row block (tree split)
+  int32_t red_off;    // byte offset of the intra-group partials
+  int32_t slot_off;   // byte offset of the DSMEM reduction slots (TRAV_CLUSTER)
+  FinalizeArgs fin;   // (TRAV_FINAL, TRAV_CLUSTER)
+};
+
+template <typename ACC>
+__device__ __forceinline__ ACC leaf_to_acc(float v);
+template <>
+__device__ __forceinline__ long long leaf_to_acc<long long>(float v) {
+  return __float2ll_rz(v);  // v is an integer-valued float (pre-scaled by 2^-q): exact
+}
+template <>
+__device__ __forceinline__ double leaf_to_acc<double>(float v) {
+  return (double)v;
+}
+
+template <bool ML>
+__device__ __forceinline__ int go_right(float x, uint2 nd) {
+  const float t = __uint_as_float(nd.x);
+  int r = !(x <= t);  // NaN -> right (reading c2 default)
+  if (ML) r &= !((nd.y >> 31) & isnan(x));
+  return r;
+}
+
+// Walk NI trees [j, j+NI) of the chunk for this thread's row (NI independent
+// dependency chains for ILP), then gather and accumulate their leaf values.
+template <int NI, int KT, typename ACC, bool ML>
+__device__ __forceinline__ void walk_trees(const TravParams& p, const TravChunk& c, const uint2* nodes,
+                                           const float* leaves, const float* xl, int j, int I, int L, int D,
+                                           int K, int64_t row, ACC (&acc)[KT]) {
+  constexpr uint32_t kFeatMask = ML ? 0x7fffffffu : 0xffffffffu;
+  int idx[NI];
+#pragma unroll
+  for (int u = 0; u < NI; ++u) idx[u] = 0;
+  const uint2* nb = nodes + (size_t)j * I;
+  for (int lvl = 0; lvl < D; ++lvl) {
+    uint2 a[NI];
+#pragma unroll
+    for (int u = 0; u < NI; ++u) a[u] = nb[u * I + idx[u]];
+    float x[NI];
+#pragma unroll
+    for (int u = 0; u < NI; ++u) x[u] = xl[(a[u].y & kFeatMask) * 32];
+#pragma unroll
+    for (int u = 0; u < NI; ++u) idx[u] = 2 * idx[u] + 1 + go_right<ML>(x[u], a[u]);
+  }
+  if (p.mode == TRAV_APPLY) {
+    if (row < p.n_rows) {
+      int32_t* o = p.out_leaf + row * p.T;
+#pragma unroll
+      for (int u = 0; u < NI; ++u) {
+        const int s = c.first_slot + j + u;
+        o[p.slot_tree[s]] = p.leaf_ids[p.slot_leafid_off[s] + idx[u] - I];
+      }
+    }
+    return;
+  }
+  if (KT == K && (KT == 2 || KT == 4)) {
+    // K == KT: one vector load per tree (8/16-byte aligned leaf records)
+#pragma unroll
+    for (int u = 0; u < NI; ++u) {
+      const float* e = leaves + ((size_t)(j + u) * L + (idx[u] - I)) * KT;
+      if (KT == 2) {
+        const float2 v = *reinterpret_cast<const float2*>(e);
+        acc[0] += leaf_to_acc<ACC>(v.x);
+        acc[KT > 1 ? 1 : 0] += leaf_to_acc<ACC>(v.y);
+      } else {
+        const float4 v = *reinterpret_cast<const float4*>(e);
+        acc[0] += leaf_to_acc<ACC>(v.x);
+        acc[KT > 1 ? 1 : 0] += leaf_to_acc<ACC>(v.y);
+        acc[KT > 2 ? 2 : 0] += leaf_to_acc<ACC>(v.z);
+        acc[KT > 3 ? 3 : 0] += leaf_to_acc<ACC>(v.w);
+      }
+    }
+    return;
+  }
+#pragma unroll
+  for (int u = 0; u < NI; ++u) {
+    const float* e = leaves + ((size_t)(j + u) * L + (idx[u] - I)) * K;
+#pragma unroll
+    for (int k = 0; k < KT; ++k)
+      if (k < K) acc[k] += leaf_to_acc<ACC>(e[k]);
+  }
+}
+
+// one pass over r (<= 12) trees with ILP = r
+template <int KT, typename ACC, bool ML, int MAXNI>
+__device__ __forceinline__ void walk_tail(int r, const TravParams& p, const TravChunk& c, const uint2* nodes,
+                                          const float* leaves, const float* xl, int j, int I, int L, int D, int K,
+                                          int64_t row, ACC (&acc)[KT]) {
+  switch (r) {
+#define BRIDGER_TAIL(N) \
+  case N: if (N <= MAXNI) walk_trees<(N <= MAXNI ? N : 1), KT, ACC, ML>(p, c, nodes, leaves, xl, j, I, L, D, K, row, acc); break;
+    BRIDGER_TAIL(1) BRIDGER_TAIL(2) BRIDGER_TAIL(3) BRIDGER_TAIL(4) BRIDGER_TAIL(5) BRIDGER_TAIL(6)
+    BRIDGER_TAIL(7) BRIDGER_TAIL(8) BRIDGER_TAIL(9) BRIDGER_TAIL(10) BRIDGER_TAIL(11) BRIDGER_TAIL(12)
+#undef BRIDGER_TAIL
+    default: break;
+  }
+}
+
+// Barrier among the G warps that share one row block (named barrier 1+group).
+__device__ __forceinline__ void group_sync(int group, int G) {
+  if (G == 1) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + group), "r"(G * 32) : "memory");
+  }
+}
+
+template <int KT, typename ACC, bool ML, bool GT>
+__global__ void __launch_bounds__(512, 1) trav_kernel(const TravParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
+  const int G = p.group, NB = NW / G;          // G warps share each of NB row blocks
+  const int grp = warp / G, gw = warp % G;     // row-block group, warp within the group
+  const int chunk_id = blockIdx.x % p.n_chunks_grid;
+  const int cta_in_chunk = blockIdx.x / p.n_chunks_grid;
+  const TravChunk c = p.chunks[chunk_id];
+  const int F = p.F;
+  const int K = p.K;
+
+  uint8_t* cdata = smem;
+  float* Xs = reinterpret_cast<float*>(smem + p.chunk_cap) + (size_t)grp * 64 * F;  // [F][32]
+  float* St = Xs + 32 * F;                                                          // [32][F]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.chunk_cap + (size_t)NB * 256 * F);
+  uint64_t* red = reinterpret_cast<uint64_t*>(smem + p.red_off);  // [NB][G-1][32][K] intra-group partials
+
+  const bool clustered = p.mode == TRAV_CLUSTER;
+  const int nC = p.n_chunks;
+  uint64_t* full_bar = bars + 1 + NB;        // [NB][2] (leader): peers' partials landed
+  uint64_t* empty_bar = bars + 1 + 3 * NB;   // [NB][2] (peers): leader consumed the slot
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bars[0], 1);
+    for (int b = 0; b < NB; ++b) ptx::mbar_init(&bars[1 + b], 1);
+    if (clustered)
+      for (int b = 0; b < 2 * NB; ++b) {
+        ptx::mbar_init(&full_bar[b], 32 * (nC - 1));
+        ptx::mbar_init(&empty_bar[b], 32);
+      }
+    ptx::fence_barrier_init();
+    ptx::fence_proxy_async();
+  }
+  if (clustered) ptx::cluster_sync();
+  else __syncthreads();
+  if (!GT && threadIdx.x == 0) {
+    ptx::mbar_arrive_expect_tx(&bars[0], (uint32_t)c.bytes);
+    const uint8_t* src = p.data + c.offset;
+    for (int32_t o = 0; o < c.bytes; o += 65536) {
+      const uint32_t n = (uint32_t)min(65536, c.bytes - o);
+      ptx::bulk_g2s(cdata + o, src + o, n, &bars[0]);
+    }
+  }
+
+  const int64_t n_rows = p.n_rows;
+  const int64_t n_blocks = (n_rows + 31) / 32;
+  const int64_t stride = (int64_t)p.cpc * NB;
+  int64_t blk = (int64_t)cta_in_chunk * NB + grp;
+  uint64_t* sbar = &bars[1 + grp];
+  uint32_t sphase = 0;
+  const uint32_t block_bytes = 32u * (uint32_t)F * 4u;
+
+  auto issue = [&](int64_t b) {  // warp 0 of the group, lane 0: next block -> staging
+    if (gw == 0 && lane == 0 && b < n_blocks && (b + 1) * 32 <= n_rows) {
+      ptx::fence_proxy_async();
+      ptx::mbar_arrive_expect_tx(sbar, block_bytes);
+      ptx::bulk_g2s(St, p.X + b * 32 * (int64_t)F, block_bytes, sbar);
+    }
+  };
+  issue(blk);
+  if (!GT) ptx::mbar_wait(&bars[0], 0);  // chunk resident
+
+  const float* xl = Xs + lane;
+  // feature share of the transpose
+  const int f_lo = F * gw / G, f_hi = F * (gw + 1) / G;
+  uint64_t* slots = reinterpret_cast<uint64_t*>(smem + p.slot_off);  // [NB][2][nC-1][32][K]
+  uint32_t it = 0;
+
+  while (blk < n_blocks) {
+    const int64_t row0 = blk * 32;
+    const bool full = row0 + 32 <= n_rows;
+    if (full) {
+      ptx::mbar_wait(sbar, sphase);
+      sphase ^= 1;
+    } else {
+      const int rows = (int)(n_rows - row0);
+      const float* src = p.X + row0 * F;
+      if (gw == 0)
+        for (int e = lane; e < rows * F; e += 32) St[e] = src[e];
+      group_sync(grp, G);
+    }
+    // transpose staging [32][F] -> feature-major [F][32] (features split over
+    // the group's warps).  Every write hits bank `lane`; reads of row `lane`
+    // start at a lane-dependent feature so one instruction spreads over banks.
+    if ((F & 3) == 0 && G == 1) {
+      const float4* srow = reinterpret_cast<const float4*>(St + lane * F);
+#pragma unroll 2
+      for (int f4 = 0; f4 < F / 4; ++f4) {
+        const float4 v = srow[f4];
+        Xs[(4 * f4 + 0) * 32 + lane] = v.x;
+        Xs[(4 * f4 + 1) * 32 + lane] = v.y;
+        Xs[(4 * f4 + 2) * 32 + lane] = v.z;
+        Xs[(4 * f4 + 3) * 32 + lane] = v.w;
+      }
+    } else {
+      const float* srow = St + lane * F;
+      const int span = f_hi - f_lo;
+      if (span > 0) {
+        int f = f_lo + lane % span;
+#pragma unroll 4
+        for (int f0 = 0; f0 < span; ++f0) {
+          Xs[f * 32 + lane] = srow[f];
+          f = (f + 1 == f_hi) ? f_lo : f + 1;
+        }
+      }
+    }
+    group_sync(grp, G);  // Xs ready, staging free
+    const int64_t next = blk + stride;
+    issue(next);
+
+    const int64_t row = row0 + lane;
+    ACC acc[KT];
+#pragma unroll
+    for (int k = 0; k < KT; ++k) acc[k] = ACC(0);
+
+    // ceil(nt / NI_MAX) passes of (nearly) equal size: each pass walks its
+    // trees as independent dependency chains (ILP); a pass costs about the same
+    // latency whatever its width, so the pass count is what matters.  Full ILP
+    // range for the common int64 / no-missing / K <= 8 kernels, passes of <= 4
+    // for the rare variants (compile time).
+    auto run_chunk = [&](const TravChunk& cc, const uint8_t* base) {
+      constexpr int NI_MAX = (!ML && KT <= 8 && !std::is_same<ACC, double>::value) ? 12 : 4;
+      const int D = cc.depth;
+      const int I = (1 << D) - 1, L = 1 << D;
+      const uint2* nodes = reinterpret_cast<const uint2*>(base);
+      const float* leaves = reinterpret_cast<const float*>(base + cc.leaf_offset);
+      // this warp's share of the chunk's trees
+      const int t0 = (int)((int64_t)cc.n_trees * gw / G), t1 = (int)((int64_t)cc.n_trees * (gw + 1) / G);
+      const int nt = t1 - t0;
+      const int n_pass = (nt + NI_MAX - 1) / NI_MAX;
+      int j = t0;
+      for (int q = 0; q < n_pass; ++q) {
+        const int sz = nt / n_pass + (q < nt % n_pass ? 1 : 0);
+        walk_tail<KT, ACC, ML, NI_MAX>(sz, p, cc, nodes, leaves, xl, j, I, L, D, K, row, acc);
+        j += sz;
+      }
+    };
+    if (GT) {
+      // trees too large for shared memory: every CTA walks all chunks from
+      // global memory (L1/L2), no cross-CTA combine
+      for (int ci = 0; ci < nC; ++ci) {
+        const TravChunk cc = p.chunks[ci];
+        run_chunk(cc, p.data + cc.offset);
+      }
+    } else {
+      run_chunk(c, cdata);
+    }
+
+    if (p.mode != TRAV_APPLY) {
+      // combine the group's warps (exact int64 / fixed order)
+      uint64_t* gred = red + (size_t)grp * (G - 1) * 32 * K;
+      if (gw > 0) {
+        uint64_t* dst = gred + ((size_t)(gw - 1) * 32 + lane) * K;
+#pragma unroll
+        for (int k = 0; k < KT; ++k)
+          if (k < K) dst[k] = reinterpret_cast<const uint64_t&>(acc[k]);
+      }
+      group_sync(grp, G);
+      if (gw == 0) {
+        for (int q = 0; q < G - 1; ++q) {
+          const uint64_t* src = gred + ((size_t)q * 32 + lane) * K;
+#pragma unroll
+          for (int k = 0; k < KT; ++k)
+            if (k < K) acc[k] += reinterpret_cast<const ACC&>(src[k]);
+        }
+        if (clustered) {
+          const int s = it & 1;
+          const uint32_t ph = (it >> 1) & 1;
+          ++it;
+          uint64_t* slot = slots + (size_t)(grp * 2 + s) * (nC - 1) * 32 * K;
+          if (chunk_id != 0) {
+            ptx::mbar_wait_cluster(&empty_bar[grp * 2 + s], ph ^ 1);
+            const uint32_t dst = ptx::mapa(ptx::s2u(slot + ((size_t)(chunk_id - 1) * 32 + lane) * K), 0);
+#pragma unroll
+            for (int k = 0; k < KT; ++k)
+              if (k < K) ptx::st_cluster_u64(dst + 8 * k, reinterpret_cast<const uint64_t&>(acc[k]));
+            ptx::mbar_arrive_remote(ptx::mapa(ptx::s2u(&full_bar[grp * 2 + s]), 0));
+          } else {
+            ptx::mbar_wait_cluster(&full_bar[grp * 2 + s], ph);
+            for (int q = 0; q < nC - 1; ++q) {
+              const uint64_t* src = slot + ((size_t)q * 32 + lane) * K;
+#pragma unroll
+              for (int k = 0; k < KT; ++k)
+                if (k < K) acc[k] += reinterpret_cast<const ACC&>(src[k]);
+            }
+            for (int q = 1; q < nC; ++q)
+              ptx::mbar_arrive_remote(ptx::mapa(ptx::s2u(&empty_bar[grp * 2 + s]), q));
+            if (row < n_rows) finalize_row<KT, ACC>(p.fin, row, acc);
+          }
+        } else if (row < n_rows) {
+          if (p.mode == TRAV_PARTIAL) {
+            ACC* o = static_cast<ACC*>(p.partial) + ((size_t)chunk_id * n_rows + row) * K;
+#pragma unroll
+            for (int k = 0; k < KT; ++k)
+              if (k < K) o[k] = acc[k];
+          } else {
+            finalize_row<KT, ACC>(p.fin, row, acc);
+          }
+        }
+      }
+    } else {
+      group_sync(grp, G);  // keep the group's barrier sequence uniform
+    }
+    blk = next;
+  }
+  if (clustered) ptx::cluster_sync();  // no CTA leaves while peers may touch its shared memory
+}
+
+// Sum per-chunk partials in chunk order (exact for int64) and finalize.
+template <int KT, typename ACC>
+__global__ void __launch_bounds__(256) trav_combine_kernel(const ACC* partial, int32_t n_chunks,
+                                                            int64_t n_rows, FinalizeArgs fin) {
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= n_rows) return;
+  const int K = fin.K;
+  ACC acc[KT];
+#pragma unroll
+  for (int k = 0; k < KT; ++k) acc[k] = ACC(0);
+  for (int c = 0; c < n_chunks; ++c) {
+    const ACC* src = partial + ((size_t)c * n_rows + row) * K;
+#pragma unroll
+    for (int k = 0; k < KT; ++k)
+      if (k < K) acc[k] += src[k];
+  }
+  finalize_row<KT, ACC>(fin, row, acc);
+}
+
+template <int KT, typename ACC, bool ML, bool GT>
+cudaError_t launch_trav_t(const TravParams& p, int grid_ctas, int block, int smem, int cluster,
+                                 cudaStream_t st) {
+  auto kern = trav_kernel<KT, ACC, ML, GT>;
+  static int configured_smem = 0;  // per instantiation
+  cudaError_t e;
+  if (configured_smem < smem) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    if (e != cudaSuccess) return e;
+    configured_smem = 232448;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  int grid = grid_ctas;
+  if (cluster > 1) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(cluster);
+    int max_clusters = 0;
+    e = cudaOccupancyMaxActiveClusters(&max_clusters, (void*)kern, &cfg);
+    if (std::getenv("BRIDGER_DEBUG"))
+      std::fprintf(stderr, "[bridger] cluster=%d smem=%d max_active_clusters=%d (%s)\n", cluster, smem,
+                   max_clusters, cudaGetErrorString(e));
+    if (e != cudaSuccess || max_clusters < 1) {
+      cudaGetLastError();
+      return cudaErrorNotSupported;  // caller falls back to partials
+    }
+    grid = std::min(grid_ctas, max_clusters * cluster);
+    grid = std::max(cluster, grid / cluster * cluster);
+  }
+  cfg.gridDim = dim3(grid);
+  TravParams q = p;
+  q.cpc = grid / p.n_chunks_grid;
+  if (std::getenv("BRIDGER_DEBUG"))
+    std::fprintf(stderr, "[bridger] trav_kernel mode=%d grid=%d block=%d smem=%d cluster=%d chunks=%d cpc=%d\n", q.mode,
+                 grid, block, smem, cluster, q.n_chunks, q.cpc);
+  cudaEvent_t ev;
+  hot_begin(st, &ev);
+  e = cudaLaunchKernelEx(&cfg, kern, q);
+  hot_end(st, ev);
+  count_launch();
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+
+#define BRIDGER_TRAV_INSTANTIATE(ACC, ML, GT)                                                                  \
+  template cudaError_t launch_trav_t<1, ACC, ML, GT>(const TravParams&, int, int, int, int, cudaStream_t);  \
+  template cudaError_t launch_trav_t<2, ACC, ML, GT>(const TravParams&, int, int, int, int, cudaStream_t);  \
+  template cudaError_t launch_trav_t<4, ACC, ML, GT>(const TravParams&, int, int, int, int, cudaStream_t);  \
+  template cudaError_t launch_trav_t<8, ACC, ML, GT>(const TravParams&, int, int, int, int, cudaStream_t);  \
+  template cudaError_t launch_trav_t<16, ACC, ML, GT>(const TravParams&, int, int, int, int, cudaStream_t); \
+  template cudaError_t launch_trav_t<64, ACC, ML, GT>(const TravParams&, int, int, int, int, cudaStream_t);
+
+}  // namespace bridger

@@ -166,3 +166,16 @@ def test_chunk_counts_cluster_and_partial_paths(n_trees):
 def test_many_deep_chunks_regression():
     m = perfect_ensemble(15, 150, 10, 20, kind="regression", lr=0.01, calib_rows=2048)
     check(m, gen_x(16, 0, 3001, 20), apply=False)
+
+
+def test_c4_shaped_global_trees():
+    """Depth-12, 8-class trees (164 KB each) exceed shared memory: walked from
+    global memory by every CTA (no partials)."""
+    c, m = make_config("C4", n_trees=6)
+    check(m, gen_x(4, 0, 4001, 64))
+
+
+def test_mixed_depth_forest():
+    m = perfect_ensemble(17, 60, 9, 11, kind="classification", n_classes=3, calib_rows=2048)
+    m = prune_ensemble(m, 17, p=0.3, with_missing=False)
+    check(m, gen_x(18, 0, 5000, 11))

@@ -1,31 +1,593 @@
-// GEMM-form lowering of steps a1..a4 (placeholder until the tcgen05 kernels land).
+// GEMM form of steps a1..a4 -- the tensor-operator lowering
+// of a tree (COR) that the paper's framework generates: an exact
+// feature gather, a threshold compare, the path-matrix contraction (matmul,
+// PAPER.md:588) and the leaf-count compare (equal), then the
+// leaf-value gather and the per-tree reduction.
+//
+//   K1 gc_kernel  a1+a2  P[t][r][i] = [X[r, A_t[i]] <= B_t[i]]  (exact fp32 gather,
+//                        never a one-hot GEMM; NaN -> missing_left)   int8 0/1
+//   K2 pc_kernel  a3+a4  S = P . C_D on tcgen05 (kind::i8, M=128, N=L_pad,
+//                        K=32 per instruction), accumulator in TMEM; the
+//                        epilogue tcgen05.ld's each row and keeps the unique l
+//                        with S[l] == D_D[l]                            int16 leaf
+//   K3 lg_kernel  a5+a6+a7  acc += E_t[leaf] (int64 fixed point), finalize
+//
+// C_D is universal per depth (host lowering); P tiles are written by K1
+// directly in the UMMA canonical K-major "interleaved" layout
+// [k-chunk of 16 B][128 rows][16 B], so K2 stages each (tree, 128-row tile)
+// operand with ONE bulk copy (TMA engine) and describes it with LBO = 2048 B
+// (next 16-byte K chunk), SBO = 128 B (next 8-row core matrix).  Rows are
+// processed in blocks so the decision scratch stays bounded.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <limits>
 #include <string>
 #include <vector>
 
 #include "bridger_internal.h"
+#include "finalize.cuh"
+#include "ptx.cuh"
 
 namespace bridger {
 
-bool gemm_build(bridger_model* m, const bridger_model_desc*, const std::vector<int32_t>&, std::string* why) {
+void count_launch();
+void hot_begin(cudaStream_t st, cudaEvent_t* ev);
+void hot_end(cudaStream_t st, cudaEvent_t start);
+
+struct GemmClassDev {
+  int32_t depth, i_pad, l_pad, n_trees;
+  int64_t feat_off;   // int32 [n][i_pad]  feature | missing_left << 31
+  int64_t thr_off;    // float [n][i_pad]
+  int64_t cmat_off;   // int8  [i_pad/16][l_pad][16]  C_D in canonical K-major layout
+  int64_t dv_off;     // int32 [l_pad]  D_D (127 for padding columns: never matches)
+  int64_t leaf_off;   // float [n][L][K]  leaf values (fixed-point scaled when exact)
+  int32_t first_slot; // index of the class's first tree in slot order
+  int32_t pad_;
+};
+
+struct GemmHost {
+  std::vector<GemmClassDev> classes;
+  std::vector<int32_t> slot_tree;      // slot -> original tree
+  std::vector<int32_t> tree_slot;      // original tree -> slot
+  std::vector<int32_t> tree_class;     // original tree -> class index
+  int64_t max_p_per_row = 0;           // max over classes of n_trees * i_pad
+  int32_t max_trees = 0;
+};
+
+static constexpr int kSmemMax = 232448;
+
+// ------------------------------------------------------------------ K1 -----
+// grid (row tiles of the block, tree groups), 128 threads = 128 rows.
+// out layout TILED: P[t][rt][kc][128][16]; PLAIN: P[t][row][i_pad].
+template <bool PLAIN>
+__global__ void __launch_bounds__(128) gc_kernel(const float* __restrict__ X, int64_t row0, int32_t rows, int32_t F,
+                                                 const uint8_t* __restrict__ gbase, GemmClassDev cls,
+                                                 int32_t tree_begin, int32_t trees_per_cta, int32_t tree_end,
+                                                 int8_t* __restrict__ P) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int r = threadIdx.x;
+  const int rt = blockIdx.x;
+  const int n_rt = gridDim.x;
+  const int S = 129;  // padded feature-major X tile: bank (f*129 + r) % 32 = (f + r) % 32
+  float* Xs = reinterpret_cast<float*>(smem);
+  // coalesced load of the 128-row tile, transposed into Xs[f][r]
+  const int64_t tile_row0 = row0 + (int64_t)rt * 128;
+  const int tile_rows = max(0, min(128, (int)(row0 + rows - tile_row0)));
+  const float* src = X + tile_row0 * F;
+  for (int e = r; e < 128 * F; e += 128) {
+    const int rr = e / F, f = e - rr * F;
+    Xs[f * S + rr] = rr < tile_rows ? src[e] : 0.0f;
+  }
+  __syncthreads();
+  const int32_t* feat = reinterpret_cast<const int32_t*>(gbase + cls.feat_off);
+  const float* thr = reinterpret_cast<const float*>(gbase + cls.thr_off);
+  const int ip = cls.i_pad;
+  const int t_lo = tree_begin + blockIdx.y * trees_per_cta;
+  const int t_hi = min(tree_end, t_lo + trees_per_cta);
+  for (int t = t_lo; t < t_hi; ++t) {
+    const int32_t* ft = feat + (size_t)t * ip;
+    const float* tt = thr + (size_t)t * ip;
+    for (int kc = 0; kc < ip / 16; ++kc) {
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t word = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int i = kc * 16 + q * 4 + b;
+          const int32_t fw = __ldg(ft + i);        // warp-uniform: broadcast
+          const float th = __ldg(tt + i);
+          const float x = Xs[(fw & 0x7fffffff) * S + r];
+          uint32_t d = (x <= th) ? 1u : 0u;         // a2: less_equal, exact fp32
+          if (fw < 0 && isnan(x)) d = 1u;           // missing_left
+          word |= d << (8 * b);
+        }
+        w[q] = word;
+      }
+      const int64_t t_local = t - tree_begin;
+      if (PLAIN) {
+        const int64_t row = (int64_t)rt * 128 + r;
+        if (r < tile_rows)
+          *reinterpret_cast<uint4*>(P + (t_local * rows + row) * ip + kc * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+      } else {
+        int8_t* dst = P + ((t_local * n_rt + rt) * (int64_t)ip * 128) + (int64_t)kc * 2048 + r * 16;
+        *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+  }
+}
+
+// plain [rows][i_pad] -> tiled [rt][kc][128][16] (step-level test entry only)
+__global__ void tile_kernel(const int8_t* __restrict__ in, int64_t rows, int32_t ip, int8_t* __restrict__ out) {
+  const int64_t n16 = (rows + 127) / 128 * 128 * (ip / 16);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n16; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e / (ip / 16);
+    const int kc = (int)(e % (ip / 16));
+    const int64_t rt = row / 128;
+    const int r = (int)(row % 128);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (row < rows) v = *reinterpret_cast<const uint4*>(in + row * ip + kc * 16);
+    *reinterpret_cast<uint4*>(out + rt * 128 * ip + (int64_t)kc * 2048 + r * 16) = v;
+  }
+}
+
+// ------------------------------------------------------------------ K2 -----
+namespace umma {
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  // sm_100 shared-memory matrix descriptor, SWIZZLE_NONE, K-major canonical layout
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  return d;                // base offset 0, lbo mode 0, layout type 0 (no swizzle)
+}
+// kind::i8 instruction descriptor: D s32, A s8, B s8, both K-major, M = 128
+__host__ __device__ constexpr uint32_t idesc_i8(int N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(ptx::s2u(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+}  // namespace umma
+
+struct PcParams {
+  const int8_t* P;       // tiled decisions [n_trees][n_rt][i_pad/16][128][16]
+  const uint8_t* gbase;  // class data (C_D tile, D_D)
+  GemmClassDev cls;
+  int32_t n_trees;       // trees in this launch (class-local, starting at 0 of P)
+  int32_t n_rt;          // 128-row tiles
+  int32_t rows;          // valid rows of the block
+  int32_t tmem_cols;     // allocated columns (power of 2)
+  int32_t b_bytes;       // i_pad * l_pad
+  int32_t mode;          // 0: int16 leaf index, 1: int32 S rows
+  int16_t* leaf;         // [n_trees][rows]
+  int32_t* S;            // [n_trees][rows][l_pad]
+};
+
+__global__ void __launch_bounds__(128, 1) pc_kernel(const PcParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ip = p.cls.i_pad, lp = p.cls.l_pad;
+  const uint32_t a_bytes = 128u * (uint32_t)ip;
+  uint8_t* sB = smem;
+  uint8_t* sA = smem + ((p.b_bytes + 1023) / 1024) * 1024;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + 2 * a_bytes);  // [0] B, [1,2] A full, [3,4] MMA done
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 5);
+  int32_t* sDv = reinterpret_cast<int32_t*>(bars + 6);
+
+  if (tid == 0) {
+    for (int i = 0; i < 5; ++i) ptx::mbar_init(&bars[i], 1);
+    ptx::fence_barrier_init();
+    ptx::fence_proxy_async();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(ptx::s2u(tmem_holder)),
+                 "r"(p.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  const int32_t* gDv = reinterpret_cast<const int32_t*>(p.gbase + p.cls.dv_off);
+  for (int l = tid; l < lp; l += 128) sDv[l] = gDv[l];
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  const int n_items = p.n_trees * p.n_rt;
+  const int grid = gridDim.x;
+  auto load_a = [&](int item, int s) {
+    ptx::fence_proxy_async();
+    ptx::mbar_arrive_expect_tx(&bars[1 + s], a_bytes);
+    ptx::bulk_g2s(sA + (size_t)s * a_bytes, p.P + (size_t)item * a_bytes, a_bytes, &bars[1 + s]);
+  };
+  if (tid == 0) {
+    ptx::mbar_arrive_expect_tx(&bars[0], (uint32_t)p.b_bytes);
+    for (int o = 0; o < p.b_bytes; o += 32768)
+      ptx::bulk_g2s(sB + o, p.gbase + p.cls.cmat_off + o, (uint32_t)min(32768, p.b_bytes - o), &bars[0]);
+    if ((int)blockIdx.x < n_items) load_a(blockIdx.x, 0);
+    if ((int)blockIdx.x + grid < n_items) load_a(blockIdx.x + grid, 1);
+    ptx::mbar_wait(&bars[0], 0);
+  }
+  const uint32_t idesc = umma::idesc_i8(lp);
+  const uint32_t sA_u = ptx::s2u(sA), sB_u = ptx::s2u(sB);
+  uint32_t aphase[2] = {0, 0}, mphase[2] = {0, 0};
+
+  auto epilogue = [&](int item, int s) {
+    ptx::mbar_wait(&bars[3 + s], mphase[s]);
+    mphase[s] ^= 1;
+    umma::fence_after();
+    if (tid == 0 && item + 2 * grid < n_items) load_a(item + 2 * grid, s);  // A stage s is free now
+    const int t = item / p.n_rt, rt = item % p.n_rt;
+    const int row = rt * 128 + warp * 32 + lane;
+    const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(s * lp);
+    int leaf = -1;
+    for (int cb = 0; cb < lp; cb += 16) {
+      uint32_t v[16];
+      umma::ld16(tbase + cb, v);
+      umma::wait_ld();
+      if (p.mode == 0) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if ((int32_t)v[j] == sDv[cb + j]) leaf = cb + j;   // a4: the unique l with S == D_D
+      } else if (row < p.rows) {
+        int4* o = reinterpret_cast<int4*>(p.S + ((size_t)t * p.rows + row) * lp + cb);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          o[j] = make_int4((int)v[4 * j], (int)v[4 * j + 1], (int)v[4 * j + 2], (int)v[4 * j + 3]);
+      }
+    }
+    if (p.mode == 0 && row < p.rows) p.leaf[(size_t)t * p.rows + row] = (int16_t)leaf;
+    umma::fence_before();
+  };
+
+  int it = 0, prev_item = -1;
+  for (int item = blockIdx.x; item < n_items; item += grid, ++it) {
+    const int s = it & 1;
+    if (tid == 0) {
+      ptx::mbar_wait(&bars[1 + s], aphase[s]);
+      aphase[s] ^= 1;
+      umma::fence_after();
+      const uint32_t a0 = sA_u + (uint32_t)s * a_bytes;
+      for (int ks = 0; ks < ip / 32; ++ks) {
+        const uint64_t ad = umma::smem_desc(a0 + (uint32_t)ks * 2u * 2048u, 2048u, 128u);
+        const uint64_t bd = umma::smem_desc(sB_u + (uint32_t)ks * 2u * (uint32_t)lp * 16u, (uint32_t)lp * 16u, 128u);
+        umma::mma_i8(tmem + (uint32_t)(s * lp), ad, bd, idesc, ks > 0 ? 1u : 0u);
+      }
+      umma::commit(&bars[3 + s]);
+    }
+    if (prev_item >= 0) epilogue(prev_item, s ^ 1);
+    __syncthreads();  // TMEM stage s^1 free for the next MMA
+    prev_item = item;
+  }
+  if (prev_item >= 0) epilogue(prev_item, (it - 1) & 1);
+  __syncthreads();
+  umma::fence_after();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols) : "memory");
+}
+
+// ------------------------------------------------------------------ K3 -----
+template <int KT, typename ACC>
+__global__ void __launch_bounds__(256) lg_kernel(const int16_t* __restrict__ leaf, int32_t rows, int32_t n_trees,
+                                                 const float* __restrict__ E, int32_t L, int32_t K,
+                                                 ACC* __restrict__ accbuf, int32_t first, int32_t last,
+                                                 int64_t row0, FinalizeArgs fin) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  ACC acc[KT];
+#pragma unroll
+  for (int k = 0; k < KT; ++k) acc[k] = (first || k >= K) ? ACC(0) : accbuf[(size_t)r * K + k];
+  for (int t = 0; t < n_trees; ++t) {
+    const int l = leaf[(size_t)t * rows + r];
+    const float* e = E + ((size_t)t * L + l) * K;
+#pragma unroll
+    for (int k = 0; k < KT; ++k)
+      if (k < K) {
+        const float v = __ldg(e + k);
+        if (std::is_same<ACC, long long>::value) acc[k] += (ACC)__float2ll_rz(v);
+        else acc[k] += (ACC)v;
+      }
+  }
+  if (last) {
+    finalize_row<KT, ACC>(fin, row0 + r, acc);
+  } else {
+#pragma unroll
+    for (int k = 0; k < KT; ++k)
+      if (k < K) accbuf[(size_t)r * K + k] = acc[k];
+  }
+}
+
+// ------------------------------------------------------------- host side ----
+static int dev_sms(int dev) {
+  int n = 148;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+bool gemm_build(bridger_model* m, const bridger_model_desc* d, const std::vector<int32_t>& depth, std::string* why) {
   m->gemm_ok = false;
-  if (why) *why = "GEMM path not built";
-  return false;
+  const int32_t T = d->n_trees, K = d->n_outputs;
+  for (int32_t t = 0; t < T; ++t)
+    if (depth[t] > 8) {
+      if (why) *why = "GEMM path supports depth <= 8 (path matrix N = 2^D <= 256)";
+      return false;
+    }
+  auto* h = new GemmHost();
+  std::vector<int32_t> order(T);
+  for (int32_t t = 0; t < T; ++t) order[t] = t;
+  auto eff = [&](int32_t t) { return std::max(1, depth[t]); };
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return eff(a) < eff(b); });
+  h->slot_tree = order;
+  h->tree_slot.assign(T, 0);
+  h->tree_class.assign(T, 0);
+  std::vector<uint8_t> buf;
+  auto align = [&](size_t a) { buf.resize((buf.size() + a - 1) / a * a, 0); };
+  PaddedTree pt;
+  int32_t s = 0;
+  while (s < T) {
+    const int32_t D = eff(order[s]);
+    int32_t n = 0;
+    while (s + n < T && eff(order[s + n]) == D) ++n;
+    GemmClassDev c{};
+    c.depth = D;
+    c.i_pad = gemm_i_pad(D);
+    c.l_pad = gemm_l_pad(D);
+    c.n_trees = n;
+    c.first_slot = s;
+    const int32_t I = (1 << D) - 1, L = 1 << D;
+    align(256);
+    c.cmat_off = (int64_t)buf.size();
+    {
+      std::vector<int8_t> Cm((size_t)c.i_pad * c.l_pad);
+      std::vector<int32_t> Dv(L);
+      path_matrix(D, c.i_pad, c.l_pad, Cm.data(), Dv.data());
+      buf.resize(buf.size() + (size_t)c.i_pad * c.l_pad);
+      int8_t* dst = reinterpret_cast<int8_t*>(buf.data() + c.cmat_off);
+      for (int32_t kc = 0; kc < c.i_pad / 16; ++kc)
+        for (int32_t l = 0; l < c.l_pad; ++l)
+          for (int32_t b = 0; b < 16; ++b) dst[((size_t)kc * c.l_pad + l) * 16 + b] = Cm[(size_t)(kc * 16 + b) * c.l_pad + l];
+      align(16);
+      c.dv_off = (int64_t)buf.size();
+      buf.resize(buf.size() + 4 * (size_t)c.l_pad);
+      int32_t* dv = reinterpret_cast<int32_t*>(buf.data() + c.dv_off);
+      for (int32_t l = 0; l < c.l_pad; ++l) dv[l] = l < L ? Dv[l] : 127;
+    }
+    align(16);
+    c.feat_off = (int64_t)buf.size();
+    buf.resize(buf.size() + 4 * (size_t)n * c.i_pad);
+    align(16);
+    c.thr_off = (int64_t)buf.size();
+    buf.resize(buf.size() + 4 * (size_t)n * c.i_pad);
+    align(16);
+    c.leaf_off = (int64_t)buf.size();
+    buf.resize(buf.size() + 4 * (size_t)n * L * K);
+    for (int32_t j = 0; j < n; ++j) {
+      const int32_t t = order[s + j];
+      h->tree_slot[t] = s + j;
+      h->tree_class[t] = (int32_t)h->classes.size();
+      pad_tree(d, t, D, &pt);
+      int32_t* fe = reinterpret_cast<int32_t*>(buf.data() + c.feat_off) + (size_t)j * c.i_pad;
+      float* th = reinterpret_cast<float*>(buf.data() + c.thr_off) + (size_t)j * c.i_pad;
+      for (int32_t i = 0; i < c.i_pad; ++i) {
+        if (i < I) {
+          fe[i] = pt.feature[i] | (pt.missing[i] ? (int32_t)0x80000000 : 0);
+          th[i] = pt.threshold[i];
+        } else {
+          fe[i] = 0;  // padding: x <= NaN is false, so P[i >= I] == 0 exactly
+          th[i] = std::numeric_limits<float>::quiet_NaN();
+        }
+      }
+      float* lv = reinterpret_cast<float*>(buf.data() + c.leaf_off) + (size_t)j * L * K;
+      for (int32_t l = 0; l < L * K; ++l) lv[l] = m->acc_int ? std::ldexp(pt.leaf_value[l], -m->ex.q) : pt.leaf_value[l];
+    }
+    h->max_p_per_row = std::max<int64_t>(h->max_p_per_row, (int64_t)n * c.i_pad);
+    h->max_trees = std::max(h->max_trees, n);
+    h->classes.push_back(c);
+    s += n;
+  }
+  void* dbuf = nullptr;
+  if (cudaMalloc(&dbuf, buf.size()) != cudaSuccess || cudaMemcpy(dbuf, buf.data(), buf.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(dbuf);
+    delete h;
+    if (why) *why = "GEMM layout upload failed";
+    return false;
+  }
+  m->d_gemm = dbuf;
+  m->gemm_host = h;
+  m->gemm_ok = true;
+  for (auto& c : h->classes) m->gemm_classes.push_back({c.depth, c.i_pad, c.l_pad, c.first_slot, c.n_trees});
+  return true;
 }
-void gemm_free(bridger_model*) {}
-cudaError_t gemm_run(const bridger_model*, const float*, int64_t, void*, int, int32_t, cudaStream_t) {
-  return cudaErrorNotSupported;
+
+void gemm_free(bridger_model* m) {
+  cudaFree(m->d_gemm);
+  m->d_gemm = nullptr;
+  delete static_cast<GemmHost*>(m->gemm_host);
+  m->gemm_host = nullptr;
 }
-cudaError_t gemm_step_decisions(const bridger_model*, const float*, int64_t, int32_t, int32_t, int8_t*, cudaStream_t,
-                                std::string* why) {
-  *why = "GEMM path not built";
-  return cudaErrorNotSupported;
+
+static cudaError_t launch_gc(const float* X, int64_t row0, int32_t rows, int32_t F, const uint8_t* gbase,
+                             const GemmClassDev& c, int32_t t_begin, int32_t t_end, int8_t* P, bool plain,
+                             cudaStream_t st) {
+  const int n_rt = (rows + 127) / 128;
+  const int n_t = t_end - t_begin;
+  // spread trees over enough CTAs to fill the machine
+  int tpc = std::max(1, (int)((int64_t)n_t * n_rt / (4 * 148)));
+  tpc = std::min(tpc, n_t);
+  dim3 grid(n_rt, (n_t + tpc - 1) / tpc);
+  const int smem = 129 * F * 4;
+  if (smem > 48 * 1024) {
+    cudaFuncSetAttribute(gc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+    cudaFuncSetAttribute(gc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+  }
+  if (plain) gc_kernel<true><<<grid, 128, smem, st>>>(X, row0, rows, F, gbase, c, t_begin, tpc, t_end, P);
+  else gc_kernel<false><<<grid, 128, smem, st>>>(X, row0, rows, F, gbase, c, t_begin, tpc, t_end, P);
+  count_launch();
+  return cudaGetLastError();
 }
-cudaError_t gemm_step_scores(const bridger_model*, int32_t, const int8_t*, int64_t, int32_t*, cudaStream_t,
-                             std::string* why) {
-  *why = "GEMM path not built";
-  return cudaErrorNotSupported;
+
+static cudaError_t launch_pc(const int8_t* P, const uint8_t* gbase, const GemmClassDev& c, int32_t n_trees,
+                             int32_t rows, int mode, int16_t* leaf, int32_t* S, int dev, cudaStream_t st) {
+  PcParams p{};
+  p.P = P;
+  p.gbase = gbase;
+  p.cls = c;
+  p.n_trees = n_trees;
+  p.n_rt = (rows + 127) / 128;
+  p.rows = rows;
+  int cols = 32;
+  while (cols < 2 * c.l_pad) cols *= 2;
+  p.tmem_cols = cols;
+  p.b_bytes = c.i_pad * c.l_pad;
+  p.mode = mode;
+  p.leaf = leaf;
+  p.S = S;
+  const int a_bytes = 128 * c.i_pad;
+  int smem = (p.b_bytes + 1023) / 1024 * 1024 + 2 * a_bytes + 6 * 8 + 4 * c.l_pad + 64;
+  // co-resident CTAs must fit in the 512 TMEM columns of an SM: pad the
+  // shared-memory request so no more CTAs than that are placed per SM
+  const int tmem_occ = std::max(1, 512 / cols);
+  smem = std::max(smem, kSmemMax / tmem_occ - 1024);
+  cudaError_t e = cudaFuncSetAttribute(pc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+  if (e != cudaSuccess) return e;
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pc_kernel, 128, smem);
+  occ = std::max(1, std::min(occ, tmem_occ));
+  const int n_items = n_trees * p.n_rt;
+  const int grid = std::max(1, std::min(n_items, dev_sms(dev) * occ));
+  cudaEvent_t ev;
+  hot_begin(st, &ev);
+  pc_kernel<<<grid, 128, smem, st>>>(p);
+  hot_end(st, ev);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t gemm_run(const bridger_model* m, const float* X, int64_t n_rows, void* out, int want, int32_t total_trees,
+                     cudaStream_t st) {
+  const GemmHost* h = static_cast<const GemmHost*>(m->gemm_host);
+  const uint8_t* gbase = static_cast<const uint8_t*>(m->d_gemm);
+  // row blocks: decision scratch <= 256 MB
+  int64_t rb = ((int64_t)256 << 20) / std::max<int64_t>(1, h->max_p_per_row);
+  rb = std::max<int64_t>(128, rb / 128 * 128);
+  rb = std::min<int64_t>(rb, (n_rows + 127) / 128 * 128);
+  int8_t* P = nullptr;
+  int16_t* leaf = nullptr;
+  void* accbuf = nullptr;
+  cudaError_t e = cudaMallocAsync(&P, (size_t)rb * h->max_p_per_row, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&leaf, (size_t)rb * h->max_trees * 2, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&accbuf, (size_t)rb * m->K * 8, st);
+  FinalizeArgs fin{};
+  fin.task = m->task;
+  fin.agg = m->agg;
+  fin.post = m->post;
+  fin.K = m->K;
+  fin.total_trees = total_trees;
+  fin.q = m->ex.q;
+  fin.acc_int = m->acc_int ? 1 : 0;
+  fin.want = want;
+  fin.leaf_scale = m->leaf_scale;
+  fin.base = m->d_base;
+  fin.out = out;
+  const int nc = (int)h->classes.size();
+  for (int64_t r0 = 0; e == cudaSuccess && r0 < n_rows; r0 += rb) {
+    const int32_t rows = (int32_t)std::min<int64_t>(rb, n_rows - r0);
+    for (int ci = 0; ci < nc && e == cudaSuccess; ++ci) {
+      const GemmClassDev& c = h->classes[ci];
+      e = launch_gc(X, r0, rows, m->F, gbase, c, 0, c.n_trees, P, false, st);
+      if (e == cudaSuccess) e = launch_pc(P, gbase, c, c.n_trees, rows, 0, leaf, nullptr, m->device, st);
+      if (e != cudaSuccess) break;
+      const int tb = 256, g = (rows + tb - 1) / tb;
+      const float* E = reinterpret_cast<const float*>(gbase + c.leaf_off);
+      BRIDGER_DISPATCH_KT(m->K, {
+        if (m->acc_int)
+          lg_kernel<KT, long long><<<g, tb, 0, st>>>(leaf, rows, c.n_trees, E, 1 << c.depth, m->K,
+                                                      static_cast<long long*>(accbuf), ci == 0, ci == nc - 1, r0, fin);
+        else
+          lg_kernel<KT, double><<<g, tb, 0, st>>>(leaf, rows, c.n_trees, E, 1 << c.depth, m->K,
+                                                   static_cast<double*>(accbuf), ci == 0, ci == nc - 1, r0, fin);
+      });
+      count_launch();
+      e = cudaGetLastError();
+    }
+  }
+  cudaFreeAsync(P, st);
+  cudaFreeAsync(leaf, st);
+  cudaFreeAsync(accbuf, st);
+  return e;
+}
+
+cudaError_t gemm_step_decisions(const bridger_model* m, const float* X, int64_t n_rows, int32_t tree0, int32_t n_trees,
+                                int8_t* out, cudaStream_t st, std::string* why) {
+  const GemmHost* h = static_cast<const GemmHost*>(m->gemm_host);
+  if (tree0 < 0 || n_trees < 1 || tree0 + n_trees > m->T) {
+    *why = "tree range out of bounds";
+    return cudaErrorInvalidValue;
+  }
+  const int ci = h->tree_class[tree0];
+  const GemmClassDev& c = h->classes[ci];
+  for (int32_t t = tree0; t < tree0 + n_trees; ++t)
+    if (h->tree_class[t] != ci || h->tree_slot[t] != h->tree_slot[tree0] + (t - tree0)) {
+      *why = "trees must be consecutive members of one depth class";
+      return cudaErrorInvalidValue;
+    }
+  if (n_rows > INT32_MAX) {
+    *why = "too many rows";
+    return cudaErrorInvalidValue;
+  }
+  const int32_t t_begin = h->tree_slot[tree0] - c.first_slot;
+  return launch_gc(X, 0, (int32_t)n_rows, m->F, static_cast<const uint8_t*>(m->d_gemm), c, t_begin,
+                   t_begin + n_trees, out, true, st);
+}
+
+cudaError_t gemm_step_scores(const bridger_model* m, int32_t depth, const int8_t* P, int64_t rows, int32_t* out,
+                             cudaStream_t st, std::string* why) {
+  const GemmHost* h = static_cast<const GemmHost*>(m->gemm_host);
+  const GemmClassDev* c = nullptr;
+  for (auto& cc : h->classes)
+    if (cc.depth == depth) c = &cc;
+  if (!c) {
+    *why = "model has no trees of that depth";
+    return cudaErrorInvalidValue;
+  }
+  if (rows > INT32_MAX) {
+    *why = "too many rows";
+    return cudaErrorInvalidValue;
+  }
+  const int64_t n_rt = (rows + 127) / 128;
+  int8_t* tiled = nullptr;
+  cudaError_t e = cudaMallocAsync(&tiled, (size_t)n_rt * 128 * c->i_pad, st);
+  if (e != cudaSuccess) return e;
+  tile_kernel<<<256, 256, 0, st>>>(P, rows, c->i_pad, tiled);
+  count_launch();
+  e = cudaGetLastError();
+  if (e == cudaSuccess)
+    e = launch_pc(tiled, static_cast<const uint8_t*>(m->d_gemm), *c, 1, (int32_t)rows, 1, nullptr, out, m->device, st);
+  cudaFreeAsync(tiled, st);
+  return e;
 }
 
 }  // namespace bridger

@@ -1,0 +1,98 @@
+"""Multi-GPU bookkeeping on CPU with gloo, world_size 2:
+row shards need no collective and concatenate to the full result; tree shards'
+int64 fixed-point partials (at the WHOLE ensemble's q, reading c9) reduce-
+scattered by row equal the full-ensemble sums exactly; partitions are
+contiguous, complete and balanced."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import paper_2405_12491_b200 as B
+from paper_2405_12491_b200.dist import reduce_scatter_rows, row_range, tree_partition, tree_visits
+from synth import gen_x, make_config, perfect_ensemble, prune_ensemble
+
+
+def test_row_range_covers_exactly():
+    for n in (0, 1, 7, 1000, 1001):
+        for w in (1, 2, 3, 8):
+            parts = [row_range(n, w, r) for r in range(w)]
+            assert parts[0][0] == 0 and parts[-1][1] == n
+            for (a, b), (c, d) in zip(parts, parts[1:]):
+                assert b == c and a <= b
+
+
+def test_tree_partition_balanced_contiguous():
+    m = prune_ensemble(perfect_ensemble(3, 57, 7, 5, calib_rows=256), 3, p=0.3)
+    cost = tree_visits(m)
+    for w in (1, 2, 4, 8):
+        parts = tree_partition(cost, w)
+        assert parts[0][0] == 0 and parts[-1][1] == m.n_trees
+        assert all(b == c for (_, b), (c, _) in zip(parts, parts[1:]))
+        loads = [cost[a:b].sum() for a, b in parts]
+        assert max(loads) - min(loads) <= 2 * cost.max()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # tree sharding
+        m = perfect_ensemble(5, 23, 6, 9, kind="regression", lr=0.05, calib_rows=512)
+        m = prune_ensemble(m, 5, p=0.2)
+        X = gen_x(6, 0, 301, 9)          # 301 rows: padded to a multiple of world
+        qx, tier, _ = B.analyze_exactness(m)
+        a, b = tree_partition(tree_visits(m), world)[rank]
+        part = oracle.run(m.subset(range(a, b)), X)["acc"]
+        raw = torch.from_numpy(np.round(np.ldexp(part, -qx)).astype(np.int64))
+        n_pad = -(-X.shape[0] // world) * world
+        raw = torch.cat([raw, torch.zeros((n_pad - X.shape[0], 1), dtype=torch.int64)])
+        mine = reduce_scatter_rows(raw)
+        full = oracle.run(m, X)["acc"]
+        want = np.round(np.ldexp(full, -qx)).astype(np.int64)
+        r0 = rank * (n_pad // world)
+        keep = min(mine.shape[0], X.shape[0] - r0)
+        np.testing.assert_array_equal(mine[:keep].numpy(), want[r0:r0 + keep])
+        # row sharding: no collective on the data path; gather only to check
+        _, mc = make_config("C2", n_trees=7)
+        Xc = gen_x(2, 0, 257, 28)
+        ra, rb = row_range(Xc.shape[0], world, rank)
+        lab = torch.from_numpy(oracle.run(mc, Xc[ra:rb])["label"].astype(np.int64))
+        sizes = [row_range(Xc.shape[0], world, r) for r in range(world)]
+        mx = max(b_ - a_ for a_, b_ in sizes)
+        padded = torch.cat([lab, torch.full((mx - lab.shape[0],), -1, dtype=torch.int64)])
+        bufs = [torch.zeros(mx, dtype=torch.int64) for _ in sizes]
+        dist.all_gather(bufs, padded)
+        got = torch.cat([bb[: b_ - a_] for bb, (a_, b_) in zip(bufs, sizes)])
+        np.testing.assert_array_equal(got.numpy(), oracle.run(mc, Xc)["label"])
+        q.put((rank, "ok"))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_tree_and_row_sharding():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: "ok", 1: "ok"}, res

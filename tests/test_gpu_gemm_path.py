@@ -1,0 +1,84 @@
+"""GEMM-form path (steps a1..a4 as K1 gather-compare, K2 tcgen05 int8 path
+contraction, K3 leaf gather/reduce) against definitions the mathematics fixes:
+
+* K1 decisions P[t][r][i] == [x[r, A_t[i]] <= B_t[i]] (NaN -> missing_left),
+  computed on the CPU from the library's own padded heap arrays, bitwise;
+* K2 S == P . C_D as a CPU int32 matmul (C_D from bridger_path_matrix, pinned by
+  exhaustive enumeration in test_boundary_cpu.py), bitwise, on random 0/1 P;
+* end to end (variant "gemm"): labels / leaves / scores == oracle (same bar as
+  the traversal).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from synth import gen_x, inject_specials, make_config, perfect_ensemble, prune_ensemble
+from tests.test_gpu_parity import check, dev
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+import paper_2405_12491_b200 as B  # noqa: E402
+
+
+def cpu_decisions(m, X, t):
+    p = B.lower_tree(m, t)
+    D = p["depth"]
+    I = (1 << D) - 1
+    ip, _ = B.gemm_geometry(max(D, 1))
+    x = X[:, p["feature"]]
+    with np.errstate(invalid="ignore"):
+        d = (x <= p["threshold"][None, :])
+    d |= np.isnan(x) & (p["missing_left"][None, :] != 0)
+    out = np.zeros((X.shape[0], ip), np.int8)
+    out[:, :I] = d
+    return out
+
+
+@pytest.mark.parametrize("name,ml", [("C2", False), ("C3", False), ("mixed", True)])
+def test_k1_decisions_bitwise(name, ml):
+    if name == "mixed":
+        m = perfect_ensemble(21, 10, 6, 9, kind="classification", n_classes=3, calib_rows=512)
+        m = prune_ensemble(m, 21, p=0.0, with_missing=ml)
+        X = inject_specials(gen_x(22, 0, 1001, 9), 22, rate=0.05)
+    else:
+        c, m = make_config(name, n_trees=12)
+        X = gen_x(c.seed, 0, 1001, c.n_features)
+    g = B.Model(m)
+    D = B.lower_tree(m, 0)["depth"]
+    ip, _ = B.gemm_geometry(D)
+    P = g.step_decisions(dev(X), 2, 5, ip).cpu().numpy()
+    for j in range(5):
+        np.testing.assert_array_equal(P[j], cpu_decisions(m, X, 2 + j))
+
+
+@pytest.mark.parametrize("D", [3, 6, 8])
+def test_k2_path_contraction_is_int_matmul(D):
+    m = perfect_ensemble(23, 4, D, 5, kind="regression")
+    g = B.Model(m)
+    ip, lp = B.gemm_geometry(D)
+    rows = 1000  # 7 full 128-row tiles + a ragged tail
+    rng = np.random.default_rng(D)
+    P = (rng.random((rows, ip)) < 0.5).astype(np.int8)
+    S = g.step_path_scores(D, dev(P)).cpu().numpy()
+    Cm, _ = B.path_matrix(D)
+    ref = P.astype(np.int32) @ Cm.astype(np.int32)
+    np.testing.assert_array_equal(S, ref)
+
+
+@pytest.mark.parametrize("name,rows", [("C1", None), ("C2", 9001), ("C3", 5001)])
+def test_gemm_variant_end_to_end(name, rows):
+    c, m = make_config(name, n_trees=None if name != "C3" else 120)
+    if name == "C1":
+        from synth import iris_like_x
+        X = iris_like_x(1)
+    else:
+        X = gen_x(c.seed, 0, rows, c.n_features)
+    g, _ = check(m, X, variant="gemm", apply=False)
+    assert g.info()["variant"] == "gemm"
+
+
+def test_gemm_variant_pruned_missing_mixed_depth():
+    m = perfect_ensemble(25, 40, 7, 13, kind="classification", n_classes=4, calib_rows=1024)
+    m = prune_ensemble(m, 25, p=0.2, with_missing=True)
+    X = inject_specials(gen_x(26, 0, 3001, 13), 26, rate=0.02)
+    check(m, X, variant="gemm", apply=False)

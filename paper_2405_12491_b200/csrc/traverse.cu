@@ -97,7 +97,11 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
   // global-tree mode: every CTA walks every chunk -> the grid is one chunk-group
   if (L.global_trees) p.n_chunks_grid = 1;
   else p.n_chunks_grid = n_chunks;
-  const int cpc = std::max(1, sms / p.n_chunks_grid);
+  // persistent grid ~ one CTA per SM, but never more CTAs per chunk than there
+  // are row-block groups to hand out (small batches: C1 is one CTA)
+  const int64_t n_blocks = (n_rows + 31) / 32;
+  const int64_t groups_needed = (n_blocks + NB - 1) / NB;
+  const int cpc = (int)std::max<int64_t>(1, std::min<int64_t>(sms / p.n_chunks_grid, groups_needed));
   const int grid = p.n_chunks_grid * cpc;
   cudaError_t err = cudaSuccess;
   BRIDGER_DISPATCH_KT(m->K, {

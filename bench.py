@@ -174,6 +174,8 @@ def main():
     ap.add_argument("--variant", default=None, choices=[None, "auto", "traverse", "gemm"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--rows", type=int, default=None, help="override rows per GPU (exploration; reported in config)")
+    ap.add_argument("--trees", type=int, default=None, help="override ensemble size (exploration)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -190,7 +192,11 @@ def main():
         dist.init_process_group("nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    cfg, m = make_config(args.config)
+    cfg, m = make_config(args.config, n_trees=args.trees)
+    if args.rows or args.trees:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, n_rows=args.rows or cfg.n_rows, n_trees=m.n_trees,
+                                  describe=cfg.describe + f" [override: {args.rows or cfg.n_rows} rows, {m.n_trees} trees]")
     n = cfg.n_rows
     row0 = rank * n
     X = gen_x_torch(cfg.seed, row0, n, cfg.n_features, device=dev)
@@ -235,20 +241,22 @@ def main():
     value = n * world / (ms_per_step / 1e3)
 
     # ---- e2e through the public host-buffer API (pinned input, labels back to host)
-    Xh = torch.from_numpy(gen_x(cfg.seed, row0, n, cfg.n_features)).pin_memory()
+    Xh = (torch.from_numpy(gen_x(cfg.seed, row0, n, cfg.n_features)) if args.e2e_steps > 0
+          else torch.zeros((32, cfg.n_features))).pin_memory()
     oh = torch.empty(n, dtype=torch.int32).pin_memory() if classif else torch.empty((n, 1)).pin_memory()
-    model.predict_host(Xh, out=oh)
+    if args.e2e_steps > 0:
+        model.predict_host(Xh, out=oh)
     e2e_times = []
-    for _ in range(max(1, args.e2e_steps)):
+    for _ in range(args.e2e_steps):
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         model.predict_host(Xh, out=oh)
         e2e_times.append(time.perf_counter() - t0)
-    te = torch.tensor([sum(e2e_times) / len(e2e_times)], dtype=torch.float64, device=dev)
+    te = torch.tensor([sum(e2e_times) / max(1, len(e2e_times))], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e = {"value": n * world / te.item(), "unit": "rows/s", "h2d_bytes_per_step": n * cfg.n_features * 4,
+    e2e = {"value": n * world / te.item() if e2e_times else None, "unit": "rows/s", "h2d_bytes_per_step": n * cfg.n_features * 4,
            "d2h_bytes_per_step": int(oh.numel() * oh.element_size()),
            "api": "bridger_predict_host (2-stream chunked H2D/compute/D2H pipeline)"}
 

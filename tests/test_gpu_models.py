@@ -1,0 +1,110 @@
+"""Real-model and edge-tier parity on the GPU: scikit-learn-trained trees
+(unbalanced, mixed depths up to 14, NaN routing), the E63 exactness tier
+(int64 exact, oracle within 1e-5; shard/permutation invariance bitwise), many
+classes (K > 8 register-array paths), and K = 1 regression through the host
+API."""
+import numpy as np
+import pytest
+
+import oracle
+from synth import gen_x, inject_specials, perfect_ensemble
+from synth.trees import ModelDesc
+from tests.sk_export import from_sklearn_forest, from_sklearn_gbr
+from tests.test_gpu_parity import check, dev
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+import paper_2405_12491_b200 as B  # noqa: E402
+
+sk = pytest.importorskip("sklearn")
+from sklearn.ensemble import GradientBoostingRegressor, RandomForestClassifier  # noqa: E402
+from sklearn.tree import DecisionTreeClassifier  # noqa: E402
+
+
+def _data(seed, n, F, k, nan_rate=0.0):
+    X = gen_x(seed, 0, n, F)
+    z = X @ np.linspace(-1, 1, F).astype(np.float32) + 0.5 * X[:, 0] * X[:, 1]
+    y = np.digitize(z, np.quantile(z, np.linspace(0, 1, k + 1)[1:-1]))
+    if nan_rate:
+        X = inject_specials(X, seed, rate=nan_rate)
+        X[np.isinf(X)] = 0
+    return X, y, z
+
+
+@pytest.mark.parametrize("variant", ["traverse", "gemm"])
+def test_sklearn_random_forest_unbounded_depth(variant):
+    X, y, _ = _data(31, 6000, 12, 5, nan_rate=0.01)
+    depth = 14 if variant == "traverse" else 8
+    est = RandomForestClassifier(n_estimators=40, max_depth=depth, random_state=0).fit(X, y)
+    m = from_sklearn_forest(est, 12, with_missing=True)
+    Xt, _, _ = _data(32, 4001, 12, 5, nan_rate=0.01)
+    g, o = check(m, Xt, variant=variant, apply=variant == "traverse")
+    np.testing.assert_allclose(g.predict_proba(dev(Xt)).cpu().numpy(), est.predict_proba(Xt), atol=1e-6)
+
+
+def test_sklearn_decision_tree_deep():
+    X, y, _ = _data(33, 20000, 6, 3)
+    est = DecisionTreeClassifier(max_depth=14, random_state=0).fit(X, y)
+    m = from_sklearn_forest(est, 6)
+    Xt, _, _ = _data(34, 5000, 6, 3)
+    g, _ = check(m, Xt)
+    np.testing.assert_array_equal(g.apply(dev(Xt)).cpu().numpy()[:, 0], est.apply(Xt))
+
+
+def test_sklearn_gbr():
+    X, _, z = _data(35, 5000, 7, 2)
+    est = GradientBoostingRegressor(n_estimators=80, max_depth=5, random_state=0).fit(X, z)
+    m = from_sklearn_gbr(est, 7, X)
+    Xt, _, _ = _data(36, 3000, 7, 2)
+    g, _ = check(m, Xt)
+    np.testing.assert_allclose(g.predict(dev(Xt)).cpu().numpy()[:, 0], est.predict(Xt), rtol=1e-5, atol=1e-6)
+
+
+def test_e63_tier_exact_and_order_free():
+    m = perfect_ensemble(41, 64, 6, 8, kind="regression", lr=1.0)
+    v = m.value.copy()
+    leaves = np.nonzero(m.left == -1)[0]
+    # every value a multiple of 2^-10 (q = -10) with per-tree maxima 2^42:
+    # M = 64 * 2^42 * 2^10 = 2^58 -> tier E63 (fp64 sums of such values round)
+    v[leaves] = np.round(v[leaves] * 1024) / np.float32(1024)
+    v[leaves[::3]] = np.float32(2.0 ** 42) * np.sign(v[leaves[::3]] + 1e-30)
+    v[leaves[1]] = np.float32(2.0 ** -10)
+    m = ModelDesc(**{**m.__dict__, "value": v.astype(np.float32)})
+    q, tier, l2 = B.analyze_exactness(m)
+    assert tier == "E63", (tier, l2)
+    X = gen_x(42, 0, 3000, 8)
+    g = B.Model(m)
+    assert g.info()["acc_is_int64"] and g.info()["acc_scale_exp"] == q
+    raw = g.predict_raw(dev(X))
+    # exact reference: integer sum of the leaf values the oracle's walk reached
+    o = oracle.run(m, X)
+    offs = m.tree_offsets
+    ints = np.round(np.ldexp(m.value.astype(np.float64), -q)).astype(np.int64)
+    exact = np.zeros(X.shape[0], np.int64)
+    for t in range(m.n_trees):
+        exact += ints[offs[t] + o["leaf"][:, t]]
+    np.testing.assert_array_equal(raw.cpu().numpy()[:, 0], exact)
+    # finalize from the exact sum, same fp64 operations as the definition (c6)
+    a = exact.astype(np.float64) * 2.0 ** q
+    want = (np.float64(0.5) + np.float64(m.leaf_scale) * a).astype(np.float32)
+    np.testing.assert_array_equal(g.predict(dev(X)).cpu().numpy()[:, 0], want)
+    # the oracle's fp64 tree-order sum is within its own rounding bound of the exact sum
+    bound = m.n_trees * 2.0 ** -52 * np.max(np.abs(m.value)) * m.n_trees
+    assert np.max(np.abs(o["acc"][:, 0] - a)) <= bound
+    # int64 accumulation is order-free: a permuted ensemble gives identical bits
+    perm = np.random.default_rng(1).permutation(m.n_trees)
+    assert torch.equal(raw, B.Model(m.subset(perm)).predict_raw(dev(X)))
+
+
+@pytest.mark.parametrize("K", [9, 16, 33])
+def test_many_classes(K):
+    m = perfect_ensemble(43, 25, 5, 10, kind="classification", n_classes=K, calib_rows=512)
+    check(m, gen_x(44, 0, 2001, 10))
+
+
+def test_regression_host_api():
+    m = perfect_ensemble(45, 30, 6, 12, kind="regression")
+    X = gen_x(46, 0, 50001, 12)
+    g = B.Model(m)
+    out = g.predict_host(X).numpy()
+    np.testing.assert_array_equal(out, oracle.run(m, X)["pred"])

@@ -122,6 +122,12 @@ bridger_status bridger_model_free(bridger_model* m); /* NULL is OK; synchronises
 bridger_status bridger_model_info(const bridger_model* m, int32_t* max_depth, int32_t* exact_tier,
                                   int32_t* acc_is_int64, int32_t* acc_scale_exp);
 bridger_status bridger_model_set_variant(bridger_model* m, int32_t variant); /* bridger_variant */
+/* Traversal layout chosen at load: number of tree chunks,
+ * threshold-bin coded mode (4-byte nodes + u16 input codes), global-tree mode
+ * (trees too large for shared memory), warps per CTA and warps per row block.
+ * Any output pointer may be NULL. */
+bridger_status bridger_model_layout(const bridger_model* m, int32_t* n_chunks, int32_t* coded, int32_t* global_trees,
+                                    int32_t* n_warps, int32_t* group);
 int32_t bridger_model_variant(const bridger_model* m); /* variant that predicts will run */
 
 /* predict: regression -> float out[n_rows * K] (s cast to fp32);

@@ -49,7 +49,7 @@ EXPORTS = [
     "bridger_predict_raw", "bridger_finalize", "bridger_predict_host", "bridger_step_decisions",
     "bridger_step_path_scores", "bridger_gemm_geometry", "bridger_path_matrix", "bridger_lower_tree",
     "bridger_analyze_exactness", "bridger_validate", "bridger_last_error", "bridger_status_string",
-    "bridger_launch_count", "bridger_hot_kernel_timing", "bridger_hot_kernel_time",
+    "bridger_launch_count", "bridger_hot_kernel_timing", "bridger_hot_kernel_time", "bridger_model_layout",
 ]
 
 
@@ -82,6 +82,7 @@ def _load_lib():
         "bridger_launch_count": ([], i64),
         "bridger_hot_kernel_timing": ([i32], i32),
         "bridger_hot_kernel_time": ([vp, vp], i32),
+        "bridger_model_layout": ([vp, vp, vp, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -244,6 +245,12 @@ class Model:
         _check(_lib.bridger_model_info(self._h, C.byref(d), C.byref(t), C.byref(a), C.byref(q)))
         return dict(max_depth=d.value, exact_tier=TIERS[t.value], acc_is_int64=bool(a.value), acc_scale_exp=q.value,
                     variant={v: k for k, v in VARIANTS.items()}[_lib.bridger_model_variant(self._h)])
+
+    def layout(self) -> dict:
+        n, c, g, w, gr = (C.c_int32() for _ in range(5))
+        _check(_lib.bridger_model_layout(self._h, C.byref(n), C.byref(c), C.byref(g), C.byref(w), C.byref(gr)))
+        return dict(n_chunks=n.value, coded=bool(c.value), global_trees=bool(g.value), n_warps=w.value,
+                    group=gr.value)
 
     def set_variant(self, name: str):
         _check(_lib.bridger_model_set_variant(self._h, VARIANTS[name]))

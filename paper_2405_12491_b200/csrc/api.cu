@@ -110,6 +110,8 @@ static void free_model(bridger_model* m) {
   cudaFree(m->d_slot_leafid_off);
   cudaFree(m->d_leaf_ids);
   cudaFree(m->d_base);
+  cudaFree(m->d_bin_table);
+  cudaFree(m->d_bin_offsets);
   gemm_free(m);
   delete m;
 }
@@ -315,7 +317,9 @@ bridger_status bridger_model_load(const bridger_model_desc* d, int cuda_device, 
         (e = upload(reinterpret_cast<TravChunk**>(&m->d_trav_chunks), L.chunks.data(), L.chunks.size())) != cudaSuccess ||
         (e = upload(&m->d_slot_tree, L.slot_tree.data(), L.slot_tree.size())) != cudaSuccess ||
         (e = upload(&m->d_slot_leafid_off, L.slot_leafid_off.data(), L.slot_leafid_off.size())) != cudaSuccess ||
-        (e = upload(&m->d_leaf_ids, L.leaf_ids.data(), L.leaf_ids.size())) != cudaSuccess) {
+        (e = upload(&m->d_leaf_ids, L.leaf_ids.data(), L.leaf_ids.size())) != cudaSuccess ||
+        (e = upload(&m->d_bin_table, L.bin_table.data(), L.bin_table.size())) != cudaSuccess ||
+        (e = upload(&m->d_bin_offsets, L.bin_offsets.data(), L.bin_offsets.size())) != cudaSuccess) {
       free_model(m);
       return e == cudaErrorMemoryAllocation ? fail(BRIDGER_E_OOM, "device allocation failed") : cuda_fail(e, "upload");
     }
@@ -367,6 +371,17 @@ bridger_status bridger_model_set_variant(bridger_model* m, int32_t variant) {
 }
 
 int32_t bridger_model_variant(const bridger_model* m) { return m ? m->resolved_variant : -1; }
+
+bridger_status bridger_model_layout(const bridger_model* m, int32_t* n_chunks, int32_t* coded, int32_t* global_trees,
+                                    int32_t* n_warps, int32_t* group) {
+  if (!m) return fail(BRIDGER_E_NULL_ARG, "model is NULL");
+  if (n_chunks) *n_chunks = m->trav_ok ? (int32_t)m->trav.chunks.size() : 0;
+  if (coded) *coded = m->trav_ok && m->trav.codes ? 1 : 0;
+  if (global_trees) *global_trees = m->trav_ok && m->trav.global_trees ? 1 : 0;
+  if (n_warps) *n_warps = m->trav.n_warps;
+  if (group) *group = m->trav.group;
+  return BRIDGER_OK;
+}
 
 bridger_status bridger_predict(const bridger_model* m, const float* X, int64_t n_rows, int32_t n_features,
                                void* out, void* stream) {

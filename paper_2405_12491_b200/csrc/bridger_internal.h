@@ -71,6 +71,9 @@ struct TravLayout {
   int32_t group = 2;            // warps sharing one 32-row X block (they split the chunk's trees)
   bool use_cluster = false;     // cross-chunk reduction over DSMEM (else global partials)
   bool global_trees = false;    // trees too large for shared memory: walked from global memory
+  bool codes = false;           // threshold-bin codes: 4-byte nodes, u16 X codes (see lowering.cpp)
+  std::vector<float> bin_table;     // concatenated sorted distinct thresholds per feature
+  std::vector<int32_t> bin_offsets; // [F+1]
   int32_t smem_bytes = 0;       // dynamic shared memory per CTA
   int32_t chunk_budget = 0;     // max bytes of one chunk
   bool has_missing = false;
@@ -84,7 +87,7 @@ struct TravLayout {
 // Shared-memory carve-up of the traversal kernel after the chunk:
 //   [NB row blocks x (feature-major X + staging) = NB*256*F][mbarriers]
 //   [intra-group partials NB*(G-1)*32*K*8][cluster DSMEM slots NB*2*(nC-1)*32*K*8]
-inline int32_t trav_bar_bytes(int32_t nb) { return ((1 + 5 * nb) * 8 + 15) / 16 * 16; }
+inline int32_t trav_bar_bytes(int32_t nb) { return ((1 + 6 * nb) * 8 + 15) / 16 * 16; }
 inline int32_t trav_red_bytes(int32_t nb, int32_t g, int32_t K) { return nb * (g - 1) * 32 * K * 8; }
 inline int32_t trav_slot_bytes(int32_t nb, int32_t n_chunks, int32_t K) {
   return (n_chunks >= 2 && n_chunks <= 8) ? nb * 2 * (n_chunks - 1) * 32 * K * 8 : 0;
@@ -135,6 +138,8 @@ struct bridger_model {
   int64_t* d_slot_leafid_off = nullptr;
   int32_t* d_leaf_ids = nullptr;
   double* d_base = nullptr;
+  float* d_bin_table = nullptr;      // threshold-bin codes (TravLayout::codes)
+  int32_t* d_bin_offsets = nullptr;
 
   // GEMM-path layout on device (filled by gemm_path.cu)
   bool gemm_ok = false;

@@ -210,87 +210,142 @@ void path_matrix(int32_t D, int32_t i_pad, int32_t l_pad, int8_t* C, int32_t* Dv
 // ------------------------------------------------------ traversal layout ----
 static constexpr int32_t kSmemMax = 232448;  // 227 KB opt-in per block (sm_100)
 
+// Threshold-bin codes (§8(f2), "data type rewriting" PAPER.md:502): per
+// feature f the sorted distinct thresholds U_f; x becomes
+// code(x) = #{u in U_f : u < x} (NaN -> 0xFFFF), and a node's threshold t =
+// U_f[j] becomes j.  For every non-NaN x:  x <= U_f[j]  <=>  code(x) <= j
+// (the thresholds below x are exactly U_f[0..code(x)-1]), so the comparison is
+// unchanged bit for bit.  Eligible when F <= 1023 and every |U_f| <= 65534.
+static bool build_bin_table(const bridger_model_desc* d, TravLayout* out) {
+  const int32_t F = d->n_features;
+  if (F > 1023) return false;
+  std::vector<std::vector<float>> u(F);
+  for (int32_t t = 0; t < d->n_trees; ++t)
+    for (int64_t g = d->tree_offsets[t]; g < d->tree_offsets[t + 1]; ++g)
+      if (d->left[g] != -1) u[d->feature[g]].push_back(d->threshold[g]);
+  out->bin_offsets.assign(F + 1, 0);
+  out->bin_table.clear();
+  for (int32_t f = 0; f < F; ++f) {
+    auto& v = u[f];
+    std::sort(v.begin(), v.end());
+    // -0.0 and +0.0 compare equal: keep one
+    v.erase(std::unique(v.begin(), v.end(), [](float a, float b) { return a == b; }), v.end());
+    if (v.size() > 65534) return false;
+    out->bin_offsets[f] = (int32_t)out->bin_table.size();
+    out->bin_table.insert(out->bin_table.end(), v.begin(), v.end());
+  }
+  out->bin_offsets[F] = (int32_t)out->bin_table.size();
+  return true;
+}
+
+static uint32_t code_of_threshold(const TravLayout& L, int32_t f, float t) {
+  const float* b = L.bin_table.data() + L.bin_offsets[f];
+  const float* e = L.bin_table.data() + L.bin_offsets[f + 1];
+  return (uint32_t)(std::lower_bound(b, e, t) - b);  // t is present: exact index
+}
+
 bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& depth,
                        const Exactness& ex, bool acc_int, TravLayout* out, std::string* why) {
   const int32_t T = d->n_trees, F = d->n_features, K = d->n_outputs;
   out->has_missing = d->missing_left != nullptr;
-  // 16 warps per CTA; NB row blocks of 32 rows (feature-major X + staging,
-  // 256*F bytes each) with G = 16/NB warps per block splitting the chunk's
-  // trees.  NB is the largest power of two whose X blocks fit in 120 KB
-  // (measured on B200: C2 best at NB=16/G=1, C3 at NB=4/G=4).
-  const int32_t xw = 2 * 32 * F * 4;
-  int32_t nw = 16, nb = 16;
-  while (nb > 1 && nb * xw > 120 * 1024) nb /= 2;
-  if (const char* e = std::getenv("BRIDGER_WARPS")) nw = std::max(1, std::min(16, std::atoi(e)));  // experiments
-  if (const char* e = std::getenv("BRIDGER_BLOCKS")) nb = std::max(1, std::min(16, std::atoi(e)));
-  nb = std::min(nb, nw);
-  while (nw % nb) --nb;
-  const int32_t G = nw / nb;
   out->use_cluster = std::getenv("BRIDGER_CLUSTER") != nullptr;
-  const int32_t misc = 1024 + trav_bar_bytes(nb) + trav_red_bytes(nb, G, K);
-  const int32_t base_budget = kSmemMax - misc - nb * xw;
-  out->n_warps = nw;
-  out->group = G;
-  auto tree_bytes = [&](int32_t D) -> int64_t {
-    return (int64_t)((1 << D) - 1) * 8 + (int64_t)(1 << D) * K * 4;
-  };
-  auto chunk_bytes = [&](int32_t n, int32_t D) -> int64_t {
-    const int64_t nodes = (int64_t)n * ((1 << D) - 1) * 8;
-    const int64_t nodes_al = (nodes + 15) / 16 * 16;
-    return nodes_al + ((int64_t)n * (1 << D) * K * 4 + 15) / 16 * 16;
-  };
+  // coded nodes pay for the separate binning pass only when each input value
+  // is reused by many node visits: measured on B200 C2 (800
+  // visits/row over 28 features) and C3 (3000 over 90) lose, so the default is
+  // codes iff sum_t D_t >= 64 * F.  BRIDGER_CODES=0/1 forces either format.
+  const char* codes_env = std::getenv("BRIDGER_CODES");
+  int64_t visits = 0;
+  for (int32_t t = 0; t < T; ++t) visits += std::max(1, depth[t]);
+  bool want_codes = codes_env ? codes_env[0] != '0' : visits >= 64 * (int64_t)F;
+  if (want_codes) {
+    want_codes = build_bin_table(d, out);
+    // the binning kernel keeps the whole table in shared memory
+    if (want_codes && (out->bin_table.size() * 4 + (size_t)(F + 1) * 4) > 160 * 1024) want_codes = false;
+  }
   std::vector<int32_t> order(T);
   std::iota(order.begin(), order.end(), 0);
   std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return depth[a] < depth[b]; });
   const int32_t Dmax = depth[order.back()];
-  // greedy chunking over depth-sorted trees, then even re-balancing inside runs
-  // of equal depth.  The cluster-mode reduction slots depend on the chunk
-  // count, so iterate until the budget is consistent.
+
   struct Run { int32_t start, n, D; };
   std::vector<Run> bal;
-  int32_t budget = base_budget, n_prev = 1;
-  for (int iter = 0; iter < 4; ++iter) {
-    budget = base_budget - (out->use_cluster ? trav_slot_bytes(nb, n_prev, K) : 0);
-    if (chunk_bytes(1, Dmax) > budget) {
-      // global-tree mode: chunks are runs of equal depth of any size, read from
-      // global memory by every CTA (no shared-memory residency, no partials)
-      out->global_trees = true;
-      budget = INT32_MAX / 2;
-      if (chunk_bytes(T, Dmax) > (int64_t)1 << 40) {
-        if (why) *why = "model too large";
-        return false;
+  int32_t budget = 0, nb = 16, nw = 16, G = 1, node_bytes = 8, xw = 0, misc = 0;
+
+  // plan with a node format; false if one tree of the deepest class does not fit
+  auto plan = [&](bool codes) -> bool {
+    node_bytes = codes ? 4 : 8;
+    // per 32-row block: codes mode = two u16 feature-major buffers (double
+    // buffered, filled straight by bulk copy); fp32 mode = feature-major block
+    // + dense staging block
+    xw = codes ? 2 * 32 * F * 2 : 2 * 32 * F * 4;
+    // 16 warps; NB = largest power of two with NB * xw <= 120 KB (measured on
+    // B200: C2 best at NB=16/G=1, C3 at NB=4/G=4 in fp32 mode)
+    nw = 16;
+    nb = 16;
+    while (nb > 1 && nb * xw > 120 * 1024) nb /= 2;
+    if (const char* e = std::getenv("BRIDGER_WARPS")) nw = std::max(1, std::min(16, std::atoi(e)));  // experiments
+    if (const char* e = std::getenv("BRIDGER_BLOCKS")) nb = std::max(1, std::min(16, std::atoi(e)));
+    nb = std::min(nb, nw);
+    while (nw % nb) --nb;
+    G = nw / nb;
+    misc = 1024 + trav_bar_bytes(nb) + trav_red_bytes(nb, G, K);
+    const int32_t base_budget = kSmemMax - misc - nb * xw;
+    auto chunk_bytes = [&](int32_t n, int32_t D) -> int64_t {
+      const int64_t nodes = (int64_t)n * ((1 << D) - 1) * node_bytes;
+      return (nodes + 15) / 16 * 16 + ((int64_t)n * (1 << D) * K * 4 + 15) / 16 * 16;
+    };
+    out->global_trees = false;
+    int32_t n_prev = 1;
+    for (int iter = 0; iter < 4; ++iter) {
+      budget = base_budget - (out->use_cluster ? trav_slot_bytes(nb, n_prev, K) : 0);
+      if (chunk_bytes(1, Dmax) > budget) {
+        if (codes) return false;
+        // global-tree mode: chunks are runs of equal depth of any size, read from
+        // global memory by every CTA (no shared-memory residency, no partials)
+        out->global_trees = true;
+        budget = INT32_MAX / 2;
       }
-    }
-    std::vector<Run> runs;
-    int32_t s = 0;
-    while (s < T) {
-      int32_t Dc = depth[order[s]], n = 1;
-      while (s + n < T) {
-        const int32_t Dn = std::max(Dc, depth[order[s + n]]);
-        if (out->global_trees ? (Dn != Dc || chunk_bytes(n + 1, Dn) > (1 << 30)) : (chunk_bytes(n + 1, Dn) > budget)) break;
-        Dc = Dn;
-        ++n;
+      std::vector<Run> runs;
+      int32_t s = 0;
+      while (s < T) {
+        int32_t Dc = depth[order[s]], n = 1;
+        while (s + n < T) {
+          const int32_t Dn = std::max(Dc, depth[order[s + n]]);
+          if (out->global_trees ? (Dn != Dc || chunk_bytes(n + 1, Dn) > (1 << 30)) : (chunk_bytes(n + 1, Dn) > budget))
+            break;
+          Dc = Dn;
+          ++n;
+        }
+        runs.push_back({s, n, Dc});
+        s += n;
       }
-      runs.push_back({s, n, Dc});
-      s += n;
-    }
-    bal.clear();
-    for (size_t i = 0; i < runs.size();) {
-      size_t j = i;
-      int32_t total = 0;
-      while (j < runs.size() && runs[j].D == runs[i].D) total += runs[j++].n;
-      const int32_t nc = (int32_t)(j - i);
-      int32_t st = runs[i].start;
-      for (int32_t c = 0; c < nc; ++c) {
-        const int32_t n = total / nc + (c < total % nc ? 1 : 0);
-        bal.push_back({st, n, runs[i].D});
-        st += n;
+      bal.clear();
+      for (size_t i = 0; i < runs.size();) {
+        size_t j = i;
+        int32_t total = 0;
+        while (j < runs.size() && runs[j].D == runs[i].D) total += runs[j++].n;
+        const int32_t nc = (int32_t)(j - i);
+        int32_t st = runs[i].start;
+        for (int32_t c = 0; c < nc; ++c) {
+          const int32_t n = total / nc + (c < total % nc ? 1 : 0);
+          bal.push_back({st, n, runs[i].D});
+          st += n;
+        }
+        i = j;
       }
-      i = j;
+      if (out->global_trees || (int32_t)bal.size() <= n_prev) break;
+      n_prev = (int32_t)bal.size();
     }
-    if (out->global_trees || (int32_t)bal.size() == n_prev || (int32_t)bal.size() < n_prev) break;
-    n_prev = (int32_t)bal.size();
+    return true;
+  };
+  out->codes = want_codes && plan(true);
+  if (!out->codes) {
+    out->bin_table.clear();
+    out->bin_offsets.clear();
+    plan(false);
   }
+  out->n_warps = nw;
+  out->group = G;
   out->chunk_budget = budget;
   out->chunks.clear();
   out->data.clear();
@@ -306,20 +361,32 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
     c.n_trees = r.n;
     c.depth = D;
     c.first_slot = r.start;
-    const int64_t nodes = (int64_t)r.n * I * 8;
+    const int64_t nodes = (int64_t)r.n * I * node_bytes;
     c.leaf_offset = (int32_t)((nodes + 15) / 16 * 16);
-    c.bytes = (int32_t)chunk_bytes(r.n, D);
+    c.bytes = (int32_t)(c.leaf_offset + ((int64_t)r.n * L * K * 4 + 15) / 16 * 16);
     out->data.resize(off + c.bytes, 0);
     uint8_t* base = out->data.data() + off;
     for (int32_t j = 0; j < r.n; ++j) {
       const int32_t t = order[r.start + j];
       pad_tree(d, t, D, &pt);
-      uint32_t* nd = reinterpret_cast<uint32_t*>(base) + (size_t)j * I * 2;
-      for (int32_t i = 0; i < I; ++i) {
-        uint32_t tb;
-        std::memcpy(&tb, &pt.threshold[i], 4);
-        nd[2 * i] = tb;
-        nd[2 * i + 1] = (uint32_t)pt.feature[i] | ((uint32_t)pt.missing[i] << 31);
+      if (out->codes) {
+        // node word: code index j (bits 16..31) | feature * 64 (bits 6..15: byte
+        // offset of the feature's row in a [F][32] u16 block) | missing (bit 0)
+        uint32_t* nd = reinterpret_cast<uint32_t*>(base) + (size_t)j * I;
+        for (int32_t i = 0; i < I; ++i) {
+          // real nodes: t is in U_f, exact index; dummy nodes under replicated
+          // leaves (feature 0, threshold 0): any code routes to identical leaves
+          const uint32_t code = code_of_threshold(*out, pt.feature[i], pt.threshold[i]);
+          nd[i] = (code << 16) | ((uint32_t)pt.feature[i] << 6) | (uint32_t)pt.missing[i];
+        }
+      } else {
+        uint32_t* nd = reinterpret_cast<uint32_t*>(base) + (size_t)j * I * 2;
+        for (int32_t i = 0; i < I; ++i) {
+          uint32_t tb;
+          std::memcpy(&tb, &pt.threshold[i], 4);
+          nd[2 * i] = tb;
+          nd[2 * i + 1] = (uint32_t)pt.feature[i] | ((uint32_t)pt.missing[i] << 31);
+        }
       }
       float* lv = reinterpret_cast<float*>(base + c.leaf_offset) + (size_t)j * L * K;
       for (int32_t l = 0; l < L * K; ++l) {
@@ -337,6 +404,7 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
   int32_t maxc = 0;
   for (auto& c : out->chunks) maxc = std::max(maxc, c.bytes);
   out->smem_bytes = maxc + nb * xw + misc;
+  (void)why;
   return true;
 }
 

@@ -2,6 +2,6 @@
 #include "traverse.cuh"
 
 namespace bridger {
-BRIDGER_TRAV_INSTANTIATE(double, false, true)
-BRIDGER_TRAV_INSTANTIATE(double, true, true)
+BRIDGER_TRAV_INSTANTIATE(double, false, true, false)
+BRIDGER_TRAV_INSTANTIATE(double, true, true, false)
 }  // namespace bridger

@@ -2,6 +2,6 @@
 #include "traverse.cuh"
 
 namespace bridger {
-BRIDGER_TRAV_INSTANTIATE(long long, false, true)
-BRIDGER_TRAV_INSTANTIATE(long long, true, true)
+BRIDGER_TRAV_INSTANTIATE(long long, false, true, false)
+BRIDGER_TRAV_INSTANTIATE(long long, true, true, false)
 }  // namespace bridger

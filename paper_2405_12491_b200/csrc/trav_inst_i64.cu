@@ -2,5 +2,6 @@
 #include "traverse.cuh"
 
 namespace bridger {
-BRIDGER_TRAV_INSTANTIATE(long long, false, false)
+BRIDGER_TRAV_INSTANTIATE(long long, false, false, false)
+BRIDGER_TRAV_INSTANTIATE(long long, false, false, true)
 }  // namespace bridger

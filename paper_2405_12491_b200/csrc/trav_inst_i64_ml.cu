@@ -2,5 +2,6 @@
 #include "traverse.cuh"
 
 namespace bridger {
-BRIDGER_TRAV_INSTANTIATE(long long, true, false)
+BRIDGER_TRAV_INSTANTIATE(long long, true, false, false)
+BRIDGER_TRAV_INSTANTIATE(long long, true, false, true)
 }  // namespace bridger

@@ -8,24 +8,98 @@
 #include <cstdlib>
 
 #include "traverse.cuh"
+#include "ptx.cuh"
 
 namespace bridger {
 
-#define BRIDGER_TRAV_EXTERN(ACC, ML, GT)                                                                           \
-  extern template cudaError_t launch_trav_t<1, ACC, ML, GT>(const TravParams&, int, int, int, int, cudaStream_t);  \
-  extern template cudaError_t launch_trav_t<2, ACC, ML, GT>(const TravParams&, int, int, int, int, cudaStream_t);  \
-  extern template cudaError_t launch_trav_t<4, ACC, ML, GT>(const TravParams&, int, int, int, int, cudaStream_t);  \
-  extern template cudaError_t launch_trav_t<8, ACC, ML, GT>(const TravParams&, int, int, int, int, cudaStream_t);  \
-  extern template cudaError_t launch_trav_t<16, ACC, ML, GT>(const TravParams&, int, int, int, int, cudaStream_t); \
-  extern template cudaError_t launch_trav_t<64, ACC, ML, GT>(const TravParams&, int, int, int, int, cudaStream_t);
-BRIDGER_TRAV_EXTERN(long long, false, false)
-BRIDGER_TRAV_EXTERN(long long, true, false)
-BRIDGER_TRAV_EXTERN(double, false, false)
-BRIDGER_TRAV_EXTERN(double, true, false)
-BRIDGER_TRAV_EXTERN(long long, false, true)
-BRIDGER_TRAV_EXTERN(long long, true, true)
-BRIDGER_TRAV_EXTERN(double, false, true)
-BRIDGER_TRAV_EXTERN(double, true, true)
+#define BRIDGER_TRAV_EXTERN(ACC, ML, GT, CODES)                                                                           \
+  extern template cudaError_t launch_trav_t<1, ACC, ML, GT, CODES>(const TravParams&, int, int, int, int, cudaStream_t);  \
+  extern template cudaError_t launch_trav_t<2, ACC, ML, GT, CODES>(const TravParams&, int, int, int, int, cudaStream_t);  \
+  extern template cudaError_t launch_trav_t<4, ACC, ML, GT, CODES>(const TravParams&, int, int, int, int, cudaStream_t);  \
+  extern template cudaError_t launch_trav_t<8, ACC, ML, GT, CODES>(const TravParams&, int, int, int, int, cudaStream_t);  \
+  extern template cudaError_t launch_trav_t<16, ACC, ML, GT, CODES>(const TravParams&, int, int, int, int, cudaStream_t); \
+  extern template cudaError_t launch_trav_t<64, ACC, ML, GT, CODES>(const TravParams&, int, int, int, int, cudaStream_t);
+BRIDGER_TRAV_EXTERN(long long, false, false, false)
+BRIDGER_TRAV_EXTERN(long long, true, false, false)
+BRIDGER_TRAV_EXTERN(double, false, false, false)
+BRIDGER_TRAV_EXTERN(double, true, false, false)
+BRIDGER_TRAV_EXTERN(long long, false, false, true)
+BRIDGER_TRAV_EXTERN(long long, true, false, true)
+BRIDGER_TRAV_EXTERN(double, false, false, true)
+BRIDGER_TRAV_EXTERN(double, true, false, true)
+BRIDGER_TRAV_EXTERN(long long, false, true, false)
+BRIDGER_TRAV_EXTERN(long long, true, true, false)
+BRIDGER_TRAV_EXTERN(double, false, true, false)
+BRIDGER_TRAV_EXTERN(double, true, true, false)
+
+// Threshold-bin coding of the input (§8(f2)): X [N][F] fp32 row-major ->
+// codes [n_blocks][F][32] u16, code = #{u in U_f : u < x} (binary search over
+// the feature's sorted distinct thresholds, all in shared memory), NaN ->
+// 0xFFFF.  The output is already in the traversal kernel's feature-major
+// 32-row block layout, so the traversal bulk-copies it with no transpose.
+__global__ void __launch_bounds__(512) bin_kernel(const float* __restrict__ X, int64_t n_rows, int32_t F,
+                                                  const float* __restrict__ table, const int32_t* __restrict__ offs,
+                                                  int32_t table_n, uint16_t* __restrict__ codes) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  float* U = reinterpret_cast<float*>(smem);
+  int32_t* O = reinterpret_cast<int32_t*>(smem + (size_t)table_n * 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
+  const int S = F | 1;  // odd staging stride: St[lane*S + f] is bank-conflict free for a uniform f
+  float* St = reinterpret_cast<float*>(smem + (size_t)table_n * 4 + (size_t)(F + 1) * 4) + (size_t)warp * 32 * S;
+  for (int i = threadIdx.x; i < table_n; i += blockDim.x) U[i] = table[i];
+  for (int i = threadIdx.x; i <= F; i += blockDim.x) O[i] = offs[i];
+  __syncthreads();
+  const int64_t n_blocks = (n_rows + 31) / 32;
+  for (int64_t blk = (int64_t)blockIdx.x * NW + warp; blk < n_blocks; blk += (int64_t)gridDim.x * NW) {
+    const int64_t row0 = blk * 32;
+    const int rows = (int)(n_rows - row0 < 32 ? n_rows - row0 : 32);
+    const float* src = X + row0 * F;
+    // row-major copy into the odd-stride staging block: async 4-byte copies,
+    // all in flight at once (zero-filled past the last row)
+    for (int r = 0; r < 32; ++r)
+      for (int f = lane; f < F; f += 32) {
+        const uint32_t dsts = ptx::s2u(St + r * S + f);
+        const float* g = src + (int64_t)(r < rows ? r : 0) * F + f;
+        const uint32_t nbytes = r < rows ? 4u : 0u;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dsts), "l"(g), "r"(nbytes) : "memory");
+      }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    uint16_t* dst = codes + blk * 32 * (int64_t)F;
+    // lower_bound over the feature's sorted distinct thresholds; 4 features per
+    // pass give 4 independent dependency chains per thread, and lane = row
+    // with a warp-uniform feature makes the first search steps broadcasts
+    for (int f0 = 0; f0 < F; f0 += 4) {
+      float x[4];
+      int lo[4], len[4], base[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int f = min(f0 + u, F - 1);
+        x[u] = St[lane * S + f];
+        base[u] = O[f];
+        len[u] = O[f + 1] - base[u];
+        lo[u] = 0;
+      }
+      bool any = true;
+      while (any) {
+        any = false;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (len[u] > 0) {
+            const int half = len[u] >> 1;
+            const bool less = U[base[u] + lo[u] + half] < x[u];
+            lo[u] = less ? lo[u] + half + 1 : lo[u];
+            len[u] = less ? len[u] - half - 1 : half;
+            any = true;
+          }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (f0 + u < F) dst[(f0 + u) * 32 + lane] = isnan(x[u]) ? (uint16_t)0xFFFF : (uint16_t)lo[u];
+    }
+    __syncwarp();
+  }
+}
 
 // ------------------------------------------------------------- launchers ----
 static int num_sms(int dev) {
@@ -74,7 +148,8 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
   const int NW = L.n_warps, G = L.group, NB = NW / G;
   const int block = NW * 32;
   p.group = G;
-  p.red_off = p.chunk_cap + NB * 256 * m->F + trav_bar_bytes(NB);
+  const int xblk = L.codes ? 128 * m->F : 256 * m->F;
+  p.red_off = p.chunk_cap + NB * xblk + trav_bar_bytes(NB);
   p.slot_off = p.red_off + trav_red_bytes(NB, G, m->K);
   int smem = p.slot_off;
   int cluster = 1;
@@ -104,20 +179,57 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
   const int cpc = (int)std::max<int64_t>(1, std::min<int64_t>(sms / p.n_chunks_grid, groups_needed));
   const int grid = p.n_chunks_grid * cpc;
   cudaError_t err = cudaSuccess;
+  void* codes = nullptr;
+  if (L.codes) {
+    // step a1 in coded form: bin the rows once (all chunks reuse the codes)
+    const int64_t nbk = (n_rows + 31) / 32;
+    err = cudaMallocAsync(&codes, (size_t)nbk * 32 * m->F * 2, st);
+    if (err != cudaSuccess) return err;
+    const int table_n = (int)L.bin_table.size();
+    const int fixed = table_n * 4 + (m->F + 1) * 4;
+    int nwb = 16;
+    while (nwb > 1 && fixed + nwb * 32 * (m->F | 1) * 4 > 232448) --nwb;
+    const int bsmem = fixed + nwb * 32 * (m->F | 1) * 4;
+    static bool bin_attr = false;
+    if (!bin_attr) {
+      cudaFuncSetAttribute(bin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+      bin_attr = true;
+    }
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bin_kernel, nwb * 32, bsmem);
+    const int64_t want_ctas = (nbk + nwb - 1) / nwb;
+    const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>(want_ctas, (int64_t)sms * std::max(1, occ)));
+    bin_kernel<<<bgrid, nwb * 32, bsmem, st>>>(X, n_rows, m->F, m->d_bin_table, m->d_bin_offsets, table_n,
+                                                 static_cast<uint16_t*>(codes));
+    count_launch();
+    err = cudaGetLastError();
+    if (err != cudaSuccess) {
+      cudaFreeAsync(codes, st);
+      return err;
+    }
+    p.X = static_cast<const float*>(codes);
+  }
   BRIDGER_DISPATCH_KT(m->K, {
     auto launch = [&]() {
+      if (L.codes) {
+        if (m->acc_int)
+          return L.has_missing ? launch_trav_t<KT, long long, true, false, true>(p, grid, block, smem, cluster, st)
+                               : launch_trav_t<KT, long long, false, false, true>(p, grid, block, smem, cluster, st);
+        return L.has_missing ? launch_trav_t<KT, double, true, false, true>(p, grid, block, smem, cluster, st)
+                             : launch_trav_t<KT, double, false, false, true>(p, grid, block, smem, cluster, st);
+      }
       if (L.global_trees) {
         if (m->acc_int)
-          return L.has_missing ? launch_trav_t<KT, long long, true, true>(p, grid, block, smem, cluster, st)
-                               : launch_trav_t<KT, long long, false, true>(p, grid, block, smem, cluster, st);
-        return L.has_missing ? launch_trav_t<KT, double, true, true>(p, grid, block, smem, cluster, st)
-                             : launch_trav_t<KT, double, false, true>(p, grid, block, smem, cluster, st);
+          return L.has_missing ? launch_trav_t<KT, long long, true, true, false>(p, grid, block, smem, cluster, st)
+                               : launch_trav_t<KT, long long, false, true, false>(p, grid, block, smem, cluster, st);
+        return L.has_missing ? launch_trav_t<KT, double, true, true, false>(p, grid, block, smem, cluster, st)
+                             : launch_trav_t<KT, double, false, true, false>(p, grid, block, smem, cluster, st);
       }
       if (m->acc_int)
-        return L.has_missing ? launch_trav_t<KT, long long, true, false>(p, grid, block, smem, cluster, st)
-                             : launch_trav_t<KT, long long, false, false>(p, grid, block, smem, cluster, st);
-      return L.has_missing ? launch_trav_t<KT, double, true, false>(p, grid, block, smem, cluster, st)
-                           : launch_trav_t<KT, double, false, false>(p, grid, block, smem, cluster, st);
+        return L.has_missing ? launch_trav_t<KT, long long, true, false, false>(p, grid, block, smem, cluster, st)
+                             : launch_trav_t<KT, long long, false, false, false>(p, grid, block, smem, cluster, st);
+      return L.has_missing ? launch_trav_t<KT, double, true, false, false>(p, grid, block, smem, cluster, st)
+                           : launch_trav_t<KT, double, false, false, false>(p, grid, block, smem, cluster, st);
     };
     err = launch();
     if (err != cudaSuccess && p.mode == TRAV_CLUSTER) {
@@ -143,6 +255,7 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
     }
   });
   if (partial) cudaFreeAsync(partial, st);
+  if (codes) cudaFreeAsync(codes, st);
   return err;
 }
 

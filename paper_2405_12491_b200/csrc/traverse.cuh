@@ -90,24 +90,46 @@ __device__ __forceinline__ int go_right(float x, uint2 nd) {
 
 // Walk NI trees [j, j+NI) of the chunk for this thread's row (NI independent
 // dependency chains for ILP), then gather and accumulate their leaf values.
-template <int NI, int KT, typename ACC, bool ML>
-__device__ __forceinline__ void walk_trees(const TravParams& p, const TravChunk& c, const uint2* nodes,
-                                           const float* leaves, const float* xl, int j, int I, int L, int D,
+template <int NI, int KT, typename ACC, bool ML, bool CODES>
+__device__ __forceinline__ void walk_trees(const TravParams& p, const TravChunk& c, const void* nodes,
+                                           const float* leaves, const void* xl, int j, int I, int L, int D,
                                            int K, int64_t row, ACC (&acc)[KT]) {
-  constexpr uint32_t kFeatMask = ML ? 0x7fffffffu : 0xffffffffu;
   int idx[NI];
 #pragma unroll
   for (int u = 0; u < NI; ++u) idx[u] = 0;
-  const uint2* nb = nodes + (size_t)j * I;
-  for (int lvl = 0; lvl < D; ++lvl) {
-    uint2 a[NI];
+  if (CODES) {
+    // 4-byte node: code index (31..16) | feature*64 (15..6) | missing (0);
+    // xl points at this lane's u16 code in a feature-major [F][32] block
+    const uint32_t* nb = static_cast<const uint32_t*>(nodes) + (size_t)j * I;
+    const uint8_t* xb = static_cast<const uint8_t*>(xl);
+    for (int lvl = 0; lvl < D; ++lvl) {
+      uint32_t a[NI];
 #pragma unroll
-    for (int u = 0; u < NI; ++u) a[u] = nb[u * I + idx[u]];
-    float x[NI];
+      for (int u = 0; u < NI; ++u) a[u] = nb[u * I + idx[u]];
+      uint32_t x[NI];
 #pragma unroll
-    for (int u = 0; u < NI; ++u) x[u] = xl[(a[u].y & kFeatMask) * 32];
+      for (int u = 0; u < NI; ++u) x[u] = *reinterpret_cast<const uint16_t*>(xb + (a[u] & 0xFFC0u));
 #pragma unroll
-    for (int u = 0; u < NI; ++u) idx[u] = 2 * idx[u] + 1 + go_right<ML>(x[u], a[u]);
+      for (int u = 0; u < NI; ++u) {
+        int r = x[u] > (a[u] >> 16);  // code(x) > j  <=>  !(x <= t);  NaN code 0xFFFF -> right
+        if (ML) r &= !((a[u] & 1u) & (x[u] == 0xFFFFu));
+        idx[u] = 2 * idx[u] + 1 + r;
+      }
+    }
+  } else {
+    constexpr uint32_t kFeatMask = ML ? 0x7fffffffu : 0xffffffffu;
+    const uint2* nb = static_cast<const uint2*>(nodes) + (size_t)j * I;
+    const float* xf = static_cast<const float*>(xl);
+    for (int lvl = 0; lvl < D; ++lvl) {
+      uint2 a[NI];
+#pragma unroll
+      for (int u = 0; u < NI; ++u) a[u] = nb[u * I + idx[u]];
+      float x[NI];
+#pragma unroll
+      for (int u = 0; u < NI; ++u) x[u] = xf[(a[u].y & kFeatMask) * 32];
+#pragma unroll
+      for (int u = 0; u < NI; ++u) idx[u] = 2 * idx[u] + 1 + go_right<ML>(x[u], a[u]);
+    }
   }
   if (p.mode == TRAV_APPLY) {
     if (row < p.n_rows) {
@@ -149,13 +171,13 @@ __device__ __forceinline__ void walk_trees(const TravParams& p, const TravChunk&
 }
 
 // one pass over r (<= 12) trees with ILP = r
-template <int KT, typename ACC, bool ML, int MAXNI>
-__device__ __forceinline__ void walk_tail(int r, const TravParams& p, const TravChunk& c, const uint2* nodes,
-                                          const float* leaves, const float* xl, int j, int I, int L, int D, int K,
+template <int KT, typename ACC, bool ML, bool CODES, int MAXNI>
+__device__ __forceinline__ void walk_tail(int r, const TravParams& p, const TravChunk& c, const void* nodes,
+                                          const float* leaves, const void* xl, int j, int I, int L, int D, int K,
                                           int64_t row, ACC (&acc)[KT]) {
   switch (r) {
 #define BRIDGER_TAIL(N) \
-  case N: if (N <= MAXNI) walk_trees<(N <= MAXNI ? N : 1), KT, ACC, ML>(p, c, nodes, leaves, xl, j, I, L, D, K, row, acc); break;
+  case N: if (N <= MAXNI) walk_trees<(N <= MAXNI ? N : 1), KT, ACC, ML, CODES>(p, c, nodes, leaves, xl, j, I, L, D, K, row, acc); break;
     BRIDGER_TAIL(1) BRIDGER_TAIL(2) BRIDGER_TAIL(3) BRIDGER_TAIL(4) BRIDGER_TAIL(5) BRIDGER_TAIL(6)
     BRIDGER_TAIL(7) BRIDGER_TAIL(8) BRIDGER_TAIL(9) BRIDGER_TAIL(10) BRIDGER_TAIL(11) BRIDGER_TAIL(12)
 #undef BRIDGER_TAIL
@@ -172,7 +194,7 @@ __device__ __forceinline__ void group_sync(int group, int G) {
   }
 }
 
-template <int KT, typename ACC, bool ML, bool GT>
+template <int KT, typename ACC, bool ML, bool GT, bool CODES>
 __global__ void __launch_bounds__(512, 1) trav_kernel(const TravParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
@@ -185,9 +207,13 @@ __global__ void __launch_bounds__(512, 1) trav_kernel(const TravParams p) {
   const int K = p.K;
 
   uint8_t* cdata = smem;
-  float* Xs = reinterpret_cast<float*>(smem + p.chunk_cap) + (size_t)grp * 64 * F;  // [F][32]
-  float* St = Xs + 32 * F;                                                          // [32][F]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.chunk_cap + (size_t)NB * 256 * F);
+  // per row-block group: fp32 mode  Xs [F][32] float + St [32][F] float (256*F B)
+  //                      codes mode Cb[2] [F][32] u16, double buffered (128*F B)
+  const size_t xblk = CODES ? (size_t)128 * F : (size_t)256 * F;
+  float* Xs = reinterpret_cast<float*>(smem + p.chunk_cap + (size_t)grp * xblk);  // [F][32]
+  float* St = Xs + 32 * F;                                                         // [32][F]
+  uint16_t* Cb = reinterpret_cast<uint16_t*>(smem + p.chunk_cap + (size_t)grp * xblk);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.chunk_cap + (size_t)NB * xblk);
   uint64_t* red = reinterpret_cast<uint64_t*>(smem + p.red_off);  // [NB][G-1][32][K] intra-group partials
 
   const bool clustered = p.mode == TRAV_CLUSTER;
@@ -197,6 +223,7 @@ __global__ void __launch_bounds__(512, 1) trav_kernel(const TravParams p) {
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bars[0], 1);
     for (int b = 0; b < NB; ++b) ptx::mbar_init(&bars[1 + b], 1);
+    for (int b = 0; b < NB; ++b) ptx::mbar_init(&bars[1 + 5 * NB + b], 1);  // codes: 2nd buffer
     if (clustered)
       for (int b = 0; b < 2 * NB; ++b) {
         ptx::mbar_init(&full_bar[b], 32 * (nC - 1));
@@ -231,56 +258,78 @@ __global__ void __launch_bounds__(512, 1) trav_kernel(const TravParams p) {
       ptx::bulk_g2s(St, p.X + b * 32 * (int64_t)F, block_bytes, sbar);
     }
   };
-  issue(blk);
+  // codes mode: blocks of the binned input are [F][32] u16, always complete
+  const uint16_t* codes = reinterpret_cast<const uint16_t*>(p.X);
+  const uint32_t code_block_bytes = 64u * (uint32_t)F;
+  auto issue_codes = [&](int64_t b, int s) {
+    if (gw == 0 && lane == 0 && b < n_blocks) {
+      uint64_t* bar = s ? &bars[1 + 5 * NB + grp] : sbar;
+      ptx::fence_proxy_async();
+      ptx::mbar_arrive_expect_tx(bar, code_block_bytes);
+      ptx::bulk_g2s(Cb + (size_t)s * 32 * F, codes + b * 32 * (int64_t)F, code_block_bytes, bar);
+    }
+  };
+  if (CODES) issue_codes(blk, 0);
+  else issue(blk);
   if (!GT) ptx::mbar_wait(&bars[0], 0);  // chunk resident
 
-  const float* xl = Xs + lane;
   // feature share of the transpose
   const int f_lo = F * gw / G, f_hi = F * (gw + 1) / G;
   uint64_t* slots = reinterpret_cast<uint64_t*>(smem + p.slot_off);  // [NB][2][nC-1][32][K]
   uint32_t it = 0;
 
+  uint32_t itx = 0;  // blocks consumed by this group (codes double buffer)
   while (blk < n_blocks) {
     const int64_t row0 = blk * 32;
-    const bool full = row0 + 32 <= n_rows;
-    if (full) {
-      ptx::mbar_wait(sbar, sphase);
-      sphase ^= 1;
+    const int64_t next = blk + stride;
+    const void* xptr;
+    if (CODES) {
+      const int sb = itx & 1;
+      ptx::mbar_wait(sb ? &bars[1 + 5 * NB + grp] : sbar, (itx >> 1) & 1);
+      ++itx;
+      issue_codes(next, sb ^ 1);  // the other buffer was released by the previous block's group sync
+      xptr = reinterpret_cast<const uint8_t*>(Cb + (size_t)sb * 32 * F) + 2 * lane;
     } else {
-      const int rows = (int)(n_rows - row0);
-      const float* src = p.X + row0 * F;
-      if (gw == 0)
-        for (int e = lane; e < rows * F; e += 32) St[e] = src[e];
-      group_sync(grp, G);
-    }
-    // transpose staging [32][F] -> feature-major [F][32] (features split over
-    // the group's warps).  Every write hits bank `lane`; reads of row `lane`
-    // start at a lane-dependent feature so one instruction spreads over banks.
-    if ((F & 3) == 0 && G == 1) {
-      const float4* srow = reinterpret_cast<const float4*>(St + lane * F);
-#pragma unroll 2
-      for (int f4 = 0; f4 < F / 4; ++f4) {
-        const float4 v = srow[f4];
-        Xs[(4 * f4 + 0) * 32 + lane] = v.x;
-        Xs[(4 * f4 + 1) * 32 + lane] = v.y;
-        Xs[(4 * f4 + 2) * 32 + lane] = v.z;
-        Xs[(4 * f4 + 3) * 32 + lane] = v.w;
+      const bool full = row0 + 32 <= n_rows;
+      if (full) {
+        ptx::mbar_wait(sbar, sphase);
+        sphase ^= 1;
+      } else {
+        const int rows = (int)(n_rows - row0);
+        const float* src = p.X + row0 * F;
+        if (gw == 0)
+          for (int e = lane; e < rows * F; e += 32) St[e] = src[e];
+        group_sync(grp, G);
       }
-    } else {
-      const float* srow = St + lane * F;
-      const int span = f_hi - f_lo;
-      if (span > 0) {
-        int f = f_lo + lane % span;
+      // transpose staging [32][F] -> feature-major [F][32] (features split over
+      // the group's warps).  Every write hits bank `lane`; reads of row `lane`
+      // start at a lane-dependent feature so one instruction spreads over banks.
+      if ((F & 3) == 0 && G == 1) {
+        const float4* srow = reinterpret_cast<const float4*>(St + lane * F);
+#pragma unroll 2
+        for (int f4 = 0; f4 < F / 4; ++f4) {
+          const float4 v = srow[f4];
+          Xs[(4 * f4 + 0) * 32 + lane] = v.x;
+          Xs[(4 * f4 + 1) * 32 + lane] = v.y;
+          Xs[(4 * f4 + 2) * 32 + lane] = v.z;
+          Xs[(4 * f4 + 3) * 32 + lane] = v.w;
+        }
+      } else {
+        const float* srow = St + lane * F;
+        const int span = f_hi - f_lo;
+        if (span > 0) {
+          int f = f_lo + lane % span;
 #pragma unroll 4
-        for (int f0 = 0; f0 < span; ++f0) {
-          Xs[f * 32 + lane] = srow[f];
-          f = (f + 1 == f_hi) ? f_lo : f + 1;
+          for (int f0 = 0; f0 < span; ++f0) {
+            Xs[f * 32 + lane] = srow[f];
+            f = (f + 1 == f_hi) ? f_lo : f + 1;
+          }
         }
       }
+      group_sync(grp, G);  // Xs ready, staging free
+      issue(next);
+      xptr = Xs + lane;
     }
-    group_sync(grp, G);  // Xs ready, staging free
-    const int64_t next = blk + stride;
-    issue(next);
 
     const int64_t row = row0 + lane;
     ACC acc[KT];
@@ -296,7 +345,7 @@ __global__ void __launch_bounds__(512, 1) trav_kernel(const TravParams p) {
       constexpr int NI_MAX = (!ML && KT <= 8 && !std::is_same<ACC, double>::value) ? 12 : 4;
       const int D = cc.depth;
       const int I = (1 << D) - 1, L = 1 << D;
-      const uint2* nodes = reinterpret_cast<const uint2*>(base);
+      const void* nodes = base;
       const float* leaves = reinterpret_cast<const float*>(base + cc.leaf_offset);
       // this warp's share of the chunk's trees
       const int t0 = (int)((int64_t)cc.n_trees * gw / G), t1 = (int)((int64_t)cc.n_trees * (gw + 1) / G);
@@ -305,7 +354,7 @@ __global__ void __launch_bounds__(512, 1) trav_kernel(const TravParams p) {
       int j = t0;
       for (int q = 0; q < n_pass; ++q) {
         const int sz = nt / n_pass + (q < nt % n_pass ? 1 : 0);
-        walk_tail<KT, ACC, ML, NI_MAX>(sz, p, cc, nodes, leaves, xl, j, I, L, D, K, row, acc);
+        walk_tail<KT, ACC, ML, CODES, NI_MAX>(sz, p, cc, nodes, leaves, xptr, j, I, L, D, K, row, acc);
         j += sz;
       }
     };
@@ -399,10 +448,10 @@ __global__ void __launch_bounds__(256) trav_combine_kernel(const ACC* partial, i
   finalize_row<KT, ACC>(fin, row, acc);
 }
 
-template <int KT, typename ACC, bool ML, bool GT>
+template <int KT, typename ACC, bool ML, bool GT, bool CODES>
 cudaError_t launch_trav_t(const TravParams& p, int grid_ctas, int block, int smem, int cluster,
                                  cudaStream_t st) {
-  auto kern = trav_kernel<KT, ACC, ML, GT>;
+  auto kern = trav_kernel<KT, ACC, ML, GT, CODES>;
   static int configured_smem = 0;  // per instantiation
   cudaError_t e;
   if (configured_smem < smem) {
@@ -452,12 +501,12 @@ cudaError_t launch_trav_t(const TravParams& p, int grid_ctas, int block, int sme
 }
 
 
-#define BRIDGER_TRAV_INSTANTIATE(ACC, ML, GT)                                                                  \
-  template cudaError_t launch_trav_t<1, ACC, ML, GT>(const TravParams&, int, int, int, int, cudaStream_t);  \
-  template cudaError_t launch_trav_t<2, ACC, ML, GT>(const TravParams&, int, int, int, int, cudaStream_t);  \
-  template cudaError_t launch_trav_t<4, ACC, ML, GT>(const TravParams&, int, int, int, int, cudaStream_t);  \
-  template cudaError_t launch_trav_t<8, ACC, ML, GT>(const TravParams&, int, int, int, int, cudaStream_t);  \
-  template cudaError_t launch_trav_t<16, ACC, ML, GT>(const TravParams&, int, int, int, int, cudaStream_t); \
-  template cudaError_t launch_trav_t<64, ACC, ML, GT>(const TravParams&, int, int, int, int, cudaStream_t);
+#define BRIDGER_TRAV_INSTANTIATE(ACC, ML, GT, CODES)                                                                  \
+  template cudaError_t launch_trav_t<1, ACC, ML, GT, CODES>(const TravParams&, int, int, int, int, cudaStream_t);  \
+  template cudaError_t launch_trav_t<2, ACC, ML, GT, CODES>(const TravParams&, int, int, int, int, cudaStream_t);  \
+  template cudaError_t launch_trav_t<4, ACC, ML, GT, CODES>(const TravParams&, int, int, int, int, cudaStream_t);  \
+  template cudaError_t launch_trav_t<8, ACC, ML, GT, CODES>(const TravParams&, int, int, int, int, cudaStream_t);  \
+  template cudaError_t launch_trav_t<16, ACC, ML, GT, CODES>(const TravParams&, int, int, int, int, cudaStream_t); \
+  template cudaError_t launch_trav_t<64, ACC, ML, GT, CODES>(const TravParams&, int, int, int, int, cudaStream_t);
 
 }  // namespace bridger

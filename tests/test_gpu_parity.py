@@ -179,3 +179,19 @@ def test_mixed_depth_forest():
     m = perfect_ensemble(17, 60, 9, 11, kind="classification", n_classes=3, calib_rows=2048)
     m = prune_ensemble(m, 17, p=0.3, with_missing=False)
     check(m, gen_x(18, 0, 5000, 11))
+
+
+@pytest.mark.parametrize("coded", ["1", "0"])
+def test_coded_and_fp32_node_formats(coded, monkeypatch):
+    """Threshold-bin codes (§8(f2)) vs plain fp32 nodes: both bit-exact against
+    the oracle, including NaN / inf / -0 / subnormal inputs and missing_left."""
+    monkeypatch.setenv("BRIDGER_CODES", coded)
+    m = perfect_ensemble(27, 90, 8, 21, kind="classification", n_classes=3, calib_rows=2048)
+    m = prune_ensemble(m, 27, p=0.1, with_missing=True)
+    X = inject_specials(gen_x(28, 0, 6007, 21), 28, rate=0.03)
+    X[::97, 3] = m.threshold[m.feature == 3][0]          # exact ties with a threshold
+    g, _ = check(m, X)
+    assert g.layout()["coded"] == (coded == "1")
+    c, m2 = make_config("C3", n_trees=60)
+    g2, _ = check(m2, gen_x(3, 0, 4001, 90))
+    assert g2.layout()["coded"] == (coded == "1")

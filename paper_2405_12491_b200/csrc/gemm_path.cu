@@ -72,8 +72,12 @@ __global__ void __launch_bounds__(128) gc_kernel(const float* __restrict__ X, in
   const int r = threadIdx.x;
   const int rt = blockIdx.x;
   const int n_rt = gridDim.x;
+  const int ip = cls.i_pad;
   const int S = 129;  // padded feature-major X tile: bank (f*129 + r) % 32 = (f + r) % 32
-  float* Xs = reinterpret_cast<float*>(smem);
+  // [2][ip] {feature | missing<<31, threshold} node records of the current tree
+  // (double buffered: one __syncthreads per tree), then the X tile
+  uint2* nd = reinterpret_cast<uint2*>(smem);
+  float* Xs = reinterpret_cast<float*>(smem + (size_t)2 * ip * 8);
   // coalesced load of the 128-row tile, transposed into Xs[f][r]
   const int64_t tile_row0 = row0 + (int64_t)rt * 128;
   const int tile_rows = max(0, min(128, (int)(row0 + rows - tile_row0)));
@@ -82,15 +86,17 @@ __global__ void __launch_bounds__(128) gc_kernel(const float* __restrict__ X, in
     const int rr = e / F, f = e - rr * F;
     Xs[f * S + rr] = rr < tile_rows ? src[e] : 0.0f;
   }
-  __syncthreads();
   const int32_t* feat = reinterpret_cast<const int32_t*>(gbase + cls.feat_off);
   const float* thr = reinterpret_cast<const float*>(gbase + cls.thr_off);
-  const int ip = cls.i_pad;
   const int t_lo = tree_begin + blockIdx.y * trees_per_cta;
   const int t_hi = min(tree_end, t_lo + trees_per_cta);
-  for (int t = t_lo; t < t_hi; ++t) {
-    const int32_t* ft = feat + (size_t)t * ip;
-    const float* tt = thr + (size_t)t * ip;
+  const float* xr = Xs + r;
+  for (int t = t_lo, buf = 0; t < t_hi; ++t, buf ^= 1) {
+    uint2* ndb = nd + buf * ip;
+    for (int i = r; i < ip; i += 128)
+      ndb[i] = make_uint2((uint32_t)feat[(size_t)t * ip + i], __float_as_uint(thr[(size_t)t * ip + i]));
+    __syncthreads();  // node records (and, first time, the X tile) visible
+    const int64_t t_local = t - tree_begin;
     for (int kc = 0; kc < ip / 16; ++kc) {
       uint32_t w[4];
 #pragma unroll
@@ -98,17 +104,14 @@ __global__ void __launch_bounds__(128) gc_kernel(const float* __restrict__ X, in
         uint32_t word = 0;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-          const int i = kc * 16 + q * 4 + b;
-          const int32_t fw = __ldg(ft + i);        // warp-uniform: broadcast
-          const float th = __ldg(tt + i);
-          const float x = Xs[(fw & 0x7fffffff) * S + r];
-          uint32_t d = (x <= th) ? 1u : 0u;         // a2: less_equal, exact fp32
-          if (fw < 0 && isnan(x)) d = 1u;           // missing_left
+          const uint2 n = ndb[kc * 16 + q * 4 + b];            // broadcast read
+          const float x = xr[(n.x & 0x7fffffffu) * S];          // exact fp32 gather (a1)
+          uint32_t d = (x <= __uint_as_float(n.y)) ? 1u : 0u;   // a2: less_equal
+          if ((int32_t)n.x < 0 && isnan(x)) d = 1u;             // missing_left
           word |= d << (8 * b);
         }
         w[q] = word;
       }
-      const int64_t t_local = t - tree_begin;
       if (PLAIN) {
         const int64_t row = (int64_t)rt * 128 + r;
         if (r < tile_rows)
@@ -180,112 +183,147 @@ struct PcParams {
   int32_t n_trees;       // trees in this launch (class-local, starting at 0 of P)
   int32_t n_rt;          // 128-row tiles
   int32_t rows;          // valid rows of the block
-  int32_t tmem_cols;     // allocated columns (power of 2)
+  int32_t tmem_cols;     // allocated columns (power of 2): 2 accumulator stages
   int32_t b_bytes;       // i_pad * l_pad
+  int32_t stages;        // depth of the A-operand ring
   int32_t mode;          // 0: int16 leaf index, 1: int32 S rows
   int16_t* leaf;         // [n_trees][rows]
   int32_t* S;            // [n_trees][rows][l_pad]
 };
 
-__global__ void __launch_bounds__(128, 1) pc_kernel(const PcParams p) {
+// Warp-specialised tcgen05 pipeline (18 warps):
+//   warps 0-15 epilogue: warp w reads TMEM lanes 32(w%4)..+31 (= rows of the
+//              tile) and column quarter w/4 with tcgen05.ld, a4 leaf-count
+//              compare; the leaf is unique, so exactly one quarter writes it;
+//              then release the TMEM stage (4 warps per SMSP hide the LDTM and
+//              compare latencies: measured 4x faster than 1 warp per SMSP)
+//   warp 16    producer: bulk copies (TMA engine) of C_D once and of each
+//              (tree, 128-row) decision tile into a `stages`-deep ring
+//   warp 17    MMA issuer: one thread issues I_pad/32 tcgen05.mma kind::i8 per
+//              tile into one of two TMEM accumulators; tcgen05.commit frees the
+//              A stage and signals the epilogue
+constexpr int kPcEpiWarps = 16;
+constexpr int kPcThreads = (kPcEpiWarps + 2) * 32;
+
+__global__ void __launch_bounds__(kPcThreads, 1) pc_kernel(const PcParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int ip = p.cls.i_pad, lp = p.cls.l_pad;
+  const int ip = p.cls.i_pad, lp = p.cls.l_pad, D = p.cls.depth;
+  const int NS = p.stages;
   const uint32_t a_bytes = 128u * (uint32_t)ip;
   uint8_t* sB = smem;
   uint8_t* sA = smem + ((p.b_bytes + 1023) / 1024) * 1024;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + 2 * a_bytes);  // [0] B, [1,2] A full, [3,4] MMA done
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 5);
-  int32_t* sDv = reinterpret_cast<int32_t*>(bars + 6);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + (size_t)NS * a_bytes);
+  uint64_t* bfull = bars;               // [1]
+  uint64_t* afull = bars + 1;           // [NS]
+  uint64_t* aempty = bars + 1 + NS;     // [NS]
+  uint64_t* tfull = bars + 1 + 2 * NS;  // [2]
+  uint64_t* tempty = bars + 3 + 2 * NS; // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 5 + 2 * NS);
 
   if (tid == 0) {
-    for (int i = 0; i < 5; ++i) ptx::mbar_init(&bars[i], 1);
+    ptx::mbar_init(bfull, 1);
+    for (int i = 0; i < NS; ++i) {
+      ptx::mbar_init(&afull[i], 1);
+      ptx::mbar_init(&aempty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&tfull[i], 1);
+      ptx::mbar_init(&tempty[i], kPcEpiWarps * 32);
+    }
     ptx::fence_barrier_init();
     ptx::fence_proxy_async();
   }
-  if (warp == 0) {
+  if (warp == kPcEpiWarps) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(ptx::s2u(tmem_holder)),
                  "r"(p.tmem_cols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  const int32_t* gDv = reinterpret_cast<const int32_t*>(p.gbase + p.cls.dv_off);
-  for (int l = tid; l < lp; l += 128) sDv[l] = gDv[l];
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
   const uint32_t tmem = *tmem_holder;
-
   const int n_items = p.n_trees * p.n_rt;
   const int grid = gridDim.x;
-  auto load_a = [&](int item, int s) {
-    ptx::fence_proxy_async();
-    ptx::mbar_arrive_expect_tx(&bars[1 + s], a_bytes);
-    ptx::bulk_g2s(sA + (size_t)s * a_bytes, p.P + (size_t)item * a_bytes, a_bytes, &bars[1 + s]);
-  };
-  if (tid == 0) {
-    ptx::mbar_arrive_expect_tx(&bars[0], (uint32_t)p.b_bytes);
-    for (int o = 0; o < p.b_bytes; o += 32768)
-      ptx::bulk_g2s(sB + o, p.gbase + p.cls.cmat_off + o, (uint32_t)min(32768, p.b_bytes - o), &bars[0]);
-    if ((int)blockIdx.x < n_items) load_a(blockIdx.x, 0);
-    if ((int)blockIdx.x + grid < n_items) load_a(blockIdx.x + grid, 1);
-    ptx::mbar_wait(&bars[0], 0);
-  }
-  const uint32_t idesc = umma::idesc_i8(lp);
-  const uint32_t sA_u = ptx::s2u(sA), sB_u = ptx::s2u(sB);
-  uint32_t aphase[2] = {0, 0}, mphase[2] = {0, 0};
 
-  auto epilogue = [&](int item, int s) {
-    ptx::mbar_wait(&bars[3 + s], mphase[s]);
-    mphase[s] ^= 1;
-    umma::fence_after();
-    if (tid == 0 && item + 2 * grid < n_items) load_a(item + 2 * grid, s);  // A stage s is free now
-    const int t = item / p.n_rt, rt = item % p.n_rt;
-    const int row = rt * 128 + warp * 32 + lane;
-    const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(s * lp);
-    int leaf = -1;
-    for (int cb = 0; cb < lp; cb += 16) {
-      uint32_t v[16];
-      umma::ld16(tbase + cb, v);
-      umma::wait_ld();
-      if (p.mode == 0) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j)
-          if ((int32_t)v[j] == sDv[cb + j]) leaf = cb + j;   // a4: the unique l with S == D_D
-      } else if (row < p.rows) {
-        int4* o = reinterpret_cast<int4*>(p.S + ((size_t)t * p.rows + row) * lp + cb);
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          o[j] = make_int4((int)v[4 * j], (int)v[4 * j + 1], (int)v[4 * j + 2], (int)v[4 * j + 3]);
+  if (warp == kPcEpiWarps) {
+    if (lane == 0) {
+      ptx::mbar_arrive_expect_tx(bfull, (uint32_t)p.b_bytes);
+      for (int o = 0; o < p.b_bytes; o += 32768)
+        ptx::bulk_g2s(sB + o, p.gbase + p.cls.cmat_off + o, (uint32_t)min(32768, p.b_bytes - o), bfull);
+      int k = 0;
+      for (int item = blockIdx.x; item < n_items; item += grid, ++k) {
+        const int s = k % NS;
+        ptx::mbar_wait(&aempty[s], ((k / NS) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&afull[s], a_bytes);
+        ptx::bulk_g2s(sA + (size_t)s * a_bytes, p.P + (size_t)item * a_bytes, a_bytes, &afull[s]);
       }
     }
-    if (p.mode == 0 && row < p.rows) p.leaf[(size_t)t * p.rows + row] = (int16_t)leaf;
-    umma::fence_before();
-  };
-
-  int it = 0, prev_item = -1;
-  for (int item = blockIdx.x; item < n_items; item += grid, ++it) {
-    const int s = it & 1;
-    if (tid == 0) {
-      ptx::mbar_wait(&bars[1 + s], aphase[s]);
-      aphase[s] ^= 1;
+  } else if (warp == kPcEpiWarps + 1) {
+    if (lane == 0) {
+      ptx::mbar_wait(bfull, 0);
+      const uint32_t idesc = umma::idesc_i8(lp);
+      const uint32_t sA_u = ptx::s2u(sA), sB_u = ptx::s2u(sB);
+      int k = 0;
+      for (int item = blockIdx.x; item < n_items; item += grid, ++k) {
+        const int s = k % NS, acc = k & 1;
+        ptx::mbar_wait(&tempty[acc], ((k >> 1) & 1) ^ 1);   // epilogue drained this accumulator
+        ptx::mbar_wait(&afull[s], (k / NS) & 1);             // decision tile landed
+        umma::fence_after();
+        const uint32_t a0 = sA_u + (uint32_t)s * a_bytes;
+        for (int ks = 0; ks < ip / 32; ++ks) {
+          const uint64_t ad = umma::smem_desc(a0 + (uint32_t)ks * 2u * 2048u, 2048u, 128u);
+          const uint64_t bd = umma::smem_desc(sB_u + (uint32_t)ks * 2u * (uint32_t)lp * 16u, (uint32_t)lp * 16u, 128u);
+          umma::mma_i8(tmem + (uint32_t)(acc * lp), ad, bd, idesc, ks > 0 ? 1u : 0u);
+        }
+        umma::commit(&aempty[s]);   // A stage free once these MMAs have read it
+        umma::commit(&tfull[acc]);  // accumulator ready for the epilogue
+      }
+    }
+  } else {
+    // epilogue warps: thread = row of the tile (TMEM lane), a quarter of the columns
+    const int quad = warp & 3, part = warp >> 2;
+    const int n_parts = lp >= 64 ? 4 : lp / 16;      // 16-column tcgen05.ld granularity
+    const int cols = lp / n_parts;
+    const bool active = part < n_parts;
+    int k = 0;
+    for (int item = blockIdx.x; item < n_items; item += grid, ++k) {
+      const int acc = k & 1;
+      ptx::mbar_wait(&tfull[acc], (k >> 1) & 1);
       umma::fence_after();
-      const uint32_t a0 = sA_u + (uint32_t)s * a_bytes;
-      for (int ks = 0; ks < ip / 32; ++ks) {
-        const uint64_t ad = umma::smem_desc(a0 + (uint32_t)ks * 2u * 2048u, 2048u, 128u);
-        const uint64_t bd = umma::smem_desc(sB_u + (uint32_t)ks * 2u * (uint32_t)lp * 16u, (uint32_t)lp * 16u, 128u);
-        umma::mma_i8(tmem + (uint32_t)(s * lp), ad, bd, idesc, ks > 0 ? 1u : 0u);
+      const int t = item / p.n_rt, rt = item % p.n_rt;
+      const int row = rt * 128 + quad * 32 + lane;
+      const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * lp);
+      int leaf = -1;
+      const int L = 1 << D;
+      if (active) {
+        for (int cb = part * cols; cb < (part + 1) * cols; cb += 16) {
+          uint32_t v[16];
+          umma::ld16(tbase + cb, v);
+          umma::wait_ld();
+          if (p.mode == 0) {
+            // a4: D_D[l] = D - popc(l); popc(cb + j) = popc(cb) + popc(j) for j < 16
+            const int base = D - __popc(cb);
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if ((int32_t)v[j] + __popc(j) == base && cb + j < L) leaf = cb + j;
+          } else if (row < p.rows) {
+            int4* o = reinterpret_cast<int4*>(p.S + ((size_t)t * p.rows + row) * lp + cb);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              o[j] = make_int4((int)v[4 * j], (int)v[4 * j + 1], (int)v[4 * j + 2], (int)v[4 * j + 3]);
+          }
+        }
       }
-      umma::commit(&bars[3 + s]);
+      umma::fence_before();
+      ptx::mbar_arrive(&tempty[acc]);
+      if (p.mode == 0 && leaf >= 0 && row < p.rows) p.leaf[(size_t)t * p.rows + row] = (int16_t)leaf;
     }
-    if (prev_item >= 0) epilogue(prev_item, s ^ 1);
-    __syncthreads();  // TMEM stage s^1 free for the next MMA
-    prev_item = item;
   }
-  if (prev_item >= 0) epilogue(prev_item, (it - 1) & 1);
   __syncthreads();
   umma::fence_after();
-  if (warp == 0)
+  if (warp == kPcEpiWarps)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols) : "memory");
 }
 
@@ -438,7 +476,7 @@ static cudaError_t launch_gc(const float* X, int64_t row0, int32_t rows, int32_t
   int tpc = std::max(1, (int)((int64_t)n_t * n_rt / (4 * 148)));
   tpc = std::min(tpc, n_t);
   dim3 grid(n_rt, (n_t + tpc - 1) / tpc);
-  const int smem = 129 * F * 4;
+  const int smem = 129 * F * 4 + 2 * c.i_pad * 8;
   if (smem > 48 * 1024) {
     cudaFuncSetAttribute(gc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
     cudaFuncSetAttribute(gc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
@@ -466,7 +504,12 @@ static cudaError_t launch_pc(const int8_t* P, const uint8_t* gbase, const GemmCl
   p.leaf = leaf;
   p.S = S;
   const int a_bytes = 128 * c.i_pad;
-  int smem = (p.b_bytes + 1023) / 1024 * 1024 + 2 * a_bytes + 6 * 8 + 4 * c.l_pad + 64;
+  const int b_al = (p.b_bytes + 1023) / 1024 * 1024;
+  // as deep an A ring as fits next to C_D (2..8 stages)
+  int stages = 8;
+  while (stages > 2 && b_al + stages * a_bytes + 256 > kSmemMax) --stages;
+  p.stages = stages;
+  int smem = b_al + stages * a_bytes + (5 + 2 * stages) * 8 + 16 + 64;
   // co-resident CTAs must fit in the 512 TMEM columns of an SM: pad the
   // shared-memory request so no more CTAs than that are placed per SM
   const int tmem_occ = std::max(1, 512 / cols);
@@ -474,13 +517,13 @@ static cudaError_t launch_pc(const int8_t* P, const uint8_t* gbase, const GemmCl
   cudaError_t e = cudaFuncSetAttribute(pc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
   if (e != cudaSuccess) return e;
   int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pc_kernel, 128, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pc_kernel, kPcThreads, smem);
   occ = std::max(1, std::min(occ, tmem_occ));
   const int n_items = n_trees * p.n_rt;
   const int grid = std::max(1, std::min(n_items, dev_sms(dev) * occ));
   cudaEvent_t ev;
   hot_begin(st, &ev);
-  pc_kernel<<<grid, 128, smem, st>>>(p);
+  pc_kernel<<<grid, kPcThreads, smem, st>>>(p);
   hot_end(st, ev);
   count_launch();
   return cudaGetLastError();

@@ -156,6 +156,45 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def gemm_roofline(B, m, cfg, X, dev, args):
+    """The paper's GEMM form of steps a1..a4 on the same input: int8 tcgen05
+    path-contraction kernel (K2) throughput vs the measured int8 tensor peak,
+    and the whole GEMM variant's step time (the variant AUTO does not pick)."""
+    import torch
+    try:
+        with open(os.path.join(ROOT, "profiles", "int8_peak.json")) as fh:
+            peak = json.load(fh)["int8_tops_burst"]
+            src = "measured (profiles/int8_peak.json: cuBLASLt s8 8192^3)"
+    except Exception:
+        peak, src = 2 * _peaks()[0].get("bf16_tflops", 1590.0), "bf16 measured x 2 (nominal int8/bf16 ratio)"
+    g = B.Model(m, device=dev.index, variant="gemm")
+    n = X.shape[0]
+    out = torch.empty(n, dtype=torch.int32, device=dev) if cfg.kind == "classification" else torch.empty((n, 1), device=dev)
+    for _ in range(2):
+        g.predict(X, out=out)
+    torch.cuda.synchronize(dev)
+    steps = 2
+    B.hot_kernel_timing(True)
+    B.hot_kernel_time()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        g.predict(X, out=out)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    k2_ms, k2_n = B.hot_kernel_time()
+    B.hot_kernel_timing(False)
+    step_ms = e0.elapsed_time(e1) / steps
+    ip, lp = B.gemm_geometry(cfg.depth)
+    ops = 2.0 * n * cfg.n_trees * ip * lp * steps        # dense int8 ops of the contraction (padded)
+    achieved = ops / (k2_ms / 1e3) / 1e12
+    return {"kernel": "pc_kernel (tcgen05.mma.cta_group::1.kind::i8, TMEM accumulators)", "bound": "tensor",
+            "achieved": achieved, "peak": peak, "unit": "TOP/s", "frac": achieved / peak, "peak_source": src,
+            "k2_ms_per_step": k2_ms / steps, "k2_launches_per_step": k2_n // steps,
+            "gemm_variant_ms_per_step": step_ms, "gemm_variant_rows_per_s": n / (step_ms / 1e3),
+            "note": "GEMM form of a1..a4 (decisions materialised per 128-row tile); AUTO selects the traversal"}
+
+
 def workload_config(cfg, world):
     return {"workload": f"{cfg.name}: {cfg.describe}", "n_rows_per_gpu": cfg.n_rows, "n_trees": cfg.n_trees,
             "depth": cfg.depth, "n_features": cfg.n_features, "n_outputs": cfg.n_classes,
@@ -173,6 +212,7 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--variant", default=None, choices=[None, "auto", "traverse", "gemm"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-gemm", action="store_true", help="skip the GEMM-form (tcgen05) sub-measurement")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--rows", type=int, default=None, help="override rows per GPU (exploration; reported in config)")
     ap.add_argument("--trees", type=int, default=None, help="override ensemble size (exploration)")
@@ -297,6 +337,8 @@ def main():
         "config": workload_config(cfg, world), "variant": variant, "exact_tier": info["exact_tier"],
         "gpu_launches": launches, "wall_s_timed": t_wall, "roofline": roof, "e2e": e2e, "clocks": clocks,
     }
+    if cfg.depth <= 8 and not args.no_gemm:
+        line["path_contraction"] = gemm_roofline(B, m, cfg, X, dev, args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(m, cfg)
     if rank == 0:

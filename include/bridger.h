@@ -111,8 +111,10 @@ typedef enum { BRIDGER_EXACT_E53 = 0, BRIDGER_EXACT_E63 = 1, BRIDGER_EXACT_F64 =
  * K outside [1,64]), E_INVALID_TREE (offsets not increasing; exactly one of
  * left/right == -1; child out of range or == self; a node with != 1 parent or
  * unreachable from 0; feature outside [0,F); NaN threshold; non-finite leaf
- * value), E_UNSUPPORTED (padded depth > 14, SIGMOID with K != 1 or regression),
- * E_CUDA, E_OOM.  *out is set only on success. */
+ * value), E_UNSUPPORTED (SIGMOID with K != 1 or regression), E_CUDA, E_OOM.
+ * Any depth is accepted: trees deeper than 14 levels or too unbalanced to pad
+ * into perfect heaps use the sparse pointer layout (DESIGN.md §6, §8(f3)).
+ * *out is set only on success. */
 bridger_status bridger_model_load(const bridger_model_desc* desc, int cuda_device, bridger_model** out);
 bridger_status bridger_model_free(bridger_model* m); /* NULL is OK; synchronises the device */
 
@@ -123,7 +125,8 @@ bridger_status bridger_model_info(const bridger_model* m, int32_t* max_depth, in
                                   int32_t* acc_is_int64, int32_t* acc_scale_exp);
 bridger_status bridger_model_set_variant(bridger_model* m, int32_t variant); /* bridger_variant */
 /* Traversal layout chosen at load: number of tree chunks,
- * threshold-bin coded mode (4-byte nodes + u16 input codes), global-tree mode
+ * node format (*coded: 0 heap fp32, 1 threshold-bin codes, 2 sparse pointer
+ * layout for deep / unbalanced trees), global-tree mode
  * (trees too large for shared memory), warps per CTA and warps per row block.
  * Any output pointer may be NULL. */
 bridger_status bridger_model_layout(const bridger_model* m, int32_t* n_chunks, int32_t* coded, int32_t* global_trees,

@@ -249,8 +249,9 @@ class Model:
     def layout(self) -> dict:
         n, c, g, w, gr = (C.c_int32() for _ in range(5))
         _check(_lib.bridger_model_layout(self._h, C.byref(n), C.byref(c), C.byref(g), C.byref(w), C.byref(gr)))
-        return dict(n_chunks=n.value, coded=bool(c.value), global_trees=bool(g.value), n_warps=w.value,
-                    group=gr.value)
+        return dict(n_chunks=n.value, coded=c.value == 1, sparse=c.value == 2,
+                    format={0: "heap", 1: "codes", 2: "sparse"}[c.value], global_trees=bool(g.value),
+                    n_warps=w.value, group=gr.value)
 
     def set_variant(self, name: str):
         _check(_lib.bridger_model_set_variant(self._h, VARIANTS[name]))

@@ -111,6 +111,8 @@ static void free_model(bridger_model* m) {
   cudaFree(m->d_leaf_ids);
   cudaFree(m->d_base);
   cudaFree(m->d_bin_table);
+  cudaFree(m->d_sparse_trees);
+  cudaFree(m->d_sparse_nodes);
   cudaFree(m->d_bin_offsets);
   gemm_free(m);
   delete m;
@@ -265,7 +267,7 @@ bridger_status bridger_model_load(const bridger_model_desc* d, int cuda_device, 
     depth[t] = tree_depth(d, t);
     Dmax = std::max(Dmax, depth[t]);
   }
-  if (Dmax > 14) return fail(BRIDGER_E_UNSUPPORTED, "padded depth " + std::to_string(Dmax) + " > 14");
+  if (Dmax > 1000000) return fail(BRIDGER_E_UNSUPPORTED, "tree depth > 1e6");
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
@@ -319,7 +321,9 @@ bridger_status bridger_model_load(const bridger_model_desc* d, int cuda_device, 
         (e = upload(&m->d_slot_leafid_off, L.slot_leafid_off.data(), L.slot_leafid_off.size())) != cudaSuccess ||
         (e = upload(&m->d_leaf_ids, L.leaf_ids.data(), L.leaf_ids.size())) != cudaSuccess ||
         (e = upload(&m->d_bin_table, L.bin_table.data(), L.bin_table.size())) != cudaSuccess ||
-        (e = upload(&m->d_bin_offsets, L.bin_offsets.data(), L.bin_offsets.size())) != cudaSuccess) {
+        (e = upload(&m->d_bin_offsets, L.bin_offsets.data(), L.bin_offsets.size())) != cudaSuccess ||
+        (e = upload(reinterpret_cast<SparseTree**>(&m->d_sparse_trees), L.sparse_trees.data(), L.sparse_trees.size())) != cudaSuccess ||
+        (e = upload(reinterpret_cast<uint32_t**>(&m->d_sparse_nodes), L.sparse_nodes.data(), L.sparse_nodes.size())) != cudaSuccess) {
       free_model(m);
       return e == cudaErrorMemoryAllocation ? fail(BRIDGER_E_OOM, "device allocation failed") : cuda_fail(e, "upload");
     }
@@ -376,7 +380,7 @@ bridger_status bridger_model_layout(const bridger_model* m, int32_t* n_chunks, i
                                     int32_t* n_warps, int32_t* group) {
   if (!m) return fail(BRIDGER_E_NULL_ARG, "model is NULL");
   if (n_chunks) *n_chunks = m->trav_ok ? (int32_t)m->trav.chunks.size() : 0;
-  if (coded) *coded = m->trav_ok && m->trav.codes ? 1 : 0;
+  if (coded) *coded = m->trav_ok && m->trav.codes ? 1 : (m->trav_ok && m->trav.sparse ? 2 : 0);
   if (global_trees) *global_trees = m->trav_ok && m->trav.global_trees ? 1 : 0;
   if (n_warps) *n_warps = m->trav.n_warps;
   if (group) *group = m->trav.group;

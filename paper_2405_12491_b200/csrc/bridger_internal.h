@@ -66,12 +66,24 @@ struct TravChunk {
   int32_t pad_;
 };
 
+// Sparse (pointer) tree descriptor (§8(f3)): unbounded / unbalanced trees.
+struct SparseTree {
+  int64_t node_off;    // first 16-byte node record of the tree
+  int64_t leaf_off;    // first leaf value (float index) of the tree
+  int64_t leafid_off;  // first original leaf id of the tree
+  int32_t depth;       // longest root-to-leaf path (internal nodes)
+  int32_t slot_tree;   // original tree index
+};
+
 struct TravLayout {
   int32_t n_warps = 16;         // warps per CTA
   int32_t group = 2;            // warps sharing one 32-row X block (they split the chunk's trees)
   bool use_cluster = false;     // cross-chunk reduction over DSMEM (else global partials)
   bool global_trees = false;    // trees too large for shared memory: walked from global memory
   bool codes = false;           // threshold-bin codes: 4-byte nodes, u16 X codes (see lowering.cpp)
+  bool sparse = false;          // pointer-format trees (deep / unbalanced), walked from global memory
+  std::vector<SparseTree> sparse_trees;
+  std::vector<uint32_t> sparse_nodes;   // [n][4] records
   std::vector<float> bin_table;     // concatenated sorted distinct thresholds per feature
   std::vector<int32_t> bin_offsets; // [F+1]
   int32_t smem_bytes = 0;       // dynamic shared memory per CTA
@@ -138,6 +150,8 @@ struct bridger_model {
   int64_t* d_slot_leafid_off = nullptr;
   int32_t* d_leaf_ids = nullptr;
   double* d_base = nullptr;
+  void* d_sparse_trees = nullptr;    // SparseTree[T] (TravLayout::sparse)
+  void* d_sparse_nodes = nullptr;    // uint4 records
   float* d_bin_table = nullptr;      // threshold-bin codes (TravLayout::codes)
   int32_t* d_bin_offsets = nullptr;
 

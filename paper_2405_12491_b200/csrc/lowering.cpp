@@ -244,9 +244,104 @@ static uint32_t code_of_threshold(const TravLayout& L, int32_t f, float t) {
   return (uint32_t)(std::lower_bound(b, e, t) - b);  // t is present: exact index
 }
 
+// Sparse (pointer) layout (§8(f3)): each tree in BFS order with the two
+// children of a node adjacent, 16-byte records {threshold, feature |
+// missing<<30 | leaf<<31, left-child index | leaf index, 0}, leaf values per
+// tree.  Used for trees deeper than the heap layouts allow or so unbalanced
+// that padding them to perfect trees would blow up (sklearn max_depth=None).
+static void build_sparse_layout(const bridger_model_desc* d, const Exactness& ex, bool acc_int, TravLayout* out) {
+  const int32_t T = d->n_trees, F = d->n_features, K = d->n_outputs;
+  out->sparse = true;
+  out->global_trees = true;
+  out->codes = false;
+  out->bin_table.clear();
+  out->bin_offsets.clear();
+  out->sparse_trees.assign(T, SparseTree{});
+  out->sparse_nodes.clear();
+  out->slot_tree.assign(T, 0);
+  out->slot_leafid_off.assign(T, 0);
+  out->leaf_ids.clear();
+  std::vector<float> leaves;
+  std::vector<std::pair<int32_t, int32_t>> q;
+  for (int32_t t = 0; t < T; ++t) {
+    const int64_t a = d->tree_offsets[t];
+    SparseTree& st = out->sparse_trees[t];
+    st.node_off = (int64_t)(out->sparse_nodes.size() / 4);
+    st.leaf_off = (int64_t)leaves.size();
+    st.leafid_off = (int64_t)out->leaf_ids.size();
+    st.slot_tree = t;
+    int32_t dmax = 0, n_leaf = 0;
+    q.clear();
+    q.push_back({0, 0});
+    for (size_t i = 0; i < q.size(); ++i) {
+      const int32_t n = q[i].first, dep = q[i].second;
+      const int64_t g = a + n;
+      uint32_t rec[4] = {0, 0, 0, 0};
+      if (d->left[g] == -1) {
+        rec[1] = 1u << 31;
+        rec[2] = (uint32_t)n_leaf++;
+        for (int32_t k = 0; k < K; ++k) {
+          const float v = d->value[g * K + k];
+          leaves.push_back(acc_int ? std::ldexp(v, -ex.q) : v);
+        }
+        out->leaf_ids.push_back(n);
+        dmax = std::max(dmax, dep);
+      } else {
+        std::memcpy(&rec[0], &d->threshold[g], 4);
+        rec[1] = (uint32_t)d->feature[g] | ((d->missing_left && d->missing_left[g]) ? (1u << 30) : 0u);
+        rec[2] = (uint32_t)q.size();
+        q.push_back({d->left[g], dep + 1});
+        q.push_back({d->right[g], dep + 1});
+      }
+      out->sparse_nodes.insert(out->sparse_nodes.end(), rec, rec + 4);
+    }
+    st.depth = dmax;
+    out->slot_leafid_off[t] = st.leafid_off;
+    out->slot_tree[t] = t;
+  }
+  out->data.assign(reinterpret_cast<const uint8_t*>(leaves.data()),
+                   reinterpret_cast<const uint8_t*>(leaves.data()) + leaves.size() * 4);
+  out->data.resize((out->data.size() + 127) / 128 * 128 + 128, 0);
+  TravChunk c{};
+  c.offset = 0;
+  c.bytes = (int32_t)std::min<size_t>(out->data.size(), INT32_MAX / 2);
+  c.n_trees = T;
+  c.depth = 0;
+  c.leaf_offset = 0;
+  c.first_slot = 0;
+  out->chunks.assign(1, c);
+  int32_t nb = 16;
+  while (nb > 1 && nb * 256 * F > 200 * 1024) nb /= 2;
+  out->n_warps = 16;
+  out->group = 16 / nb;
+  out->chunk_budget = 0;
+  out->smem_bytes = nb * 256 * F + 1024 + trav_bar_bytes(nb) + trav_red_bytes(nb, 16 / nb, K);
+}
+
 bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& depth,
                        const Exactness& ex, bool acc_int, TravLayout* out, std::string* why) {
   const int32_t T = d->n_trees, F = d->n_features, K = d->n_outputs;
+  {
+    // deep or badly unbalanced trees -> sparse pointer layout
+    int64_t orig = 0, padded = 0;
+    int32_t dmax = 0;
+    for (int32_t t = 0; t < T; ++t) {
+      orig += d->tree_offsets[t + 1] - d->tree_offsets[t];
+      dmax = std::max(dmax, depth[t]);
+      padded += depth[t] > 30 ? ((int64_t)1 << 40) : ((int64_t)2 << depth[t]) - 1;
+    }
+    const char* env = std::getenv("BRIDGER_SPARSE");
+    const bool sparse = env ? env[0] != '0' : (dmax > 14 || padded > 4 * orig + 4096);
+    out->has_missing = d->missing_left != nullptr;
+    out->use_cluster = false;
+    if (sparse) {
+      build_sparse_layout(d, ex, acc_int, out);
+      return true;
+    }
+    out->sparse = false;
+    out->sparse_trees.clear();
+    out->sparse_nodes.clear();
+  }
   out->has_missing = d->missing_left != nullptr;
   out->use_cluster = std::getenv("BRIDGER_CLUSTER") != nullptr;
   // coded nodes pay for the separate binning pass only when each input value

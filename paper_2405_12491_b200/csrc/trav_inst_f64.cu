@@ -2,8 +2,8 @@
 #include "traverse.cuh"
 
 namespace bridger {
-BRIDGER_TRAV_INSTANTIATE(double, false, false, false)
-BRIDGER_TRAV_INSTANTIATE(double, true, false, false)
-BRIDGER_TRAV_INSTANTIATE(double, false, false, true)
-BRIDGER_TRAV_INSTANTIATE(double, true, false, true)
+BRIDGER_TRAV_INSTANTIATE(double, false, false, 0)
+BRIDGER_TRAV_INSTANTIATE(double, true, false, 0)
+BRIDGER_TRAV_INSTANTIATE(double, false, false, 1)
+BRIDGER_TRAV_INSTANTIATE(double, true, false, 1)
 }  // namespace bridger

@@ -2,6 +2,6 @@
 #include "traverse.cuh"
 
 namespace bridger {
-BRIDGER_TRAV_INSTANTIATE(double, false, true, false)
-BRIDGER_TRAV_INSTANTIATE(double, true, true, false)
+BRIDGER_TRAV_INSTANTIATE(double, false, true, 0)
+BRIDGER_TRAV_INSTANTIATE(double, true, true, 0)
 }  // namespace bridger

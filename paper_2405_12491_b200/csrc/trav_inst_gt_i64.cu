@@ -2,6 +2,6 @@
 #include "traverse.cuh"
 
 namespace bridger {
-BRIDGER_TRAV_INSTANTIATE(long long, false, true, false)
-BRIDGER_TRAV_INSTANTIATE(long long, true, true, false)
+BRIDGER_TRAV_INSTANTIATE(long long, false, true, 0)
+BRIDGER_TRAV_INSTANTIATE(long long, true, true, 0)
 }  // namespace bridger

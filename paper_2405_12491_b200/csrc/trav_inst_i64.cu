@@ -2,6 +2,6 @@
 #include "traverse.cuh"
 
 namespace bridger {
-BRIDGER_TRAV_INSTANTIATE(long long, false, false, false)
-BRIDGER_TRAV_INSTANTIATE(long long, false, false, true)
+BRIDGER_TRAV_INSTANTIATE(long long, false, false, 0)
+BRIDGER_TRAV_INSTANTIATE(long long, false, false, 1)
 }  // namespace bridger

@@ -2,6 +2,6 @@
 #include "traverse.cuh"
 
 namespace bridger {
-BRIDGER_TRAV_INSTANTIATE(long long, true, false, false)
-BRIDGER_TRAV_INSTANTIATE(long long, true, false, true)
+BRIDGER_TRAV_INSTANTIATE(long long, true, false, 0)
+BRIDGER_TRAV_INSTANTIATE(long long, true, false, 1)
 }  // namespace bridger

@@ -12,25 +12,29 @@
 
 namespace bridger {
 
-#define BRIDGER_TRAV_EXTERN(ACC, ML, GT, CODES)                                                                           \
-  extern template cudaError_t launch_trav_t<1, ACC, ML, GT, CODES>(const TravParams&, int, int, int, int, cudaStream_t);  \
-  extern template cudaError_t launch_trav_t<2, ACC, ML, GT, CODES>(const TravParams&, int, int, int, int, cudaStream_t);  \
-  extern template cudaError_t launch_trav_t<4, ACC, ML, GT, CODES>(const TravParams&, int, int, int, int, cudaStream_t);  \
-  extern template cudaError_t launch_trav_t<8, ACC, ML, GT, CODES>(const TravParams&, int, int, int, int, cudaStream_t);  \
-  extern template cudaError_t launch_trav_t<16, ACC, ML, GT, CODES>(const TravParams&, int, int, int, int, cudaStream_t); \
-  extern template cudaError_t launch_trav_t<64, ACC, ML, GT, CODES>(const TravParams&, int, int, int, int, cudaStream_t);
-BRIDGER_TRAV_EXTERN(long long, false, false, false)
-BRIDGER_TRAV_EXTERN(long long, true, false, false)
-BRIDGER_TRAV_EXTERN(double, false, false, false)
-BRIDGER_TRAV_EXTERN(double, true, false, false)
-BRIDGER_TRAV_EXTERN(long long, false, false, true)
-BRIDGER_TRAV_EXTERN(long long, true, false, true)
-BRIDGER_TRAV_EXTERN(double, false, false, true)
-BRIDGER_TRAV_EXTERN(double, true, false, true)
-BRIDGER_TRAV_EXTERN(long long, false, true, false)
-BRIDGER_TRAV_EXTERN(long long, true, true, false)
-BRIDGER_TRAV_EXTERN(double, false, true, false)
-BRIDGER_TRAV_EXTERN(double, true, true, false)
+#define BRIDGER_TRAV_EXTERN(ACC, ML, GT, FMT)                                                                           \
+  extern template cudaError_t launch_trav_t<1, ACC, ML, GT, FMT>(const TravParams&, int, int, int, int, cudaStream_t);  \
+  extern template cudaError_t launch_trav_t<2, ACC, ML, GT, FMT>(const TravParams&, int, int, int, int, cudaStream_t);  \
+  extern template cudaError_t launch_trav_t<4, ACC, ML, GT, FMT>(const TravParams&, int, int, int, int, cudaStream_t);  \
+  extern template cudaError_t launch_trav_t<8, ACC, ML, GT, FMT>(const TravParams&, int, int, int, int, cudaStream_t);  \
+  extern template cudaError_t launch_trav_t<16, ACC, ML, GT, FMT>(const TravParams&, int, int, int, int, cudaStream_t); \
+  extern template cudaError_t launch_trav_t<64, ACC, ML, GT, FMT>(const TravParams&, int, int, int, int, cudaStream_t);
+BRIDGER_TRAV_EXTERN(long long, false, false, 0)
+BRIDGER_TRAV_EXTERN(long long, true, false, 0)
+BRIDGER_TRAV_EXTERN(double, false, false, 0)
+BRIDGER_TRAV_EXTERN(double, true, false, 0)
+BRIDGER_TRAV_EXTERN(long long, false, false, 1)
+BRIDGER_TRAV_EXTERN(long long, true, false, 1)
+BRIDGER_TRAV_EXTERN(double, false, false, 1)
+BRIDGER_TRAV_EXTERN(double, true, false, 1)
+BRIDGER_TRAV_EXTERN(long long, false, true, 0)
+BRIDGER_TRAV_EXTERN(long long, true, true, 0)
+BRIDGER_TRAV_EXTERN(double, false, true, 0)
+BRIDGER_TRAV_EXTERN(double, true, true, 0)
+BRIDGER_TRAV_EXTERN(long long, false, true, 2)
+BRIDGER_TRAV_EXTERN(long long, true, true, 2)
+BRIDGER_TRAV_EXTERN(double, false, true, 2)
+BRIDGER_TRAV_EXTERN(double, true, true, 2)
 
 // Threshold-bin coding of the input (§8(f2)): X [N][F] fp32 row-major ->
 // codes [n_blocks][F][32] u16, code = #{u in U_f : u < x} (binary search over
@@ -129,6 +133,8 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
   for (auto& c : L.chunks) maxc = std::max(maxc, c.bytes);
   p.chunk_cap = L.global_trees ? 0 : (maxc + 127) / 128 * 128;
   p.slot_tree = m->d_slot_tree;
+  p.sparse = static_cast<const SparseTree*>(m->d_sparse_trees);
+  p.sparse_nodes = static_cast<const uint4*>(m->d_sparse_nodes);
   p.slot_leafid_off = m->d_slot_leafid_off;
   p.leaf_ids = m->d_leaf_ids;
   p.T = m->T;
@@ -211,25 +217,32 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
   }
   BRIDGER_DISPATCH_KT(m->K, {
     auto launch = [&]() {
+      if (L.sparse) {
+        if (m->acc_int)
+          return L.has_missing ? launch_trav_t<KT, long long, true, true, 2>(p, grid, block, smem, cluster, st)
+                               : launch_trav_t<KT, long long, false, true, 2>(p, grid, block, smem, cluster, st);
+        return L.has_missing ? launch_trav_t<KT, double, true, true, 2>(p, grid, block, smem, cluster, st)
+                             : launch_trav_t<KT, double, false, true, 2>(p, grid, block, smem, cluster, st);
+      }
       if (L.codes) {
         if (m->acc_int)
-          return L.has_missing ? launch_trav_t<KT, long long, true, false, true>(p, grid, block, smem, cluster, st)
-                               : launch_trav_t<KT, long long, false, false, true>(p, grid, block, smem, cluster, st);
-        return L.has_missing ? launch_trav_t<KT, double, true, false, true>(p, grid, block, smem, cluster, st)
-                             : launch_trav_t<KT, double, false, false, true>(p, grid, block, smem, cluster, st);
+          return L.has_missing ? launch_trav_t<KT, long long, true, false, 1>(p, grid, block, smem, cluster, st)
+                               : launch_trav_t<KT, long long, false, false, 1>(p, grid, block, smem, cluster, st);
+        return L.has_missing ? launch_trav_t<KT, double, true, false, 1>(p, grid, block, smem, cluster, st)
+                             : launch_trav_t<KT, double, false, false, 1>(p, grid, block, smem, cluster, st);
       }
       if (L.global_trees) {
         if (m->acc_int)
-          return L.has_missing ? launch_trav_t<KT, long long, true, true, false>(p, grid, block, smem, cluster, st)
-                               : launch_trav_t<KT, long long, false, true, false>(p, grid, block, smem, cluster, st);
-        return L.has_missing ? launch_trav_t<KT, double, true, true, false>(p, grid, block, smem, cluster, st)
-                             : launch_trav_t<KT, double, false, true, false>(p, grid, block, smem, cluster, st);
+          return L.has_missing ? launch_trav_t<KT, long long, true, true, 0>(p, grid, block, smem, cluster, st)
+                               : launch_trav_t<KT, long long, false, true, 0>(p, grid, block, smem, cluster, st);
+        return L.has_missing ? launch_trav_t<KT, double, true, true, 0>(p, grid, block, smem, cluster, st)
+                             : launch_trav_t<KT, double, false, true, 0>(p, grid, block, smem, cluster, st);
       }
       if (m->acc_int)
-        return L.has_missing ? launch_trav_t<KT, long long, true, false, false>(p, grid, block, smem, cluster, st)
-                             : launch_trav_t<KT, long long, false, false, false>(p, grid, block, smem, cluster, st);
-      return L.has_missing ? launch_trav_t<KT, double, true, false, false>(p, grid, block, smem, cluster, st)
-                           : launch_trav_t<KT, double, false, false, false>(p, grid, block, smem, cluster, st);
+        return L.has_missing ? launch_trav_t<KT, long long, true, false, 0>(p, grid, block, smem, cluster, st)
+                             : launch_trav_t<KT, long long, false, false, 0>(p, grid, block, smem, cluster, st);
+      return L.has_missing ? launch_trav_t<KT, double, true, false, 0>(p, grid, block, smem, cluster, st)
+                           : launch_trav_t<KT, double, false, false, 0>(p, grid, block, smem, cluster, st);
     };
     err = launch();
     if (err != cudaSuccess && p.mode == TRAV_CLUSTER) {

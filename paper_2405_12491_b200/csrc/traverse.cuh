@@ -43,6 +43,7 @@ void hot_end(cudaStream_t st, cudaEvent_t start);
 // per-row partial sums into the leader CTA's shared memory over DSMEM
 // (st.shared::cluster + remote mbarrier arrive), the leader adds them in rank
 // order and finalizes -- no global partials, no second kernel.
+enum TravFmt : int { FMT_HEAP = 0, FMT_CODES = 1, FMT_SPARSE = 2 };
 enum TravMode : int32_t { TRAV_FINAL = 0, TRAV_PARTIAL = 1, TRAV_APPLY = 2, TRAV_CLUSTER = 3 };
 
 struct TravParams {
@@ -63,6 +64,8 @@ struct TravParams {
   const int64_t* slot_leafid_off;
   const int32_t* leaf_ids;
   int32_t T;
+  const SparseTree* sparse;  // FMT_SPARSE: per-slot tree descriptors
+  const uint4* sparse_nodes; //             16-byte node records
   int32_t group;      // warps sharing one 32-row block (tree split)
   int32_t red_off;    // byte offset of the intra-group partials
   int32_t slot_off;   // byte offset of the DSMEM reduction slots (TRAV_CLUSTER)
@@ -194,8 +197,70 @@ __device__ __forceinline__ void group_sync(int group, int G) {
   }
 }
 
-template <int KT, typename ACC, bool ML, bool GT, bool CODES>
+// Sparse (pointer) format for unbounded / unbalanced trees (§8(f3)): BFS order,
+// the two children of a node adjacent; record {threshold, feature | missing<<30
+// | leaf<<31, left-child index or leaf index, -}.  NI trees walk together;
+// lanes that reached a leaf idle until the pass's deepest tree is done.
+template <int NI, int KT, typename ACC, bool ML>
+__device__ __forceinline__ void walk_sparse(const TravParams& p, int t0, const float* xl, int K, int64_t row,
+                                            ACC (&acc)[KT]) {
+  int64_t base[NI];
+  int32_t idx[NI], leaf[NI];
+  int steps = 0;
+#pragma unroll
+  for (int u = 0; u < NI; ++u) {
+    const SparseTree td = p.sparse[t0 + u];
+    base[u] = td.node_off;
+    idx[u] = 0;
+    leaf[u] = -1;
+    steps = max(steps, td.depth + 1);
+  }
+  for (int s = 0; s < steps; ++s) {
+#pragma unroll
+    for (int u = 0; u < NI; ++u)
+      if (leaf[u] < 0) {
+        const uint4 r = __ldg(p.sparse_nodes + base[u] + idx[u]);
+        if (r.y >> 31) {
+          leaf[u] = (int32_t)r.z;
+        } else {
+          const float x = xl[(r.y & 0x3FFFFFFFu) * 32];
+          int go = !(x <= __uint_as_float(r.x));
+          if (ML) go &= !(((r.y >> 30) & 1u) & isnan(x));
+          idx[u] = (int32_t)r.z + go;
+        }
+      }
+  }
+#pragma unroll
+  for (int u = 0; u < NI; ++u) {
+    const SparseTree td = p.sparse[t0 + u];
+    if (p.mode == TRAV_APPLY) {
+      if (row < p.n_rows) p.out_leaf[row * p.T + td.slot_tree] = p.leaf_ids[td.leafid_off + leaf[u]];
+    } else {
+      const float* e = reinterpret_cast<const float*>(p.data) + td.leaf_off + (int64_t)leaf[u] * K;
+#pragma unroll
+      for (int k = 0; k < KT; ++k)
+        if (k < K) acc[k] += leaf_to_acc<ACC>(__ldg(e + k));
+    }
+  }
+}
+
+template <int KT, typename ACC, bool ML>
+__device__ __forceinline__ void walk_sparse_tail(int r, const TravParams& p, int t0, const float* xl, int K,
+                                                 int64_t row, ACC (&acc)[KT]) {
+  switch (r) {
+#define BRIDGER_STAIL(N) \
+  case N: walk_sparse<N, KT, ACC, ML>(p, t0, xl, K, row, acc); break;
+    BRIDGER_STAIL(1) BRIDGER_STAIL(2) BRIDGER_STAIL(3) BRIDGER_STAIL(4) BRIDGER_STAIL(5) BRIDGER_STAIL(6)
+    BRIDGER_STAIL(7) BRIDGER_STAIL(8)
+#undef BRIDGER_STAIL
+    default: break;
+  }
+}
+
+template <int KT, typename ACC, bool ML, bool GT, int FMT>
 __global__ void __launch_bounds__(512, 1) trav_kernel(const TravParams p) {
+  constexpr bool CODES = FMT == FMT_CODES;
+  constexpr bool SPARSE = FMT == FMT_SPARSE;
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
   const int G = p.group, NB = NW / G;          // G warps share each of NB row blocks
@@ -358,7 +423,19 @@ __global__ void __launch_bounds__(512, 1) trav_kernel(const TravParams p) {
         j += sz;
       }
     };
-    if (GT) {
+    if (SPARSE) {
+      // pointer-format trees from global memory: every CTA walks every tree
+      const int T = c.n_trees;
+      const int t0 = (int)((int64_t)T * gw / G), t1 = (int)((int64_t)T * (gw + 1) / G);
+      const int nt = t1 - t0;
+      const int n_pass = (nt + 7) / 8;
+      int j = t0;
+      for (int q = 0; q < n_pass; ++q) {
+        const int sz = nt / n_pass + (q < nt % n_pass ? 1 : 0);
+        walk_sparse_tail<KT, ACC, ML>(sz, p, j, static_cast<const float*>(xptr), K, row, acc);
+        j += sz;
+      }
+    } else if (GT) {
       // trees too large for shared memory: every CTA walks all chunks from
       // global memory (L1/L2), no cross-CTA combine
       for (int ci = 0; ci < nC; ++ci) {
@@ -448,10 +525,10 @@ __global__ void __launch_bounds__(256) trav_combine_kernel(const ACC* partial, i
   finalize_row<KT, ACC>(fin, row, acc);
 }
 
-template <int KT, typename ACC, bool ML, bool GT, bool CODES>
+template <int KT, typename ACC, bool ML, bool GT, int FMT>
 cudaError_t launch_trav_t(const TravParams& p, int grid_ctas, int block, int smem, int cluster,
                                  cudaStream_t st) {
-  auto kern = trav_kernel<KT, ACC, ML, GT, CODES>;
+  auto kern = trav_kernel<KT, ACC, ML, GT, FMT>;
   static int configured_smem = 0;  // per instantiation
   cudaError_t e;
   if (configured_smem < smem) {
@@ -501,12 +578,12 @@ cudaError_t launch_trav_t(const TravParams& p, int grid_ctas, int block, int sme
 }
 
 
-#define BRIDGER_TRAV_INSTANTIATE(ACC, ML, GT, CODES)                                                                  \
-  template cudaError_t launch_trav_t<1, ACC, ML, GT, CODES>(const TravParams&, int, int, int, int, cudaStream_t);  \
-  template cudaError_t launch_trav_t<2, ACC, ML, GT, CODES>(const TravParams&, int, int, int, int, cudaStream_t);  \
-  template cudaError_t launch_trav_t<4, ACC, ML, GT, CODES>(const TravParams&, int, int, int, int, cudaStream_t);  \
-  template cudaError_t launch_trav_t<8, ACC, ML, GT, CODES>(const TravParams&, int, int, int, int, cudaStream_t);  \
-  template cudaError_t launch_trav_t<16, ACC, ML, GT, CODES>(const TravParams&, int, int, int, int, cudaStream_t); \
-  template cudaError_t launch_trav_t<64, ACC, ML, GT, CODES>(const TravParams&, int, int, int, int, cudaStream_t);
+#define BRIDGER_TRAV_INSTANTIATE(ACC, ML, GT, FMT)                                                                  \
+  template cudaError_t launch_trav_t<1, ACC, ML, GT, FMT>(const TravParams&, int, int, int, int, cudaStream_t);  \
+  template cudaError_t launch_trav_t<2, ACC, ML, GT, FMT>(const TravParams&, int, int, int, int, cudaStream_t);  \
+  template cudaError_t launch_trav_t<4, ACC, ML, GT, FMT>(const TravParams&, int, int, int, int, cudaStream_t);  \
+  template cudaError_t launch_trav_t<8, ACC, ML, GT, FMT>(const TravParams&, int, int, int, int, cudaStream_t);  \
+  template cudaError_t launch_trav_t<16, ACC, ML, GT, FMT>(const TravParams&, int, int, int, int, cudaStream_t); \
+  template cudaError_t launch_trav_t<64, ACC, ML, GT, FMT>(const TravParams&, int, int, int, int, cudaStream_t);
 
 }  // namespace bridger

@@ -108,3 +108,28 @@ def test_regression_host_api():
     g = B.Model(m)
     out = g.predict_host(X).numpy()
     np.testing.assert_array_equal(out, oracle.run(m, X)["pred"])
+
+
+def test_sklearn_unbounded_depth_forest_sparse_layout():
+    """sklearn's default max_depth=None: deep, unbalanced trees (beyond any
+    perfect-heap padding) run in the sparse pointer layout (§8(f3))."""
+    X, y, _ = _data(51, 30000, 10, 4, nan_rate=0.005)
+    est = RandomForestClassifier(n_estimators=12, max_depth=None, random_state=0).fit(X, y)
+    assert max(e.tree_.max_depth for e in est.estimators_) > 14
+    m = from_sklearn_forest(est, 10, with_missing=True)
+    Xt, _, _ = _data(52, 7001, 10, 4, nan_rate=0.005)
+    g, _ = check(m, Xt)
+    assert g.layout()["format"] == "sparse"
+    np.testing.assert_array_equal(g.apply(dev(Xt)).cpu().numpy(), est.apply(Xt))
+    np.testing.assert_allclose(g.predict_proba(dev(Xt)).cpu().numpy(), est.predict_proba(Xt), atol=1e-6)
+
+
+def test_sparse_layout_forced_matches_heap(monkeypatch):
+    m = perfect_ensemble(53, 50, 7, 9, kind="regression", calib_rows=1024)
+    X = gen_x(54, 0, 4001, 9)
+    a = B.Model(m).predict(dev(X)).cpu().numpy()
+    monkeypatch.setenv("BRIDGER_SPARSE", "1")
+    g = B.Model(m)
+    assert g.layout()["format"] == "sparse"
+    np.testing.assert_array_equal(g.predict(dev(X)).cpu().numpy(), a)
+    check(m, X)

@@ -301,7 +301,9 @@ bridger_status bridger_model_load(const bridger_model_desc* d, int cuda_device, 
   m->acc_int = m->ex.tier != BRIDGER_EXACT_F64;
 
   std::string why;
-  m->trav_ok = build_trav_layout(d, depth, m->ex, m->acc_int, &m->trav, &why);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
+  m->trav_ok = build_trav_layout(d, depth, m->ex, m->acc_int, sms, &m->trav, &why);
   std::string why_gemm;
   DeviceGuard g(cuda_device);
   {
@@ -380,7 +382,8 @@ bridger_status bridger_model_layout(const bridger_model* m, int32_t* n_chunks, i
                                     int32_t* n_warps, int32_t* group) {
   if (!m) return fail(BRIDGER_E_NULL_ARG, "model is NULL");
   if (n_chunks) *n_chunks = m->trav_ok ? (int32_t)m->trav.chunks.size() : 0;
-  if (coded) *coded = m->trav_ok && m->trav.codes ? 1 : (m->trav_ok && m->trav.sparse ? 2 : 0);
+  if (coded)
+    *coded = !m->trav_ok ? 0 : m->trav.codes ? 1 : m->trav.sparse ? 2 : m->trav.pretransposed ? 3 : 0;
   if (global_trees) *global_trees = m->trav_ok && m->trav.global_trees ? 1 : 0;
   if (n_warps) *n_warps = m->trav.n_warps;
   if (group) *group = m->trav.group;

@@ -82,6 +82,7 @@ struct TravLayout {
   bool global_trees = false;    // trees too large for shared memory: walked from global memory
   bool codes = false;           // threshold-bin codes: 4-byte nodes, u16 X codes (see lowering.cpp)
   bool sparse = false;          // pointer-format trees (deep / unbalanced), walked from global memory
+  bool pretransposed = false;   // fp32 input transposed once into feature-major blocks (wide X, many chunks)
   std::vector<SparseTree> sparse_trees;
   std::vector<uint32_t> sparse_nodes;   // [n][4] records
   std::vector<float> bin_table;     // concatenated sorted distinct thresholds per feature
@@ -108,7 +109,7 @@ inline int32_t trav_slot_bytes(int32_t nb, int32_t n_chunks, int32_t K) {
 // Builds the resident-chunk layout; returns false (with reason) when a single
 // tree does not fit the shared-memory budget.
 bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& depth,
-                       const Exactness& ex, bool acc_int, TravLayout* out, std::string* why);
+                       const Exactness& ex, bool acc_int, int32_t sms, TravLayout* out, std::string* why);
 
 // --------------------------------------------------- GEMM-path layout -------
 struct GemmClass {

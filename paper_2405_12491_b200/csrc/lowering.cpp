@@ -319,7 +319,7 @@ static void build_sparse_layout(const bridger_model_desc* d, const Exactness& ex
 }
 
 bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& depth,
-                       const Exactness& ex, bool acc_int, TravLayout* out, std::string* why) {
+                       const Exactness& ex, bool acc_int, int32_t sms, TravLayout* out, std::string* why) {
   const int32_t T = d->n_trees, F = d->n_features, K = d->n_outputs;
   {
     // deep or badly unbalanced trees -> sparse pointer layout
@@ -419,7 +419,13 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
         size_t j = i;
         int32_t total = 0;
         while (j < runs.size() && runs[j].D == runs[i].D) total += runs[j++].n;
-        const int32_t nc = (int32_t)(j - i);
+        int32_t nc = (int32_t)(j - i);
+        // many chunks of one depth: round the count up to a multiple of the SM
+        // count so the one-CTA-per-chunk grid fills every SM (C5-like models)
+        if (!out->global_trees && sms > 0 && nc > sms / 2 && nc % sms != 0) {
+          const int32_t nc2 = (nc + sms - 1) / sms * sms;
+          if (nc2 <= total) nc = nc2;
+        }
         int32_t st = runs[i].start;
         for (int32_t c = 0; c < nc; ++c) {
           const int32_t n = total / nc + (c < total % nc ? 1 : 0);
@@ -442,6 +448,13 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
   out->n_warps = nw;
   out->group = G;
   out->chunk_budget = budget;
+  {
+    // wide inputs walked by many chunks: transpose X once into feature-major
+    // blocks instead of once per chunk CTA (measured: C5-shaped models)
+    const char* env = std::getenv("BRIDGER_PRET");
+    const int64_t work = (int64_t)F * (int64_t)bal.size();
+    out->pretransposed = !out->codes && !out->global_trees && (env ? env[0] != '0' : work >= 1024);
+  }
   out->chunks.clear();
   out->data.clear();
   out->slot_tree.assign(T, 0);

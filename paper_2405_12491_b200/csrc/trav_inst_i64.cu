@@ -4,4 +4,5 @@
 namespace bridger {
 BRIDGER_TRAV_INSTANTIATE(long long, false, false, 0)
 BRIDGER_TRAV_INSTANTIATE(long long, false, false, 1)
+BRIDGER_TRAV_INSTANTIATE(long long, false, false, 3)
 }  // namespace bridger

@@ -4,4 +4,5 @@
 namespace bridger {
 BRIDGER_TRAV_INSTANTIATE(long long, true, false, 0)
 BRIDGER_TRAV_INSTANTIATE(long long, true, false, 1)
+BRIDGER_TRAV_INSTANTIATE(long long, true, false, 3)
 }  // namespace bridger

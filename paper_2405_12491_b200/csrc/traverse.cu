@@ -31,6 +31,10 @@ BRIDGER_TRAV_EXTERN(long long, false, true, 0)
 BRIDGER_TRAV_EXTERN(long long, true, true, 0)
 BRIDGER_TRAV_EXTERN(double, false, true, 0)
 BRIDGER_TRAV_EXTERN(double, true, true, 0)
+BRIDGER_TRAV_EXTERN(long long, false, false, 3)
+BRIDGER_TRAV_EXTERN(long long, true, false, 3)
+BRIDGER_TRAV_EXTERN(double, false, false, 3)
+BRIDGER_TRAV_EXTERN(double, true, false, 3)
 BRIDGER_TRAV_EXTERN(long long, false, true, 2)
 BRIDGER_TRAV_EXTERN(long long, true, true, 2)
 BRIDGER_TRAV_EXTERN(double, false, true, 2)
@@ -101,6 +105,35 @@ __global__ void __launch_bounds__(512) bin_kernel(const float* __restrict__ X, i
       for (int u = 0; u < 4; ++u)
         if (f0 + u < F) dst[(f0 + u) * 32 + lane] = isnan(x[u]) ? (uint16_t)0xFFFF : (uint16_t)lo[u];
     }
+    __syncwarp();
+  }
+}
+
+// Pre-transposed input (FMT_HEAP_T): X [N][F] fp32 row-major -> [n_blocks][F][32]
+// fp32, the traversal's feature-major 32-row block layout, written once so
+// that every chunk CTA bulk-copies blocks with no per-chunk transpose.
+__global__ void __launch_bounds__(512) xpose_kernel(const float* __restrict__ X, int64_t n_rows, int32_t F,
+                                                    float* __restrict__ XT) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
+  const int S = F | 1;
+  float* St = reinterpret_cast<float*>(smem) + (size_t)warp * 32 * S;
+  const int64_t n_blocks = (n_rows + 31) / 32;
+  for (int64_t blk = (int64_t)blockIdx.x * NW + warp; blk < n_blocks; blk += (int64_t)gridDim.x * NW) {
+    const int64_t row0 = blk * 32;
+    const int rows = (int)(n_rows - row0 < 32 ? n_rows - row0 : 32);
+    const float* src = X + row0 * F;
+    for (int r = 0; r < 32; ++r)
+      for (int f = lane; f < F; f += 32) {
+        const uint32_t dsts = ptx::s2u(St + r * S + f);
+        const float* g = src + (int64_t)(r < rows ? r : 0) * F + f;
+        const uint32_t nbytes = r < rows ? 4u : 0u;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dsts), "l"(g), "r"(nbytes) : "memory");
+      }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    float* dst = XT + blk * 32 * (int64_t)F;
+    for (int f = 0; f < F; ++f) dst[f * 32 + lane] = St[lane * S + f];
     __syncwarp();
   }
 }
@@ -214,6 +247,30 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
       return err;
     }
     p.X = static_cast<const float*>(codes);
+  } else if (L.pretransposed && want != 3) {
+    const int64_t nbk = (n_rows + 31) / 32;
+    err = cudaMallocAsync(&codes, (size_t)nbk * 32 * m->F * 4, st);
+    if (err != cudaSuccess) return err;
+    int nwx = 16;
+    while (nwx > 1 && nwx * 32 * (m->F | 1) * 4 > 200 * 1024) --nwx;
+    const int xsmem = nwx * 32 * (m->F | 1) * 4;
+    static bool x_attr = false;
+    if (!x_attr) {
+      cudaFuncSetAttribute(xpose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+      x_attr = true;
+    }
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, xpose_kernel, nwx * 32, xsmem);
+    const int64_t want_ctas = (nbk + nwx - 1) / nwx;
+    const int xgrid = (int)std::max<int64_t>(1, std::min<int64_t>(want_ctas, (int64_t)sms * std::max(1, occ)));
+    xpose_kernel<<<xgrid, nwx * 32, xsmem, st>>>(X, n_rows, m->F, static_cast<float*>(codes));
+    count_launch();
+    err = cudaGetLastError();
+    if (err != cudaSuccess) {
+      cudaFreeAsync(codes, st);
+      return err;
+    }
+    p.X = static_cast<const float*>(codes);
   }
   BRIDGER_DISPATCH_KT(m->K, {
     auto launch = [&]() {
@@ -223,6 +280,13 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
                                : launch_trav_t<KT, long long, false, true, 2>(p, grid, block, smem, cluster, st);
         return L.has_missing ? launch_trav_t<KT, double, true, true, 2>(p, grid, block, smem, cluster, st)
                              : launch_trav_t<KT, double, false, true, 2>(p, grid, block, smem, cluster, st);
+      }
+      if (L.pretransposed && want != 3) {
+        if (m->acc_int)
+          return L.has_missing ? launch_trav_t<KT, long long, true, false, 3>(p, grid, block, smem, cluster, st)
+                               : launch_trav_t<KT, long long, false, false, 3>(p, grid, block, smem, cluster, st);
+        return L.has_missing ? launch_trav_t<KT, double, true, false, 3>(p, grid, block, smem, cluster, st)
+                             : launch_trav_t<KT, double, false, false, 3>(p, grid, block, smem, cluster, st);
       }
       if (L.codes) {
         if (m->acc_int)

@@ -43,7 +43,7 @@ void hot_end(cudaStream_t st, cudaEvent_t start);
 // per-row partial sums into the leader CTA's shared memory over DSMEM
 // (st.shared::cluster + remote mbarrier arrive), the leader adds them in rank
 // order and finalizes -- no global partials, no second kernel.
-enum TravFmt : int { FMT_HEAP = 0, FMT_CODES = 1, FMT_SPARSE = 2 };
+enum TravFmt : int { FMT_HEAP = 0, FMT_CODES = 1, FMT_SPARSE = 2, FMT_HEAP_T = 3 };
 enum TravMode : int32_t { TRAV_FINAL = 0, TRAV_PARTIAL = 1, TRAV_APPLY = 2, TRAV_CLUSTER = 3 };
 
 struct TravParams {
@@ -261,6 +261,10 @@ template <int KT, typename ACC, bool ML, bool GT, int FMT>
 __global__ void __launch_bounds__(512, 1) trav_kernel(const TravParams p) {
   constexpr bool CODES = FMT == FMT_CODES;
   constexpr bool SPARSE = FMT == FMT_SPARSE;
+  // PRE: the input arrives pre-laid-out as feature-major [F][32] blocks (u16
+  // codes or pre-transposed fp32), bulk-copied into two buffers per group
+  constexpr bool PRE = CODES || FMT == FMT_HEAP_T;
+  constexpr uint32_t EB = CODES ? 2u : 4u;
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
   const int G = p.group, NB = NW / G;          // G warps share each of NB row blocks
@@ -274,7 +278,7 @@ __global__ void __launch_bounds__(512, 1) trav_kernel(const TravParams p) {
   uint8_t* cdata = smem;
   // per row-block group: fp32 mode  Xs [F][32] float + St [32][F] float (256*F B)
   //                      codes mode Cb[2] [F][32] u16, double buffered (128*F B)
-  const size_t xblk = CODES ? (size_t)128 * F : (size_t)256 * F;
+  const size_t xblk = CODES ? (size_t)128 * F : (size_t)256 * F;  // HEAP_T: 2 x 128F, same as Xs + St
   float* Xs = reinterpret_cast<float*>(smem + p.chunk_cap + (size_t)grp * xblk);  // [F][32]
   float* St = Xs + 32 * F;                                                         // [32][F]
   uint16_t* Cb = reinterpret_cast<uint16_t*>(smem + p.chunk_cap + (size_t)grp * xblk);
@@ -324,17 +328,18 @@ __global__ void __launch_bounds__(512, 1) trav_kernel(const TravParams p) {
     }
   };
   // codes mode: blocks of the binned input are [F][32] u16, always complete
-  const uint16_t* codes = reinterpret_cast<const uint16_t*>(p.X);
-  const uint32_t code_block_bytes = 64u * (uint32_t)F;
+  const uint8_t* codes = reinterpret_cast<const uint8_t*>(p.X);
+  const uint32_t code_block_bytes = 32u * EB * (uint32_t)F;
   auto issue_codes = [&](int64_t b, int s) {
     if (gw == 0 && lane == 0 && b < n_blocks) {
       uint64_t* bar = s ? &bars[1 + 5 * NB + grp] : sbar;
       ptx::fence_proxy_async();
       ptx::mbar_arrive_expect_tx(bar, code_block_bytes);
-      ptx::bulk_g2s(Cb + (size_t)s * 32 * F, codes + b * 32 * (int64_t)F, code_block_bytes, bar);
+      ptx::bulk_g2s(reinterpret_cast<uint8_t*>(Cb) + (size_t)s * code_block_bytes, codes + b * (int64_t)code_block_bytes,
+                    code_block_bytes, bar);
     }
   };
-  if (CODES) issue_codes(blk, 0);
+  if (PRE) issue_codes(blk, 0);
   else issue(blk);
   if (!GT) ptx::mbar_wait(&bars[0], 0);  // chunk resident
 
@@ -348,12 +353,12 @@ __global__ void __launch_bounds__(512, 1) trav_kernel(const TravParams p) {
     const int64_t row0 = blk * 32;
     const int64_t next = blk + stride;
     const void* xptr;
-    if (CODES) {
+    if (PRE) {
       const int sb = itx & 1;
       ptx::mbar_wait(sb ? &bars[1 + 5 * NB + grp] : sbar, (itx >> 1) & 1);
       ++itx;
       issue_codes(next, sb ^ 1);  // the other buffer was released by the previous block's group sync
-      xptr = reinterpret_cast<const uint8_t*>(Cb + (size_t)sb * 32 * F) + 2 * lane;
+      xptr = reinterpret_cast<const uint8_t*>(Cb) + (size_t)sb * code_block_bytes + EB * lane;
     } else {
       const bool full = row0 + 32 <= n_rows;
       if (full) {

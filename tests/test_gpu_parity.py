@@ -195,3 +195,13 @@ def test_coded_and_fp32_node_formats(coded, monkeypatch):
     c, m2 = make_config("C3", n_trees=60)
     g2, _ = check(m2, gen_x(3, 0, 4001, 90))
     assert g2.layout()["coded"] == (coded == "1")
+
+
+@pytest.mark.parametrize("pret", ["1", "0"])
+def test_pretransposed_input_mode(pret, monkeypatch):
+    """Wide input, many chunks: X transposed once into feature-major blocks
+    (bulk-copied by every chunk CTA) vs per-chunk transpose -- both exact."""
+    monkeypatch.setenv("BRIDGER_PRET", pret)
+    c, m = make_config("C5", n_trees=60)
+    g, _ = check(m, gen_x(5, 0, 5003, 200), apply=True)
+    assert g.layout()["format"] == ("heap_pretransposed" if pret == "1" else "heap")

@@ -112,6 +112,8 @@ static void free_model(bridger_model* m) {
   cudaFree(m->d_base);
   cudaFree(m->d_bin_table);
   cudaFree(m->d_sparse_trees);
+  cudaFree(m->d_hyb_nodes);
+  cudaFree(m->d_hyb_leaves);
   cudaFree(m->d_sparse_nodes);
   cudaFree(m->d_bin_offsets);
   gemm_free(m);
@@ -325,6 +327,8 @@ bridger_status bridger_model_load(const bridger_model_desc* d, int cuda_device, 
         (e = upload(&m->d_bin_table, L.bin_table.data(), L.bin_table.size())) != cudaSuccess ||
         (e = upload(&m->d_bin_offsets, L.bin_offsets.data(), L.bin_offsets.size())) != cudaSuccess ||
         (e = upload(reinterpret_cast<SparseTree**>(&m->d_sparse_trees), L.sparse_trees.data(), L.sparse_trees.size())) != cudaSuccess ||
+        (e = upload(reinterpret_cast<uint32_t**>(&m->d_hyb_nodes), L.hyb_nodes.data(), L.hyb_nodes.size())) != cudaSuccess ||
+        (e = upload(&m->d_hyb_leaves, L.hyb_leaves.data(), L.hyb_leaves.size())) != cudaSuccess ||
         (e = upload(reinterpret_cast<uint32_t**>(&m->d_sparse_nodes), L.sparse_nodes.data(), L.sparse_nodes.size())) != cudaSuccess) {
       free_model(m);
       return e == cudaErrorMemoryAllocation ? fail(BRIDGER_E_OOM, "device allocation failed") : cuda_fail(e, "upload");
@@ -383,7 +387,7 @@ bridger_status bridger_model_layout(const bridger_model* m, int32_t* n_chunks, i
   if (!m) return fail(BRIDGER_E_NULL_ARG, "model is NULL");
   if (n_chunks) *n_chunks = m->trav_ok ? (int32_t)m->trav.chunks.size() : 0;
   if (coded)
-    *coded = !m->trav_ok ? 0 : m->trav.codes ? 1 : m->trav.sparse ? 2 : m->trav.pretransposed ? 3 : 0;
+    *coded = !m->trav_ok ? 0 : m->trav.codes ? 1 : m->trav.sparse ? 2 : m->trav.hybrid ? 4 : m->trav.pretransposed ? 3 : 0;
   if (global_trees) *global_trees = m->trav_ok && m->trav.global_trees ? 1 : 0;
   if (n_warps) *n_warps = m->trav.n_warps;
   if (group) *group = m->trav.group;

@@ -63,7 +63,9 @@ struct TravChunk {
   int32_t depth;
   int32_t leaf_offset; // byte offset of the leaves inside the chunk
   int32_t first_slot;  // index of the chunk's first tree slot (slot -> original tree)
-  int32_t pad_;
+  int32_t top_levels;  // hybrid: heap levels resident in shared memory
+  int64_t g_nodes;     // hybrid: first deep-level record of the chunk (global)
+  int64_t g_leaves;    // hybrid: first leaf value of the chunk (global)
 };
 
 // Sparse (pointer) tree descriptor (§8(f3)): unbounded / unbalanced trees.
@@ -83,6 +85,9 @@ struct TravLayout {
   bool codes = false;           // threshold-bin codes: 4-byte nodes, u16 X codes (see lowering.cpp)
   bool sparse = false;          // pointer-format trees (deep / unbalanced), walked from global memory
   bool pretransposed = false;   // fp32 input transposed once into feature-major blocks (wide X, many chunks)
+  bool hybrid = false;          // top levels in shared memory, deep levels + leaves in global memory
+  std::vector<uint32_t> hyb_nodes;  // [records][2] deep levels of every tree (slot order)
+  std::vector<float> hyb_leaves;    // [slots][L][K]
   std::vector<SparseTree> sparse_trees;
   std::vector<uint32_t> sparse_nodes;   // [n][4] records
   std::vector<float> bin_table;     // concatenated sorted distinct thresholds per feature
@@ -151,6 +156,8 @@ struct bridger_model {
   int64_t* d_slot_leafid_off = nullptr;
   int32_t* d_leaf_ids = nullptr;
   double* d_base = nullptr;
+  void* d_hyb_nodes = nullptr;       // TravLayout::hybrid
+  float* d_hyb_leaves = nullptr;
   void* d_sparse_trees = nullptr;    // SparseTree[T] (TravLayout::sparse)
   void* d_sparse_nodes = nullptr;    // uint4 records
   float* d_bin_table = nullptr;      // threshold-bin codes (TravLayout::codes)

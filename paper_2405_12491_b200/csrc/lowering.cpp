@@ -445,6 +445,88 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
     out->bin_offsets.clear();
     plan(false);
   }
+  out->hybrid = false;
+  out->hyb_nodes.clear();
+  out->hyb_leaves.clear();
+  const char* hyb_env = std::getenv("BRIDGER_HYBRID");
+  const bool uniform = depth[order.front()] == Dmax;
+  // measured on B200: slower than global-tree mode for C4 at
+  // every shared-memory split tried, so opt-in (BRIDGER_HYBRID=1)
+  if (out->global_trees && uniform && Dmax >= 6 && hyb_env && hyb_env[0] == '1') {
+    // Hybrid: the top `top` levels of a chunk of trees resident in shared
+    // memory, deep levels + leaves in global memory; input pre-transposed.
+    int64_t base_budget = kSmemMax - misc - (int64_t)nb * xw;
+    if (const char* e = std::getenv("BRIDGER_HYB_BUDGET")) base_budget = std::min<int64_t>(base_budget, 1024LL * std::atoi(e));
+    int32_t top = std::min(Dmax - 1, 11);
+    int64_t n_fit = 0;
+    for (; top >= 3; --top) {
+      n_fit = base_budget / (((int64_t)1 << top) - 1) / 8;
+      if (n_fit >= 32 || n_fit >= T) break;
+    }
+    if (top >= 3 && n_fit >= 1) {
+      out->hybrid = true;
+      out->global_trees = false;
+      out->pretransposed = false;
+      const int32_t It = (1 << top) - 1, I = (1 << Dmax) - 1, L = 1 << Dmax;
+      int32_t nc = (int32_t)((T + n_fit - 1) / n_fit);
+      if (sms > 0 && nc > sms / 2 && nc % sms != 0) nc = std::min<int32_t>(T, (nc + sms - 1) / sms * sms);
+      out->chunks.clear();
+      out->data.clear();
+      out->slot_tree.assign(T, 0);
+      out->slot_leafid_off.assign(T, 0);
+      out->leaf_ids.clear();
+      PaddedTree pt;
+      int64_t off = 0;
+      int32_t s0 = 0;
+      for (int32_t ci = 0; ci < nc; ++ci) {
+        const int32_t n = T / nc + (ci < T % nc ? 1 : 0);
+        TravChunk c{};
+        c.offset = off;
+        c.n_trees = n;
+        c.depth = Dmax;
+        c.first_slot = s0;
+        c.top_levels = top;
+        c.g_nodes = (int64_t)s0 * (I - It);
+        c.g_leaves = (int64_t)s0 * L * K;
+        c.leaf_offset = 0;
+        c.bytes = (int32_t)(((int64_t)n * It * 8 + 15) / 16 * 16);
+        out->data.resize(off + c.bytes, 0);
+        uint32_t* nd = reinterpret_cast<uint32_t*>(out->data.data() + off);
+        for (int32_t j = 0; j < n; ++j) {
+          const int32_t t = order[s0 + j];
+          pad_tree(d, t, Dmax, &pt);
+          for (int32_t i = 0; i < I; ++i) {
+            uint32_t tb;
+            std::memcpy(&tb, &pt.threshold[i], 4);
+            const uint32_t fw = (uint32_t)pt.feature[i] | ((uint32_t)pt.missing[i] << 31);
+            if (i < It) {
+              nd[2 * ((size_t)j * It + i)] = tb;
+              nd[2 * ((size_t)j * It + i) + 1] = fw;
+            } else {
+              out->hyb_nodes.push_back(tb);
+              out->hyb_nodes.push_back(fw);
+            }
+          }
+          for (int32_t l = 0; l < L * K; ++l)
+            out->hyb_leaves.push_back(acc_int ? std::ldexp(pt.leaf_value[l], -ex.q) : pt.leaf_value[l]);
+          out->slot_tree[s0 + j] = t;
+          out->slot_leafid_off[s0 + j] = (int64_t)out->leaf_ids.size();
+          out->leaf_ids.insert(out->leaf_ids.end(), pt.leaf_id.begin(), pt.leaf_id.end());
+        }
+        out->chunks.push_back(c);
+        off += (c.bytes + 127) / 128 * 128;
+        out->data.resize(off, 0);
+        s0 += n;
+      }
+      out->n_warps = nw;
+      out->group = G;
+      out->chunk_budget = (int32_t)base_budget;
+      int32_t maxc = 0;
+      for (auto& c : out->chunks) maxc = std::max(maxc, c.bytes);
+      out->smem_bytes = maxc + nb * xw + misc;
+      return true;
+    }
+  }
   out->n_warps = nw;
   out->group = G;
   out->chunk_budget = budget;

@@ -35,6 +35,10 @@ BRIDGER_TRAV_EXTERN(long long, false, false, 3)
 BRIDGER_TRAV_EXTERN(long long, true, false, 3)
 BRIDGER_TRAV_EXTERN(double, false, false, 3)
 BRIDGER_TRAV_EXTERN(double, true, false, 3)
+BRIDGER_TRAV_EXTERN(long long, false, false, 4)
+BRIDGER_TRAV_EXTERN(long long, true, false, 4)
+BRIDGER_TRAV_EXTERN(double, false, false, 4)
+BRIDGER_TRAV_EXTERN(double, true, false, 4)
 BRIDGER_TRAV_EXTERN(long long, false, true, 2)
 BRIDGER_TRAV_EXTERN(long long, true, true, 2)
 BRIDGER_TRAV_EXTERN(double, false, true, 2)
@@ -168,6 +172,8 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
   p.slot_tree = m->d_slot_tree;
   p.sparse = static_cast<const SparseTree*>(m->d_sparse_trees);
   p.sparse_nodes = static_cast<const uint4*>(m->d_sparse_nodes);
+  p.hyb_nodes = static_cast<const uint2*>(m->d_hyb_nodes);
+  p.hyb_leaves = m->d_hyb_leaves;
   p.slot_leafid_off = m->d_slot_leafid_off;
   p.leaf_ids = m->d_leaf_ids;
   p.T = m->T;
@@ -247,7 +253,7 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
       return err;
     }
     p.X = static_cast<const float*>(codes);
-  } else if (L.pretransposed && want != 3) {
+  } else if (L.hybrid || (L.pretransposed && want != 3)) {
     const int64_t nbk = (n_rows + 31) / 32;
     err = cudaMallocAsync(&codes, (size_t)nbk * 32 * m->F * 4, st);
     if (err != cudaSuccess) return err;
@@ -280,6 +286,13 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
                                : launch_trav_t<KT, long long, false, true, 2>(p, grid, block, smem, cluster, st);
         return L.has_missing ? launch_trav_t<KT, double, true, true, 2>(p, grid, block, smem, cluster, st)
                              : launch_trav_t<KT, double, false, true, 2>(p, grid, block, smem, cluster, st);
+      }
+      if (L.hybrid) {
+        if (m->acc_int)
+          return L.has_missing ? launch_trav_t<KT, long long, true, false, 4>(p, grid, block, smem, cluster, st)
+                               : launch_trav_t<KT, long long, false, false, 4>(p, grid, block, smem, cluster, st);
+        return L.has_missing ? launch_trav_t<KT, double, true, false, 4>(p, grid, block, smem, cluster, st)
+                             : launch_trav_t<KT, double, false, false, 4>(p, grid, block, smem, cluster, st);
       }
       if (L.pretransposed && want != 3) {
         if (m->acc_int)

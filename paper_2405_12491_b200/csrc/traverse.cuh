@@ -43,7 +43,7 @@ void hot_end(cudaStream_t st, cudaEvent_t start);
 // per-row partial sums into the leader CTA's shared memory over DSMEM
 // (st.shared::cluster + remote mbarrier arrive), the leader adds them in rank
 // order and finalizes -- no global partials, no second kernel.
-enum TravFmt : int { FMT_HEAP = 0, FMT_CODES = 1, FMT_SPARSE = 2, FMT_HEAP_T = 3 };
+enum TravFmt : int { FMT_HEAP = 0, FMT_CODES = 1, FMT_SPARSE = 2, FMT_HEAP_T = 3, FMT_HYBRID = 4 };
 enum TravMode : int32_t { TRAV_FINAL = 0, TRAV_PARTIAL = 1, TRAV_APPLY = 2, TRAV_CLUSTER = 3 };
 
 struct TravParams {
@@ -66,6 +66,9 @@ struct TravParams {
   int32_t T;
   const SparseTree* sparse;  // FMT_SPARSE: per-slot tree descriptors
   const uint4* sparse_nodes; //             16-byte node records
+  const uint2* hyb_nodes;    // FMT_HYBRID: deep levels of every tree (global)
+  const float* hyb_leaves;   //             leaf values (global)
+  int32_t hyb_pret;          //             input pre-transposed (bulk-copied blocks)
   int32_t group;      // warps sharing one 32-row block (tree split)
   int32_t red_off;    // byte offset of the intra-group partials
   int32_t slot_off;   // byte offset of the DSMEM reduction slots (TRAV_CLUSTER)
@@ -197,6 +200,84 @@ __device__ __forceinline__ void group_sync(int group, int G) {
   }
 }
 
+// Hybrid heap format for trees too large for shared memory (C4: depth 12,
+// 8-class leaves): the top `top` levels of the chunk's trees are resident in
+// shared memory (where the walk is broadcast-heavy and conflict-light), the
+// deeper levels and the leaves are read from global memory (L1/L2).
+template <int NI, int KT, typename ACC, bool ML>
+__device__ __forceinline__ void walk_hybrid(const TravParams& p, const TravChunk& c, const uint2* top_nodes,
+                                            const float* xf, int j, int K, int64_t row, ACC (&acc)[KT]) {
+  const int D = c.depth, top = c.top_levels;
+  const int It = (1 << top) - 1, I = (1 << D) - 1, L = 1 << D, Ib = I - It;
+  const uint2* nt = top_nodes + (size_t)j * It;
+  const uint2* nbm = p.hyb_nodes + c.g_nodes + (int64_t)j * Ib;
+  int idx[NI];
+#pragma unroll
+  for (int u = 0; u < NI; ++u) idx[u] = 0;
+  for (int lvl = 0; lvl < top; ++lvl) {
+    uint2 a[NI];
+#pragma unroll
+    for (int u = 0; u < NI; ++u) a[u] = nt[u * It + idx[u]];
+    float x[NI];
+#pragma unroll
+    for (int u = 0; u < NI; ++u) x[u] = xf[(a[u].y & (ML ? 0x7fffffffu : 0xffffffffu)) * 32];
+#pragma unroll
+    for (int u = 0; u < NI; ++u) idx[u] = 2 * idx[u] + 1 + go_right<ML>(x[u], a[u]);
+  }
+  for (int lvl = top; lvl < D; ++lvl) {
+    uint2 a[NI];
+#pragma unroll
+    for (int u = 0; u < NI; ++u) a[u] = __ldg(nbm + (int64_t)u * Ib + (idx[u] - It));
+    float x[NI];
+#pragma unroll
+    for (int u = 0; u < NI; ++u) x[u] = xf[(a[u].y & (ML ? 0x7fffffffu : 0xffffffffu)) * 32];
+#pragma unroll
+    for (int u = 0; u < NI; ++u) idx[u] = 2 * idx[u] + 1 + go_right<ML>(x[u], a[u]);
+  }
+  if (p.mode == TRAV_APPLY) {
+    if (row < p.n_rows) {
+      int32_t* o = p.out_leaf + row * p.T;
+#pragma unroll
+      for (int u = 0; u < NI; ++u) {
+        const int s = c.first_slot + j + u;
+        o[p.slot_tree[s]] = p.leaf_ids[p.slot_leafid_off[s] + idx[u] - I];
+      }
+    }
+    return;
+  }
+#pragma unroll
+  for (int u = 0; u < NI; ++u) {
+    const float* e = p.hyb_leaves + c.g_leaves + ((int64_t)(j + u) * L + (idx[u] - I)) * K;
+    if (KT == K && (KT == 4 || KT == 8)) {
+#pragma unroll
+      for (int k4 = 0; k4 < KT; k4 += 4) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(e) + k4 / 4);
+        acc[k4 + 0 < KT ? k4 + 0 : 0] += leaf_to_acc<ACC>(v.x);
+        acc[k4 + 1 < KT ? k4 + 1 : 0] += leaf_to_acc<ACC>(v.y);
+        acc[k4 + 2 < KT ? k4 + 2 : 0] += leaf_to_acc<ACC>(v.z);
+        acc[k4 + 3 < KT ? k4 + 3 : 0] += leaf_to_acc<ACC>(v.w);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < KT; ++k)
+        if (k < K) acc[k] += leaf_to_acc<ACC>(__ldg(e + k));
+    }
+  }
+}
+
+template <int KT, typename ACC, bool ML>
+__device__ __forceinline__ void walk_hybrid_tail(int r, const TravParams& p, const TravChunk& c, const uint2* top,
+                                                 const float* xf, int j, int K, int64_t row, ACC (&acc)[KT]) {
+  switch (r) {
+#define BRIDGER_HTAIL(N) \
+  case N: walk_hybrid<N, KT, ACC, ML>(p, c, top, xf, j, K, row, acc); break;
+    BRIDGER_HTAIL(1) BRIDGER_HTAIL(2) BRIDGER_HTAIL(3) BRIDGER_HTAIL(4) BRIDGER_HTAIL(5) BRIDGER_HTAIL(6)
+    BRIDGER_HTAIL(7) BRIDGER_HTAIL(8)
+#undef BRIDGER_HTAIL
+    default: break;
+  }
+}
+
 // Sparse (pointer) format for unbounded / unbalanced trees (§8(f3)): BFS order,
 // the two children of a node adjacent; record {threshold, feature | missing<<30
 // | leaf<<31, left-child index or leaf index, -}.  NI trees walk together;
@@ -263,7 +344,8 @@ __global__ void __launch_bounds__(512, 1) trav_kernel(const TravParams p) {
   constexpr bool SPARSE = FMT == FMT_SPARSE;
   // PRE: the input arrives pre-laid-out as feature-major [F][32] blocks (u16
   // codes or pre-transposed fp32), bulk-copied into two buffers per group
-  constexpr bool PRE = CODES || FMT == FMT_HEAP_T;
+  constexpr bool HYB = FMT == FMT_HYBRID;
+  constexpr bool PRE = CODES || FMT == FMT_HEAP_T || HYB;  // hybrid always takes pre-transposed input
   constexpr uint32_t EB = CODES ? 2u : 4u;
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
@@ -428,7 +510,18 @@ __global__ void __launch_bounds__(512, 1) trav_kernel(const TravParams p) {
         j += sz;
       }
     };
-    if (SPARSE) {
+    if (HYB) {
+      const int nt = (int)((int64_t)c.n_trees * (gw + 1) / G) - (int)((int64_t)c.n_trees * gw / G);
+      const int t0 = (int)((int64_t)c.n_trees * gw / G);
+      const int n_pass = (nt + 7) / 8;
+      int j = t0;
+      for (int q = 0; q < n_pass; ++q) {
+        const int sz = nt / n_pass + (q < nt % n_pass ? 1 : 0);
+        walk_hybrid_tail<KT, ACC, ML>(sz, p, c, reinterpret_cast<const uint2*>(cdata), static_cast<const float*>(xptr),
+                                      j, K, row, acc);
+        j += sz;
+      }
+    } else if (SPARSE) {
       // pointer-format trees from global memory: every CTA walks every tree
       const int T = c.n_trees;
       const int t0 = (int)((int64_t)T * gw / G), t1 = (int)((int64_t)T * (gw + 1) / G);

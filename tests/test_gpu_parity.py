@@ -168,11 +168,16 @@ def test_many_deep_chunks_regression():
     check(m, gen_x(16, 0, 3001, 20), apply=False)
 
 
-def test_c4_shaped_global_trees():
-    """Depth-12, 8-class trees (164 KB each) exceed shared memory: walked from
-    global memory by every CTA (no partials)."""
-    c, m = make_config("C4", n_trees=6)
-    check(m, gen_x(4, 0, 4001, 64))
+@pytest.mark.parametrize("hybrid", ["1", "0"])
+def test_c4_shaped_deep_trees(hybrid, monkeypatch):
+    """Depth-12, 8-class trees (164 KB each) exceed shared memory: hybrid mode
+    (top levels in shared memory, deep levels + leaves in global) or
+    global-tree mode (every CTA walks every tree from global memory)."""
+    monkeypatch.setenv("BRIDGER_HYBRID", hybrid)
+    c, m = make_config("C4", n_trees=40)
+    g, _ = check(m, gen_x(4, 0, 4001, 64))
+    assert g.layout()["format"] == ("hybrid" if hybrid == "1" else "heap")  # hybrid is opt-in
+    assert g.layout()["global_trees"] == (hybrid == "0")
 
 
 def test_mixed_depth_forest():

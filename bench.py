@@ -183,22 +183,33 @@ def gemm_roofline(B, m, cfg, X, dev, args):
     e1.record()
     torch.cuda.synchronize(dev)
     k2_ms, k2_n = B.hot_kernel_time()
-    B.hot_kernel_timing(False)
     step_ms = e0.elapsed_time(e1) / steps
     ip, lp = B.gemm_geometry(cfg.depth)
     ops = 2.0 * n * cfg.n_trees * ip * lp * steps        # dense int8 ops of the contraction (padded)
     achieved = ops / (k2_ms / 1e3) / 1e12
+    # K1 gather-compare in production form (tiled UMMA-layout decisions), timed by
+    # the library's events: HBM bytes = X rows read + n_trees * I_pad decision bytes written
+    k1_ms, _ = B.hot_kernel_time(1)
+    k3_ms, _ = B.hot_kernel_time(2)
+    k1_bytes = steps * (n * cfg.n_features * 4 + n * cfg.n_trees * ip)
+    hbm = _peaks()[0].get("hbm_gbs", 6541.1)
+    gather = {"kernel": "gc_kernel (a1+a2: exact fp32 gather + less_equal, int8 decisions)", "bound": "hbm",
+              "achieved": k1_bytes / (k1_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+              "frac": k1_bytes / (k1_ms / 1e3) / 1e9 / hbm, "ms_per_step": k1_ms / steps,
+              "k3_leaf_gather_ms_per_step": k3_ms / steps}
+    B.hot_kernel_timing(False)
     return {"kernel": "pc_kernel (tcgen05.mma.cta_group::1.kind::i8, TMEM accumulators)", "bound": "tensor",
             "achieved": achieved, "peak": peak, "unit": "TOP/s", "frac": achieved / peak, "peak_source": src,
             "k2_ms_per_step": k2_ms / steps, "k2_launches_per_step": k2_n // steps,
             "gemm_variant_ms_per_step": step_ms, "gemm_variant_rows_per_s": n / (step_ms / 1e3),
+            "gather_compare": gather,
             "note": "GEMM form of a1..a4 (decisions materialised per 128-row tile); AUTO selects the traversal"}
 
 
 def workload_config(cfg, world):
     return {"workload": f"{cfg.name}: {cfg.describe}", "n_rows_per_gpu": cfg.n_rows, "n_trees": cfg.n_trees,
             "depth": cfg.depth, "n_features": cfg.n_features, "n_outputs": cfg.n_classes,
-            "sharding": f"rows x{world}" if world > 1 else "single GPU",
+            "sharding": (f"{cfg.sharding} x{world}" if world > 1 else "single GPU"),
             "l2": "flushed before every timed step (256 MiB write)", "output": "predict (int32 labels)"
             if cfg.kind == "classification" else "predict (fp32 scores)"}
 
@@ -238,17 +249,31 @@ def main():
         cfg = dataclasses.replace(cfg, n_rows=args.rows or cfg.n_rows, n_trees=m.n_trees,
                                   describe=cfg.describe + f" [override: {args.rows or cfg.n_rows} rows, {m.n_trees} trees]")
     n = cfg.n_rows
-    row0 = rank * n
+    tree_sharded = cfg.sharding == "trees"
+    # row sharding: each rank its own rows (weak scaling); tree sharding: all
+    # rows on every rank, trees split, one NCCL reduce-scatter (strong scaling)
+    row0 = 0 if tree_sharded else rank * n
     X = gen_x_torch(cfg.seed, row0, n, cfg.n_features, device=dev)
-    model = B.Model(m, device=local, variant=args.variant)
+    tsp = None
+    if tree_sharded and world > 1:
+        from paper_2405_12491_b200.dist import TreeShardedPredictor
+        tsp = TreeShardedPredictor(m, device=local)
+        model = tsp.model
+    else:
+        model = B.Model(m, device=local, variant=args.variant)
     classif = cfg.kind == "classification"
     out = torch.empty(n, dtype=torch.int32, device=dev) if classif else torch.empty((n, 1), device=dev)
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
     st = torch.cuda.current_stream(dev)
 
+    def step():
+        if tsp is not None:
+            return tsp.predict(X)
+        return model.predict(X, out=out)
+
     for _ in range(args.warmup):
         flush.fill_(1.0)
-        model.predict(X, out=out)
+        step()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
@@ -264,7 +289,7 @@ def main():
         for e0, e1 in ev:
             flush.fill_(1.0)
             e0.record(st)
-            model.predict(X, out=out)
+            step()
             e1.record(st)
         torch.cuda.synchronize(dev)
         if world > 1:
@@ -278,9 +303,11 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_per_step = t.item() / args.steps
-    value = n * world / (ms_per_step / 1e3)
+    value = (n if tree_sharded else n * world) / (ms_per_step / 1e3)
 
     # ---- e2e through the public host-buffer API (pinned input, labels back to host)
+    if tsp is not None:
+        args.e2e_steps = 0  # the host-buffer API runs a whole model on one device
     Xh = (torch.from_numpy(gen_x(cfg.seed, row0, n, cfg.n_features)) if args.e2e_steps > 0
           else torch.zeros((32, cfg.n_features))).pin_memory()
     oh = torch.empty(n, dtype=torch.int32).pin_memory() if classif else torch.empty((n, 1)).pin_memory()
@@ -296,7 +323,7 @@ def main():
     te = torch.tensor([sum(e2e_times) / max(1, len(e2e_times))], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e = {"value": n * world / te.item() if e2e_times else None, "unit": "rows/s", "h2d_bytes_per_step": n * cfg.n_features * 4,
+    e2e = {"value": (n if tree_sharded else n * world) / te.item() if e2e_times else None, "unit": "rows/s", "h2d_bytes_per_step": n * cfg.n_features * 4,
            "d2h_bytes_per_step": int(oh.numel() * oh.element_size()),
            "api": "bridger_predict_host (2-stream chunked H2D/compute/D2H pipeline)"}
 
@@ -309,7 +336,7 @@ def main():
     if variant == "traverse":
         # algorithmic shared-memory bytes per launch: per (row, tree) D node records (8 B) +
         # D feature values (4 B) + K leaf values (4 B)
-        alg = n * cfg.n_trees * (12 * cfg.depth + 4 * cfg.n_classes)
+        alg = n * model.n_trees * (12 * cfg.depth + 4 * cfg.n_classes)
         sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
         peak = sm_count * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e9   # GB/s
         achieved = alg / (hot_avg / 1e3) / 1e9
@@ -331,7 +358,7 @@ def main():
     line = {
         "metric": "tree-ensemble inference rows/sec", "value": value, "unit": "rows/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None,
+        "scaling": "strong" if tree_sharded else "weak", "vs_baseline": None,
         "dtype": "f32 compare, int64 fixed-point accumulate" if info["acc_is_int64"] else "f32 compare, f64 accumulate",
         "data": "synthetic (counter-based generator, seeded; random calibrated trees)",
         "config": workload_config(cfg, world), "variant": variant, "exact_tier": info["exact_tier"],

@@ -212,6 +212,9 @@ int64_t bridger_launch_count(void);
  * since the last query, and clears them. */
 bridger_status bridger_hot_kernel_timing(int32_t enable);
 bridger_status bridger_hot_kernel_time(double* total_ms, int64_t* launches);
+/* Same for a kernel id: 0 = dominant kernel (traversal / path contraction K2),
+ * 1 = gather-compare K1, 2 = leaf gather / reduce K3. */
+bridger_status bridger_hot_kernel_time_by(int32_t kernel, double* total_ms, int64_t* launches);
 
 #ifdef __cplusplus
 }

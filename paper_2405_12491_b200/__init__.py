@@ -50,6 +50,7 @@ EXPORTS = [
     "bridger_step_path_scores", "bridger_gemm_geometry", "bridger_path_matrix", "bridger_lower_tree",
     "bridger_analyze_exactness", "bridger_validate", "bridger_last_error", "bridger_status_string",
     "bridger_launch_count", "bridger_hot_kernel_timing", "bridger_hot_kernel_time", "bridger_model_layout",
+    "bridger_hot_kernel_time_by",
 ]
 
 
@@ -83,6 +84,7 @@ def _load_lib():
         "bridger_hot_kernel_timing": ([i32], i32),
         "bridger_hot_kernel_time": ([vp, vp], i32),
         "bridger_model_layout": ([vp, vp, vp, vp, vp, vp], i32),
+        "bridger_hot_kernel_time_by": ([i32, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -112,10 +114,11 @@ def hot_kernel_timing(enable: bool) -> None:
     _check(_lib.bridger_hot_kernel_timing(1 if enable else 0))
 
 
-def hot_kernel_time():
-    """(summed ms, launches) of the dominant kernel since the last query."""
+def hot_kernel_time(kernel: int = 0):
+    """(summed ms, launches) since the last query of kernel id `kernel`:
+    0 dominant (traversal / K2), 1 K1 gather-compare, 2 K3 leaf gather."""
     ms, n = C.c_double(), C.c_int64()
-    _check(_lib.bridger_hot_kernel_time(C.byref(ms), C.byref(n)))
+    _check(_lib.bridger_hot_kernel_time_by(int(kernel), C.byref(ms), C.byref(n)))
     return ms.value, n.value
 
 

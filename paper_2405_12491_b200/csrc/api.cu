@@ -24,21 +24,23 @@ bridger_status fail(bridger_status s, const std::string& msg) {
 void count_launch() { ++g_launches; }
 
 static thread_local bool g_timing = false;
-static thread_local std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_events;
-// bracket the dominant kernel of a predict with events (bench roofline)
+static thread_local std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_events[4];
+// bracket kernels of a predict with events (bench roofline); id 0 = dominant
+// kernel (traversal / path contraction), 1 = gather-compare, 2 = leaf gather
 void hot_begin(cudaStream_t st, cudaEvent_t* ev) {
   *ev = nullptr;
   if (!g_timing) return;
   cudaEventCreate(ev);
   cudaEventRecord(*ev, st);
 }
-void hot_end(cudaStream_t st, cudaEvent_t start) {
+void hot_end_id(cudaStream_t st, cudaEvent_t start, int id) {
   if (!g_timing || !start) return;
   cudaEvent_t e;
   cudaEventCreate(&e);
   cudaEventRecord(e, st);
-  g_events.push_back({start, e});
+  g_events[id & 3].push_back({start, e});
 }
+void hot_end(cudaStream_t st, cudaEvent_t start) { hot_end_id(st, start, 0); }
 
 cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, void* out, int want,
                      int32_t total_trees, cudaStream_t st);
@@ -180,9 +182,11 @@ bridger_status bridger_hot_kernel_timing(int32_t enable) {
   return BRIDGER_OK;
 }
 
-bridger_status bridger_hot_kernel_time(double* total_ms, int64_t* launches) {
+bridger_status bridger_hot_kernel_time_by(int32_t kernel, double* total_ms, int64_t* launches) {
+  if (kernel < 0 || kernel > 3) return fail(BRIDGER_E_SHAPE, "kernel id must be in [0,3]");
   double sum = 0.0;
-  for (auto& pr : g_events) {
+  auto& v = g_events[kernel];
+  for (auto& pr : v) {
     float ms = 0.f;
     cudaEventSynchronize(pr.second);
     cudaEventElapsedTime(&ms, pr.first, pr.second);
@@ -191,9 +195,13 @@ bridger_status bridger_hot_kernel_time(double* total_ms, int64_t* launches) {
     cudaEventDestroy(pr.second);
   }
   if (total_ms) *total_ms = sum;
-  if (launches) *launches = (int64_t)g_events.size();
-  g_events.clear();
+  if (launches) *launches = (int64_t)v.size();
+  v.clear();
   return BRIDGER_OK;
+}
+
+bridger_status bridger_hot_kernel_time(double* total_ms, int64_t* launches) {
+  return bridger_hot_kernel_time_by(0, total_ms, launches);
 }
 int64_t bridger_launch_count(void) { return g_launches; }
 

@@ -37,6 +37,7 @@ namespace bridger {
 void count_launch();
 void hot_begin(cudaStream_t st, cudaEvent_t* ev);
 void hot_end(cudaStream_t st, cudaEvent_t start);
+void hot_end_id(cudaStream_t st, cudaEvent_t start, int id);
 
 struct GemmClassDev {
   int32_t depth, i_pad, l_pad, n_trees;
@@ -481,8 +482,11 @@ static cudaError_t launch_gc(const float* X, int64_t row0, int32_t rows, int32_t
     cudaFuncSetAttribute(gc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
     cudaFuncSetAttribute(gc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
   }
+  cudaEvent_t ev;
+  hot_begin(st, &ev);
   if (plain) gc_kernel<true><<<grid, 128, smem, st>>>(X, row0, rows, F, gbase, c, t_begin, tpc, t_end, P);
   else gc_kernel<false><<<grid, 128, smem, st>>>(X, row0, rows, F, gbase, c, t_begin, tpc, t_end, P);
+  hot_end_id(st, ev, 1);
   count_launch();
   return cudaGetLastError();
 }
@@ -565,6 +569,8 @@ cudaError_t gemm_run(const bridger_model* m, const float* X, int64_t n_rows, voi
       if (e != cudaSuccess) break;
       const int tb = 256, g = (rows + tb - 1) / tb;
       const float* E = reinterpret_cast<const float*>(gbase + c.leaf_off);
+      cudaEvent_t ev3;
+      hot_begin(st, &ev3);
       BRIDGER_DISPATCH_KT(m->K, {
         if (m->acc_int)
           lg_kernel<KT, long long><<<g, tb, 0, st>>>(leaf, rows, c.n_trees, E, 1 << c.depth, m->K,
@@ -573,6 +579,7 @@ cudaError_t gemm_run(const bridger_model* m, const float* X, int64_t n_rows, voi
           lg_kernel<KT, double><<<g, tb, 0, st>>>(leaf, rows, c.n_trees, E, 1 << c.depth, m->K,
                                                    static_cast<double*>(accbuf), ci == 0, ci == nc - 1, r0, fin);
       });
+      hot_end_id(st, ev3, 2);
       count_launch();
       e = cudaGetLastError();
     }

@@ -159,3 +159,54 @@ def _subset(desc, trees):
         missing_left=None if ml is None else np.asarray(ml)[idx], task=getattr(desc, "task", 0),
         agg=getattr(desc, "agg", 0), post=getattr(desc, "post", 0), base_score=getattr(desc, "base_score", None),
         leaf_scale=getattr(desc, "leaf_scale", 1.0))
+
+
+# ------------------------------------------------------------- 2-D sharding --
+def grid_2d(world: int, row_groups: int, rank: int):
+    """Rank -> (row group rg, tree group tg) for a rows x trees process grid:
+    rank = rg * TG + tg with TG = world // row_groups."""
+    if world % row_groups:
+        raise ValueError("world size must be a multiple of row_groups")
+    tg_n = world // row_groups
+    return rank // tg_n, rank % tg_n, tg_n
+
+
+def make_row_group_comms(world: int, row_groups: int):
+    """One communicator per row group (its TG tree-shard ranks).  Every rank
+    must call this with the same arguments (torch.distributed.new_group is
+    collective); returns the list of groups, index rg."""
+    import torch.distributed as dist
+    tg_n = world // row_groups
+    return [dist.new_group(list(range(rg * tg_n, (rg + 1) * tg_n))) for rg in range(row_groups)]
+
+
+class TwoDShardedPredictor:
+    """rows x trees sharding (§8(f4)) for ensembles both huge and wide: the
+    row group rg owns rows shard rg, the tree group tg trees shard tg; raw int64
+    partials are reduce-scattered inside the row group only (TG ranks)."""
+
+    def __init__(self, desc, device: int, row_groups: int):
+        import torch.distributed as dist
+
+        from . import Model, analyze_exactness
+        world, rank = dist.get_world_size(), dist.get_rank()
+        self.rg, self.tg, self.tg_n = grid_2d(world, row_groups, rank)
+        self.comms = make_row_group_comms(world, row_groups)
+        q, tier, _ = analyze_exactness(desc)
+        self.total_trees = len(desc.tree_offsets) - 1
+        a, b = tree_partition(tree_visits(desc), self.tg_n)[self.tg]
+        self.model = Model(_subset(desc, range(a, b)), device=device, force_fixed_point=(q, TIER_CODE[tier]))
+
+    def predict(self, X_rows, proba: bool = False):
+        """X_rows: the row group's rows (same on its TG ranks).  Returns (row0
+        within the row group's rows, outputs of this rank's slice)."""
+        import torch
+        n = X_rows.shape[0]
+        n_pad = -(-n // self.tg_n) * self.tg_n
+        raw = self.model.predict_raw(X_rows)
+        if n_pad != n:
+            raw = torch.cat([raw, torch.zeros((n_pad - n, raw.shape[1]), dtype=raw.dtype, device=raw.device)])
+        mine = reduce_scatter_rows(raw, self.comms[self.rg])
+        row0 = self.tg * (n_pad // self.tg_n)
+        keep = max(0, min(mine.shape[0], n - row0))
+        return row0, self.model.finalize(mine[:keep].contiguous(), total_trees=self.total_trees, proba=proba)

@@ -14,7 +14,8 @@ import torch.multiprocessing as mp
 
 import oracle
 import paper_2405_12491_b200 as B
-from paper_2405_12491_b200.dist import reduce_scatter_rows, row_range, tree_partition, tree_visits
+from paper_2405_12491_b200.dist import (grid_2d, make_row_group_comms, reduce_scatter_rows, row_range,
+                                        tree_partition, tree_visits)
 from synth import gen_x, make_config, perfect_ensemble, prune_ensemble
 
 
@@ -96,3 +97,50 @@ def test_gloo_world2_tree_and_row_sharding():
     for p in procs:
         p.join(timeout=60)
     assert res == {0: "ok", 1: "ok"}, res
+
+
+def _worker_2d(rank, world, port, q):
+    """rows x trees grid 2 x 2: each row group reduce-scatters its tree shards'
+    exact int64 partials among its own 2 ranks."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        row_groups = 2
+        rg, tg, tg_n = grid_2d(world, row_groups, rank)
+        comms = make_row_group_comms(world, row_groups)
+        m = perfect_ensemble(7, 19, 5, 6, kind="regression", lr=0.05, calib_rows=512)
+        m = prune_ensemble(m, 7, p=0.2)
+        X = gen_x(8, 0, 203, 6)
+        qx, _, _ = B.analyze_exactness(m)
+        ra, rb = row_range(X.shape[0], row_groups, rg)
+        Xg = X[ra:rb]
+        a, b = tree_partition(tree_visits(m), tg_n)[tg]
+        part = oracle.run(m.subset(range(a, b)), Xg)["acc"]
+        raw = torch.from_numpy(np.round(np.ldexp(part, -qx)).astype(np.int64))
+        n = Xg.shape[0]
+        n_pad = -(-n // tg_n) * tg_n
+        raw = torch.cat([raw, torch.zeros((n_pad - n, 1), dtype=torch.int64)])
+        mine = reduce_scatter_rows(raw, comms[rg])
+        full = np.round(np.ldexp(oracle.run(m, Xg)["acc"], -qx)).astype(np.int64)
+        r0 = tg * (n_pad // tg_n)
+        keep = min(mine.shape[0], n - r0)
+        np.testing.assert_array_equal(mine[:keep].numpy(), full[r0:r0 + keep])
+        q.put((rank, "ok"))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world4_rows_x_trees_grid():
+    assert grid_2d(4, 2, 3) == (1, 1, 2) and grid_2d(8, 2, 5) == (1, 1, 4)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_2d, args=(r, 4, port, q)) for r in range(4)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {r: "ok" for r in range(4)}, res

@@ -86,6 +86,7 @@ struct TravLayout {
   bool sparse = false;          // pointer-format trees (deep / unbalanced), walked from global memory
   bool pretransposed = false;   // fp32 input transposed once into feature-major blocks (wide X, many chunks)
   bool hybrid = false;          // top levels in shared memory, deep levels + leaves in global memory
+  bool split = false;           // split nodes: fp32 threshold array + 1-byte feature array (F <= 127)
   std::vector<uint32_t> hyb_nodes;  // [records][2] deep levels of every tree (slot order)
   std::vector<float> hyb_leaves;    // [slots][L][K]
   std::vector<SparseTree> sparse_trees;

@@ -368,7 +368,7 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
 
   // plan with a node format; false if one tree of the deepest class does not fit
   auto plan = [&](bool codes) -> bool {
-    node_bytes = codes ? 4 : 8;
+    node_bytes = codes ? 4 : (out->split ? 5 : 8);
     // per 32-row block: codes mode = two u16 feature-major buffers (double
     // buffered, filled straight by bulk copy); fp32 mode = feature-major block
     // + dense staging block
@@ -386,7 +386,7 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
     misc = 1024 + trav_bar_bytes(nb) + trav_red_bytes(nb, G, K);
     const int32_t base_budget = kSmemMax - misc - nb * xw;
     auto chunk_bytes = [&](int32_t n, int32_t D) -> int64_t {
-      const int64_t nodes = (int64_t)n * ((1 << D) - 1) * node_bytes;
+      const int64_t nodes = (int64_t)n * ((1 << D) - 1) * node_bytes + (node_bytes == 5 ? 16 : 0);
       return (nodes + 15) / 16 * 16 + ((int64_t)n * (1 << D) * K * 4 + 15) / 16 * 16;
     };
     out->global_trees = false;
@@ -439,10 +439,20 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
     }
     return true;
   };
+  {
+    // split node arrays (fp32 thresholds + 1-byte features): opt-in until
+    // measured better (BRIDGER_SPLIT=1); needs F <= 127 (bit 7 = missing_left)
+    const char* env = std::getenv("BRIDGER_SPLIT");
+    out->split = !want_codes && F <= 127 && env && env[0] == '1';
+  }
   out->codes = want_codes && plan(true);
   if (!out->codes) {
     out->bin_table.clear();
     out->bin_offsets.clear();
+    plan(false);
+  }
+  if (out->split && out->global_trees) {  // split nodes only for shared-memory-resident chunks
+    out->split = false;
     plan(false);
   }
   out->hybrid = false;
@@ -535,7 +545,7 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
     // blocks instead of once per chunk CTA (measured: C5-shaped models)
     const char* env = std::getenv("BRIDGER_PRET");
     const int64_t work = (int64_t)F * (int64_t)bal.size();
-    out->pretransposed = !out->codes && !out->global_trees && (env ? env[0] != '0' : work >= 1024);
+    out->pretransposed = !out->codes && !out->split && !out->global_trees && (env ? env[0] != '0' : work >= 1024);
   }
   out->chunks.clear();
   out->data.clear();
@@ -551,7 +561,8 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
     c.n_trees = r.n;
     c.depth = D;
     c.first_slot = r.start;
-    const int64_t nodes = (int64_t)r.n * I * node_bytes;
+    const int64_t nodes = out->split ? (((int64_t)r.n * I * 4 + 15) / 16 * 16 + (int64_t)r.n * I)
+                                     : (int64_t)r.n * I * node_bytes;
     c.leaf_offset = (int32_t)((nodes + 15) / 16 * 16);
     c.bytes = (int32_t)(c.leaf_offset + ((int64_t)r.n * L * K * 4 + 15) / 16 * 16);
     out->data.resize(off + c.bytes, 0);
@@ -568,6 +579,13 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
           // leaves (feature 0, threshold 0): any code routes to identical leaves
           const uint32_t code = code_of_threshold(*out, pt.feature[i], pt.threshold[i]);
           nd[i] = (code << 16) | ((uint32_t)pt.feature[i] << 6) | (uint32_t)pt.missing[i];
+        }
+      } else if (out->split) {
+        float* th = reinterpret_cast<float*>(base) + (size_t)j * I;
+        uint8_t* fe = base + (((size_t)r.n * I * 4 + 15) / 16 * 16) + (size_t)j * I;
+        for (int32_t i = 0; i < I; ++i) {
+          th[i] = pt.threshold[i];
+          fe[i] = (uint8_t)(pt.feature[i] | (pt.missing[i] << 7));
         }
       } else {
         uint32_t* nd = reinterpret_cast<uint32_t*>(base) + (size_t)j * I * 2;

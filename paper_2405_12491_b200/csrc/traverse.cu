@@ -39,6 +39,10 @@ BRIDGER_TRAV_EXTERN(long long, false, false, 4)
 BRIDGER_TRAV_EXTERN(long long, true, false, 4)
 BRIDGER_TRAV_EXTERN(double, false, false, 4)
 BRIDGER_TRAV_EXTERN(double, true, false, 4)
+BRIDGER_TRAV_EXTERN(long long, false, false, 5)
+BRIDGER_TRAV_EXTERN(long long, true, false, 5)
+BRIDGER_TRAV_EXTERN(double, false, false, 5)
+BRIDGER_TRAV_EXTERN(double, true, false, 5)
 BRIDGER_TRAV_EXTERN(long long, false, true, 2)
 BRIDGER_TRAV_EXTERN(long long, true, true, 2)
 BRIDGER_TRAV_EXTERN(double, false, true, 2)
@@ -286,6 +290,13 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
                                : launch_trav_t<KT, long long, false, true, 2>(p, grid, block, smem, cluster, st);
         return L.has_missing ? launch_trav_t<KT, double, true, true, 2>(p, grid, block, smem, cluster, st)
                              : launch_trav_t<KT, double, false, true, 2>(p, grid, block, smem, cluster, st);
+      }
+      if (L.split) {
+        if (m->acc_int)
+          return L.has_missing ? launch_trav_t<KT, long long, true, false, 5>(p, grid, block, smem, cluster, st)
+                               : launch_trav_t<KT, long long, false, false, 5>(p, grid, block, smem, cluster, st);
+        return L.has_missing ? launch_trav_t<KT, double, true, false, 5>(p, grid, block, smem, cluster, st)
+                             : launch_trav_t<KT, double, false, false, 5>(p, grid, block, smem, cluster, st);
       }
       if (L.hybrid) {
         if (m->acc_int)

@@ -43,7 +43,7 @@ void hot_end(cudaStream_t st, cudaEvent_t start);
 // per-row partial sums into the leader CTA's shared memory over DSMEM
 // (st.shared::cluster + remote mbarrier arrive), the leader adds them in rank
 // order and finalizes -- no global partials, no second kernel.
-enum TravFmt : int { FMT_HEAP = 0, FMT_CODES = 1, FMT_SPARSE = 2, FMT_HEAP_T = 3, FMT_HYBRID = 4 };
+enum TravFmt : int { FMT_HEAP = 0, FMT_CODES = 1, FMT_SPARSE = 2, FMT_HEAP_T = 3, FMT_HYBRID = 4, FMT_SPLIT = 5 };
 enum TravMode : int32_t { TRAV_FINAL = 0, TRAV_PARTIAL = 1, TRAV_APPLY = 2, TRAV_CLUSTER = 3 };
 
 struct TravParams {
@@ -96,14 +96,39 @@ __device__ __forceinline__ int go_right(float x, uint2 nd) {
 
 // Walk NI trees [j, j+NI) of the chunk for this thread's row (NI independent
 // dependency chains for ILP), then gather and accumulate their leaf values.
-template <int NI, int KT, typename ACC, bool ML, bool CODES>
+template <int NI, int KT, typename ACC, bool ML, bool CODES, bool SPLIT = false>
 __device__ __forceinline__ void walk_trees(const TravParams& p, const TravChunk& c, const void* nodes,
                                            const float* leaves, const void* xl, int j, int I, int L, int D,
                                            int K, int64_t row, ACC (&acc)[KT]) {
   int idx[NI];
 #pragma unroll
   for (int u = 0; u < NI; ++u) idx[u] = 0;
-  if (CODES) {
+  if (SPLIT) {
+    // split node arrays: fp32 thresholds [n][I], then 1-byte features [n][I]
+    // (bit 7 = missing_left).  Byte loads of nearby nodes share 4-byte words,
+    // so the feature loads stay bank-conflict free through level 7.
+    const float* tb = static_cast<const float*>(nodes) + (size_t)j * I;
+    const uint8_t* fb = static_cast<const uint8_t*>(nodes) + (((size_t)c.n_trees * I * 4 + 15) & ~(size_t)15) + (size_t)j * I;
+    const float* xf = static_cast<const float*>(xl);
+    for (int lvl = 0; lvl < D; ++lvl) {
+      uint32_t f[NI];
+      float t[NI];
+#pragma unroll
+      for (int u = 0; u < NI; ++u) {
+        f[u] = fb[u * I + idx[u]];
+        t[u] = tb[u * I + idx[u]];
+      }
+      float x[NI];
+#pragma unroll
+      for (int u = 0; u < NI; ++u) x[u] = xf[(f[u] & 0x7Fu) * 32];
+#pragma unroll
+      for (int u = 0; u < NI; ++u) {
+        int r = !(x[u] <= t[u]);
+        if (ML) r &= !((f[u] >> 7) & isnan(x[u]));
+        idx[u] = 2 * idx[u] + 1 + r;
+      }
+    }
+  } else if (CODES) {
     // 4-byte node: code index (31..16) | feature*64 (15..6) | missing (0);
     // xl points at this lane's u16 code in a feature-major [F][32] block
     const uint32_t* nb = static_cast<const uint32_t*>(nodes) + (size_t)j * I;
@@ -177,13 +202,13 @@ __device__ __forceinline__ void walk_trees(const TravParams& p, const TravChunk&
 }
 
 // one pass over r (<= 12) trees with ILP = r
-template <int KT, typename ACC, bool ML, bool CODES, int MAXNI>
+template <int KT, typename ACC, bool ML, bool CODES, int MAXNI, bool SPLIT = false>
 __device__ __forceinline__ void walk_tail(int r, const TravParams& p, const TravChunk& c, const void* nodes,
                                           const float* leaves, const void* xl, int j, int I, int L, int D, int K,
                                           int64_t row, ACC (&acc)[KT]) {
   switch (r) {
 #define BRIDGER_TAIL(N) \
-  case N: if (N <= MAXNI) walk_trees<(N <= MAXNI ? N : 1), KT, ACC, ML, CODES>(p, c, nodes, leaves, xl, j, I, L, D, K, row, acc); break;
+  case N: if (N <= MAXNI) walk_trees<(N <= MAXNI ? N : 1), KT, ACC, ML, CODES, SPLIT>(p, c, nodes, leaves, xl, j, I, L, D, K, row, acc); break;
     BRIDGER_TAIL(1) BRIDGER_TAIL(2) BRIDGER_TAIL(3) BRIDGER_TAIL(4) BRIDGER_TAIL(5) BRIDGER_TAIL(6)
     BRIDGER_TAIL(7) BRIDGER_TAIL(8) BRIDGER_TAIL(9) BRIDGER_TAIL(10) BRIDGER_TAIL(11) BRIDGER_TAIL(12)
 #undef BRIDGER_TAIL
@@ -506,7 +531,7 @@ __global__ void __launch_bounds__(512, 1) trav_kernel(const TravParams p) {
       int j = t0;
       for (int q = 0; q < n_pass; ++q) {
         const int sz = nt / n_pass + (q < nt % n_pass ? 1 : 0);
-        walk_tail<KT, ACC, ML, CODES, NI_MAX>(sz, p, cc, nodes, leaves, xptr, j, I, L, D, K, row, acc);
+        walk_tail<KT, ACC, ML, CODES, NI_MAX, FMT == FMT_SPLIT>(sz, p, cc, nodes, leaves, xptr, j, I, L, D, K, row, acc);
         j += sz;
       }
     };

@@ -210,3 +210,14 @@ def test_pretransposed_input_mode(pret, monkeypatch):
     c, m = make_config("C5", n_trees=60)
     g, _ = check(m, gen_x(5, 0, 5003, 200), apply=True)
     assert g.layout()["format"] == ("heap_pretransposed" if pret == "1" else "heap")
+
+
+def test_split_node_format(monkeypatch):
+    """Split node arrays (fp32 thresholds + 1-byte features, bit 7 = missing)."""
+    monkeypatch.setenv("BRIDGER_SPLIT", "1")
+    m = perfect_ensemble(29, 90, 8, 21, kind="classification", n_classes=3, calib_rows=2048)
+    m = prune_ensemble(m, 29, p=0.1, with_missing=True)
+    X = inject_specials(gen_x(30, 0, 6007, 21), 30, rate=0.03)
+    check(m, X)
+    c, m2 = make_config("C2", n_trees=100)
+    check(m2, gen_x(2, 0, 9001, 28), apply=False)

@@ -338,13 +338,20 @@ def main():
         # D feature values (4 B) + K leaf values (4 B)
         alg = n * model.n_trees * (12 * cfg.depth + 4 * cfg.n_classes)
         sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
-        peak = sm_count * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e9   # GB/s
+        peak = sm_count * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e9   # GB/s, guide unit counts
+        psrc = f"derived from guide unit counts ({src} sm_max_mhz)"
+        try:  # measured on this pool's B200 by tools/smem_peak.cu (conflict-free LDS.64)
+            with open(os.path.join(ROOT, "profiles", "smem_peak.json")) as fh:
+                peak = json.load(fh)["smem_lds64_conflict_free_GBps"]
+                psrc = "measured (profiles/smem_peak.json: tools/smem_peak.cu, conflict-free LDS.64)"
+        except Exception:
+            pass
         achieved = alg / (hot_avg / 1e3) / 1e9
-        roof = {"bound": "alu", "resource": "shared-memory (LSU) pipe: 128 B/clk/SM x SMs x max SM clock",
+        roof = {"bound": "alu", "resource": "shared-memory (LSU) pipe bandwidth",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
                 "kernel": "trav_kernel", "kernel_ms": hot_avg,
                 "hbm_frac": (n * cfg.n_features * 4 + n * 4) / (hot_avg / 1e3) / 1e9 / peaks["hbm_gbs"],
-                "peak_source": f"derived from guide unit counts ({src} sm_max_mhz)"}
+                "peak_source": psrc}
     else:
         roof = {"bound": "tensor", "achieved": None, "peak": None, "unit": "TOP/s", "frac": None, "traffic": None,
                 "kernel": "path_contract", "kernel_ms": hot_avg}

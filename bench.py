@@ -157,9 +157,13 @@ def run_reference(args):
 
 
 def gemm_roofline(B, m, cfg, X, dev, args):
-    """The paper's GEMM form of steps a1..a4 on the same input: int8 tcgen05
-    path-contraction kernel (K2) throughput vs the measured int8 tensor peak,
-    and the whole GEMM variant's step time (the variant AUTO does not pick)."""
+    """The paper's GEMM form of steps a1..a4 on the same input (the variant AUTO
+    does not pick), in both pipelines:
+    * fused K5 (variant "gemm"): one warp-specialised kernel,
+      decisions only in shared memory; int8 tcgen05 throughput of the whole
+      kernel vs the measured int8 tensor peak;
+    * staged K1 -> K2 -> K3 (variant "gemm_staged"): the K2 path-contraction
+      kernel alone vs the int8 peak, K1 vs HBM."""
     import torch
     try:
         with open(os.path.join(ROOT, "profiles", "int8_peak.json")) as fh:
@@ -167,43 +171,57 @@ def gemm_roofline(B, m, cfg, X, dev, args):
             src = "measured (profiles/int8_peak.json: cuBLASLt s8 8192^3)"
     except Exception:
         peak, src = 2 * _peaks()[0].get("bf16_tflops", 1590.0), "bf16 measured x 2 (nominal int8/bf16 ratio)"
-    g = B.Model(m, device=dev.index, variant="gemm")
     n = X.shape[0]
     out = torch.empty(n, dtype=torch.int32, device=dev) if cfg.kind == "classification" else torch.empty((n, 1), device=dev)
-    for _ in range(2):
-        g.predict(X, out=out)
-    torch.cuda.synchronize(dev)
-    steps = 2
-    B.hot_kernel_timing(True)
-    B.hot_kernel_time()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(steps):
-        g.predict(X, out=out)
-    e1.record()
-    torch.cuda.synchronize(dev)
-    k2_ms, k2_n = B.hot_kernel_time()
-    step_ms = e0.elapsed_time(e1) / steps
     ip, lp = B.gemm_geometry(cfg.depth)
+    steps = 2
+
+    def timed(variant):
+        g = B.Model(m, device=dev.index, variant=variant)
+        for _ in range(2):
+            g.predict(X, out=out)
+        torch.cuda.synchronize(dev)
+        B.hot_kernel_timing(True)
+        for k in range(4):
+            B.hot_kernel_time(k)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            g.predict(X, out=out)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ks = [B.hot_kernel_time(k) for k in range(4)]
+        B.hot_kernel_timing(False)
+        g.close()
+        return e0.elapsed_time(e1) / steps, ks
+
     ops = 2.0 * n * cfg.n_trees * ip * lp * steps        # dense int8 ops of the contraction (padded)
-    achieved = ops / (k2_ms / 1e3) / 1e12
-    # K1 gather-compare in production form (tiled UMMA-layout decisions), timed by
-    # the library's events: HBM bytes = X rows read + n_trees * I_pad decision bytes written
-    k1_ms, _ = B.hot_kernel_time(1)
-    k3_ms, _ = B.hot_kernel_time(2)
+    f_ms, fk = timed("gemm")
+    k5_ms, k5_n = fk[3]
+    fused = {"kernel": "fz_kernel (K5: producer warps -> SMEM decisions -> tcgen05.mma kind::i8 -> TMEM -> "
+                       "leaf select/gather/reduce epilogue)", "bound": "tensor",
+             "achieved": ops / (k5_ms / 1e3) / 1e12, "peak": peak, "unit": "TOP/s",
+             "frac": ops / (k5_ms / 1e3) / 1e12 / peak, "peak_source": src,
+             "k5_ms_per_step": k5_ms / steps, "k5_launches_per_step": k5_n // steps,
+             "decisions_per_s": n * cfg.n_trees * ((1 << cfg.depth) - 1) * steps / (k5_ms / 1e3),
+             "ms_per_step": f_ms, "rows_per_s": n / (f_ms / 1e3)}
+    s_ms, sk = timed("gemm_staged")
+    k2_ms, k2_n = sk[0]
+    k1_ms, k3_ms = sk[1][0], sk[2][0]
     k1_bytes = steps * (n * cfg.n_features * 4 + n * cfg.n_trees * ip)
     hbm = _peaks()[0].get("hbm_gbs", 6541.1)
     gather = {"kernel": "gc_kernel (a1+a2: exact fp32 gather + less_equal, int8 decisions)", "bound": "hbm",
               "achieved": k1_bytes / (k1_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
               "frac": k1_bytes / (k1_ms / 1e3) / 1e9 / hbm, "ms_per_step": k1_ms / steps,
               "k3_leaf_gather_ms_per_step": k3_ms / steps}
-    B.hot_kernel_timing(False)
+    achieved = ops / (k2_ms / 1e3) / 1e12
     return {"kernel": "pc_kernel (tcgen05.mma.cta_group::1.kind::i8, TMEM accumulators)", "bound": "tensor",
             "achieved": achieved, "peak": peak, "unit": "TOP/s", "frac": achieved / peak, "peak_source": src,
             "k2_ms_per_step": k2_ms / steps, "k2_launches_per_step": k2_n // steps,
-            "gemm_variant_ms_per_step": step_ms, "gemm_variant_rows_per_s": n / (step_ms / 1e3),
-            "gather_compare": gather,
-            "note": "GEMM form of a1..a4 (decisions materialised per 128-row tile); AUTO selects the traversal"}
+            "gemm_variant_ms_per_step": s_ms, "gemm_variant_rows_per_s": n / (s_ms / 1e3),
+            "gather_compare": gather, "fused": fused,
+            "note": "GEMM form of a1..a4: 'fused' = K5 (variant gemm), the rest = staged K1->K2->K3 "
+                    "(variant gemm_staged); AUTO selects the traversal"}
 
 
 def workload_config(cfg, world):
@@ -221,7 +239,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
-    ap.add_argument("--variant", default=None, choices=[None, "auto", "traverse", "gemm"])
+    ap.add_argument("--variant", default=None, choices=[None, "auto", "traverse", "gemm", "gemm_staged"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gemm", action="store_true", help="skip the GEMM-form (tcgen05) sub-measurement")
     ap.add_argument("--e2e-steps", type=int, default=5)
@@ -297,6 +315,8 @@ def main():
         t_wall = time.perf_counter() - t_wall
     launches = B.launch_count() - l0
     hot_ms, hot_n = B.hot_kernel_time()
+    if hot_n == 0:  # fused GEMM-form variant: its one kernel is K5
+        hot_ms, hot_n = B.hot_kernel_time(3)
     B.hot_kernel_timing(False)
     step_ms = sum(e0.elapsed_time(e1) for e0, e1 in ev)
     t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
@@ -353,8 +373,16 @@ def main():
                 "hbm_frac": (n * cfg.n_features * 4 + n * 4) / (hot_avg / 1e3) / 1e9 / peaks["hbm_gbs"],
                 "peak_source": psrc}
     else:
-        roof = {"bound": "tensor", "achieved": None, "peak": None, "unit": "TOP/s", "frac": None, "traffic": None,
-                "kernel": "path_contract", "kernel_ms": hot_avg}
+        ip, lp = B.gemm_geometry(cfg.depth)
+        try:
+            with open(os.path.join(ROOT, "profiles", "int8_peak.json")) as fh:
+                ipeak = json.load(fh)["int8_tops_burst"]
+        except Exception:
+            ipeak = 2 * peaks.get("bf16_tflops", 1590.0)
+        ach = 2.0 * n * model.n_trees * ip * lp / (hot_avg / 1e3) / 1e12 if hot_avg > 0 else None
+        roof = {"bound": "tensor", "achieved": ach, "peak": ipeak, "unit": "TOP/s",
+                "frac": ach / ipeak if ach else None, "traffic": None,
+                "kernel": "fz_kernel" if variant == "gemm" else "pc_kernel", "kernel_ms": hot_avg}
     tr = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tr):
         try:

@@ -63,7 +63,11 @@ typedef enum { BRIDGER_POST_IDENTITY = 0, BRIDGER_POST_SIGMOID = 1 } bridger_pos
 typedef enum {
   BRIDGER_VARIANT_AUTO = 0,     /* per-depth choice from measured throughput */
   BRIDGER_VARIANT_TRAVERSE = 1, /* a4': traversal kernels (group-resident or streamed) */
-  BRIDGER_VARIANT_GEMM = 2      /* a1..a4: gather-compare + int8 tcgen05 path contraction */
+  BRIDGER_VARIANT_GEMM = 2,     /* a1..a7 fused (K5): producer warps write the int8
+                                   decisions straight into shared memory, int8 tcgen05 path contraction
+                                   into TMEM, leaf select + gather + reduce in the epilogue warps */
+  BRIDGER_VARIANT_GEMM_STAGED = 3 /* the same operator form staged through HBM: K1 gather-compare ->
+                                   K2 tcgen05 contraction -> K3 leaf gather/reduce (step-level kernels) */
 } bridger_variant;
 
 /*
@@ -213,7 +217,7 @@ int64_t bridger_launch_count(void);
 bridger_status bridger_hot_kernel_timing(int32_t enable);
 bridger_status bridger_hot_kernel_time(double* total_ms, int64_t* launches);
 /* Same for a kernel id: 0 = dominant kernel (traversal / path contraction K2),
- * 1 = gather-compare K1, 2 = leaf gather / reduce K3. */
+ * 1 = gather-compare K1, 2 = leaf gather / reduce K3, 3 = fused GEMM-form K5. */
 bridger_status bridger_hot_kernel_time_by(int32_t kernel, double* total_ms, int64_t* launches);
 
 #ifdef __cplusplus

@@ -20,7 +20,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libbridger.so")
 
 OK, E_NULL_ARG, E_SHAPE, E_INVALID_TREE, E_UNSUPPORTED, E_CUDA, E_OOM = range(7)
-VARIANTS = {"auto": 0, "traverse": 1, "gemm": 2}
+VARIANTS = {"auto": 0, "traverse": 1, "gemm": 2, "gemm_staged": 3}
 TIERS = {0: "E53", 1: "E63", 2: "F64"}
 
 
@@ -116,7 +116,7 @@ def hot_kernel_timing(enable: bool) -> None:
 
 def hot_kernel_time(kernel: int = 0):
     """(summed ms, launches) since the last query of kernel id `kernel`:
-    0 dominant (traversal / K2), 1 K1 gather-compare, 2 K3 leaf gather."""
+    0 dominant (traversal / K2), 1 K1 gather-compare, 2 K3 leaf gather, 3 fused K5."""
     ms, n = C.c_double(), C.c_int64()
     _check(_lib.bridger_hot_kernel_time_by(int(kernel), C.byref(ms), C.byref(n)))
     return ms.value, n.value

@@ -52,6 +52,8 @@ bool gemm_build(bridger_model* m, const bridger_model_desc* d, const std::vector
 void gemm_free(bridger_model* m);
 cudaError_t gemm_run(const bridger_model* m, const float* X, int64_t n_rows, void* out, int want,
                      int32_t total_trees, cudaStream_t st);
+cudaError_t gemm_run_fused(const bridger_model* m, const float* X, int64_t n_rows, void* out, int want,
+                           int32_t total_trees, cudaStream_t st);
 cudaError_t gemm_step_decisions(const bridger_model* m, const float* X, int64_t n_rows, int32_t tree0,
                                 int32_t n_trees, int8_t* out, cudaStream_t st, std::string* why);
 cudaError_t gemm_step_scores(const bridger_model* m, int32_t depth, const int8_t* P, int64_t rows,
@@ -124,7 +126,7 @@ static void free_model(bridger_model* m) {
 
 static int32_t resolve_variant(const bridger_model* m, int32_t v) {
   if (v == BRIDGER_VARIANT_TRAVERSE) return m->trav_ok ? v : -1;
-  if (v == BRIDGER_VARIANT_GEMM) return m->gemm_ok ? v : -1;
+  if (v == BRIDGER_VARIANT_GEMM || v == BRIDGER_VARIANT_GEMM_STAGED) return m->gemm_ok ? v : -1;
   // AUTO: measured on B200: the traversal wins at
   // every depth the GEMM form supports, so AUTO = traversal when available.
   if (m->trav_ok) return BRIDGER_VARIANT_TRAVERSE;
@@ -158,6 +160,8 @@ static bridger_status run(const bridger_model* m, const float* X, int64_t n_rows
   cudaError_t e;
   const int32_t v = m->resolved_variant;
   if (v == BRIDGER_VARIANT_GEMM && want != 3)
+    e = gemm_run_fused(m, X, n_rows, out, want, m->T, st);
+  else if (v == BRIDGER_VARIANT_GEMM_STAGED && want != 3)
     e = gemm_run(m, X, n_rows, out, want, m->T, st);
   else if (m->trav_ok)
     e = trav_run(m, X, n_rows, out, want, m->T, st);
@@ -355,6 +359,7 @@ bridger_status bridger_model_load(const bridger_model_desc* d, int cuda_device, 
   if (const char* env = std::getenv("BRIDGER_VARIANT")) {
     if (!std::strcmp(env, "traverse")) v = BRIDGER_VARIANT_TRAVERSE;
     else if (!std::strcmp(env, "gemm")) v = BRIDGER_VARIANT_GEMM;
+    else if (!std::strcmp(env, "gemm_staged")) v = BRIDGER_VARIANT_GEMM_STAGED;
   }
   m->variant = v;
   m->resolved_variant = resolve_variant(m, v);
@@ -380,7 +385,7 @@ bridger_status bridger_model_info(const bridger_model* m, int32_t* max_depth, in
 
 bridger_status bridger_model_set_variant(bridger_model* m, int32_t variant) {
   if (!m) return fail(BRIDGER_E_NULL_ARG, "model is NULL");
-  if (variant < 0 || variant > 2) return fail(BRIDGER_E_UNSUPPORTED, "unknown variant");
+  if (variant < 0 || variant > 3) return fail(BRIDGER_E_UNSUPPORTED, "unknown variant");
   const int32_t r = resolve_variant(m, variant);
   if (r < 0) return fail(BRIDGER_E_UNSUPPORTED, "variant not available for this model");
   m->variant = variant;

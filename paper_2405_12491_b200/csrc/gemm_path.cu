@@ -48,6 +48,8 @@ struct GemmClassDev {
   int64_t leaf_off;   // float [n][L][K]  leaf values (fixed-point scaled when exact)
   int32_t first_slot; // index of the class's first tree in slot order
   int32_t pad_;
+  int64_t node_off;   // uint2 [n][i_pad] {feature | missing<<31, threshold} (K5; row I = constant-1 node)
+  int64_t cmat2_off;  // int8 C'_D canonical K-major: C_D plus row I = popc(l) (K5, a4 folded in)
 };
 
 struct GemmHost {
@@ -57,6 +59,7 @@ struct GemmHost {
   std::vector<int32_t> tree_class;     // original tree -> class index
   int64_t max_p_per_row = 0;           // max over classes of n_trees * i_pad
   int32_t max_trees = 0;
+  bool has_missing = false;            // any real node with missing_left (K5 ML instantiation)
 };
 
 static constexpr int kSmemMax = 232448;
@@ -359,6 +362,337 @@ __global__ void __launch_bounds__(256) lg_kernel(const int16_t* __restrict__ lea
   }
 }
 
+// ------------------------------------------------------------------ K5 -----
+// Fused, warp-specialised GEMM form: a1..a7 in ONE kernel,
+// decisions never leave shared memory.  Persistent CTAs own 128-row tiles; per
+// tile every tree of the depth class is one pipeline item:
+//   producer warps (kFzProd) a1+a2: the X tile sits feature-major in SMEM
+//        (stride 129: conflict-free transpose stores AND gathers); a warp keeps
+//        16 node records of one K chunk in registers and writes the packed
+//        decisions of 32 rows straight into the UMMA canonical K-major A stage
+//   loader warp   C'_D once, then each tree's node records into a small ring
+//                 (bulk copies, TMA engine)
+//   MMA warp      a3: I_pad/32 tcgen05.mma kind::i8 per item into one of two
+//                 TMEM accumulators (as K2)
+//   epilogue warps (kFzEpi) a4..a7: tcgen05.ld, leaf select, leaf-value gather
+//        and int64 accumulation in registers across the tile's trees; at the
+//        tile's last tree the column parts are summed in SMEM and finalized.
+// a4 is folded into the contraction: the padding K row I (always present,
+// since 2^D - 1 is odd and I_pad a multiple of 32) carries a constant decision
+// 1 (feature F = a constant-zero row of the X tile, threshold +inf) and C'_D[I][l] = popc(l) (-64 for padding
+// columns), so S'[l] = S[l] + popc(l) = D exactly at the reached leaf
+// (D_D[l] = D - popc(l), reading c14) and < D everywhere else.
+constexpr int kFzProd = 8;
+constexpr int kFzEpi = 8;
+constexpr int kFzThreads = (kFzProd + kFzEpi + 2) * 32;
+constexpr int kFzNodeMax = 32;  // node-record ring depth cap (sized by bytes in fz_plan)
+constexpr int kFzXStride = 129;
+
+struct FzParams {
+  const float* X;
+  int64_t n_rows;
+  int32_t F, K, L;
+  int32_t n_tiles;
+  const uint8_t* gbase;
+  GemmClassDev cls;
+  int32_t stages;     // A ring depth
+  int32_t nstages;    // node-record ring depth
+  int32_t tmem_cols;
+  int32_t b_bytes;
+  int32_t x_off, a_off, n_off, red_off, bar_off, smem;  // shared-memory carve-up (fz_plan)
+  int32_t first, last;  // depth-class position (accbuf in/out)
+  void* accbuf;         // [n_rows][K] ACC, when the model has several depth classes
+  FinalizeArgs fin;
+};
+
+template <int KT, typename ACC, bool ML>
+__global__ void __launch_bounds__(kFzThreads, 1) fz_kernel(const FzParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ip = p.cls.i_pad, lp = p.cls.l_pad, D = p.cls.depth, nt = p.cls.n_trees;
+  const int NS = p.stages, F = p.F;
+  const uint32_t a_bytes = 128u * (uint32_t)ip;
+  uint8_t* sB = smem;
+  float* Xs = reinterpret_cast<float*>(smem + p.x_off);
+  uint8_t* sA = smem + p.a_off;
+  uint2* sN = reinterpret_cast<uint2*>(smem + p.n_off);  // [nstages][ip]
+  const int NN = p.nstages;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bar_off);
+  uint64_t* bfull = bars;                      // [1]
+  uint64_t* afull = bars + 1;                  // [NS]
+  uint64_t* aempty = afull + NS;               // [NS]
+  uint64_t* tfull = aempty + NS;               // [2]
+  uint64_t* tempty = tfull + 2;                // [2]
+  uint64_t* nfull = tempty + 2;                // [NN]
+  uint64_t* nempty = nfull + NN;               // [NN]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(nempty + NN);
+  constexpr int kLoader = kFzProd, kMma = kFzProd + 1, kEpi0 = kFzProd + 2;
+
+  if (tid == 0) {
+    ptx::mbar_init(bfull, 1);
+    for (int i = 0; i < NS; ++i) {
+      ptx::mbar_init(&afull[i], kFzProd * 32);
+      ptx::mbar_init(&aempty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&tfull[i], 1);
+      ptx::mbar_init(&tempty[i], kFzEpi * 32);
+    }
+    for (int i = 0; i < NN; ++i) {
+      ptx::mbar_init(&nfull[i], 1);
+      ptx::mbar_init(&nempty[i], kFzProd);
+    }
+    ptx::fence_barrier_init();
+    ptx::fence_proxy_async();
+  }
+  if (warp == kMma) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(ptx::s2u(tmem_holder)),
+                 "r"(p.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = *tmem_holder;
+  const int grid = gridDim.x;
+  const int my_tiles = p.n_tiles > (int)blockIdx.x ? (p.n_tiles - 1 - (int)blockIdx.x) / grid + 1 : 0;
+  const int n_items = my_tiles * nt;
+
+  if (warp < kFzProd) {
+    // ---------------------------------------------------------- producers --
+    const int n_kc = ip / 16;
+    const int n_pairs = n_kc * 4;  // (K chunk, 32-row group)
+    const int per = (n_pairs + kFzProd - 1) / kFzProd;
+    const int p_lo = warp * per, p_hi = min(n_pairs, p_lo + per);
+    int k = 0;
+    for (int ti = 0; ti < my_tiles; ++ti) {
+      const int64_t tile_row0 = (int64_t)(blockIdx.x + ti * grid) * 128;
+      const int tile_rows = (int)(p.n_rows - tile_row0 < 128 ? p.n_rows - tile_row0 : 128);
+      // the previous tile's decisions are all written: reload the X tile
+      asm volatile("bar.sync 1, %0;" ::"r"(kFzProd * 32) : "memory");
+      if (ti == 0)
+        for (int e = tid; e < 128; e += kFzProd * 32) Xs[F * kFzXStride + e] = 0.0f;  // row F: constant node
+      const float* src = p.X + tile_row0 * F;
+      if (tile_rows == 128) {
+        const float4* s4 = reinterpret_cast<const float4*>(src);
+        for (int e4 = tid; e4 < 32 * F; e4 += kFzProd * 32) {
+          const float4 v = __ldg(s4 + e4);
+          const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int e = 4 * e4 + q, rr = e / F, f = e - rr * F;
+            Xs[f * kFzXStride + rr] = vv[q];
+          }
+        }
+      } else {
+        for (int e = tid; e < 128 * F; e += kFzProd * 32) {
+          const int rr = e / F, f = e - rr * F;
+          Xs[f * kFzXStride + rr] = rr < tile_rows ? __ldg(src + e) : 0.0f;
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(kFzProd * 32) : "memory");
+      for (int t = 0; t < nt; ++t, ++k) {
+        const int s = k % NS, ns = k % NN;
+        ptx::mbar_wait(&nfull[ns], (k / NN) & 1);              // node records of tree t
+        ptx::mbar_wait(&aempty[s], ((k / NS) & 1) ^ 1);        // A stage free
+        const uint2* nd = sN + (size_t)ns * ip;
+        uint8_t* a = sA + (size_t)s * a_bytes;
+        // this warp's pairs are consecutive: runs of row groups [rg0, rg1) of one K chunk
+        for (int pr = p_lo; pr < p_hi;) {
+          const int kc = pr >> 2, rg0 = pr & 3;
+          const int rg1 = min(4, rg0 + (p_hi - pr));
+          pr += rg1 - rg0;
+          // 16 node records (broadcast loads) -> per-node shared address of this
+          // lane's x in row group rg0; the other row groups are +128 B immediates
+          uint32_t xa[16];
+          float th[16];
+          uint32_t mlm = 0;  // missing-left nodes (bit b)
+          const uint4* n4 = reinterpret_cast<const uint4*>(nd + kc * 16);
+          const uint32_t xbase = ptx::s2u(Xs) + (uint32_t)(rg0 * 32 + lane) * 4u;
+#pragma unroll
+          for (int b = 0; b < 8; ++b) {
+            const uint4 v = n4[b];
+            xa[2 * b] = xbase + (v.x & 0x7fffffffu) * (uint32_t)(kFzXStride * 4);
+            xa[2 * b + 1] = xbase + (v.z & 0x7fffffffu) * (uint32_t)(kFzXStride * 4);
+            th[2 * b] = __uint_as_float(v.y);
+            th[2 * b + 1] = __uint_as_float(v.w);
+            if (ML) mlm |= (v.x >> 31) << (2 * b) | (v.z >> 31) << (2 * b + 1);
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (j < rg1 - rg0) {
+              uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+              for (int b = 0; b < 16; ++b) {
+                float x;  // a1: exact fp32 gather (feature-major tile, conflict-free)
+                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(xa[b] + (uint32_t)(j * 128)));
+                uint32_t msk;  // a2: less_equal as an all-ones mask (NaN -> 0, goes right)
+                asm("set.le.u32.f32 %0, %1, %2;" : "=r"(msk) : "f"(x), "f"(th[b]));
+                if (ML) {  // missing-left node: unordered (NaN) compares true
+                  uint32_t mu;
+                  asm("set.leu.u32.f32 %0, %1, %2;" : "=r"(mu) : "f"(x), "f"(th[b]));
+                  msk |= mu & (0u - ((mlm >> b) & 1u));
+                }
+                w[b >> 2] |= msk & (1u << (8 * (b & 3)));
+              }
+              *reinterpret_cast<uint4*>(a + (size_t)kc * 2048 + ((rg0 + j) * 32 + lane) * 16) =
+                  make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&nempty[ns]);
+        ptx::fence_proxy_async();  // generic-proxy stores -> tensor-core (async proxy) reads
+        ptx::mbar_arrive(&afull[s]);
+      }
+    }
+  } else if (warp == kLoader) {
+    // -------------------------------------------------- bulk-copy loader --
+    if (lane == 0) {
+      ptx::mbar_arrive_expect_tx(bfull, (uint32_t)p.b_bytes);
+      for (int o = 0; o < p.b_bytes; o += 32768)
+        ptx::bulk_g2s(sB + o, p.gbase + p.cls.cmat2_off + o, (uint32_t)min(32768, p.b_bytes - o), bfull);
+      const uint8_t* nodes = p.gbase + p.cls.node_off;
+      const uint32_t nb = 8u * (uint32_t)ip;
+      for (int k = 0; k < n_items; ++k) {
+        const int ns = k % NN, t = k % nt;
+        ptx::mbar_wait(&nempty[ns], ((k / NN) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&nfull[ns], nb);
+        ptx::bulk_g2s(sN + (size_t)ns * ip, nodes + (size_t)t * nb, nb, &nfull[ns]);
+      }
+    }
+  } else if (warp == kMma) {
+    // ---------------------------------------------------------- MMA issue --
+    if (lane == 0) {
+      ptx::mbar_wait(bfull, 0);
+      const uint32_t idesc = umma::idesc_i8(lp);
+      const uint32_t sA_u = ptx::s2u(sA), sB_u = ptx::s2u(sB);
+      for (int k = 0; k < n_items; ++k) {
+        const int s = k % NS, acc = k & 1;
+        ptx::mbar_wait(&tempty[acc], ((k >> 1) & 1) ^ 1);
+        ptx::mbar_wait(&afull[s], (k / NS) & 1);
+        umma::fence_after();
+        const uint32_t a0 = sA_u + (uint32_t)s * a_bytes;
+        for (int ks = 0; ks < ip / 32; ++ks) {
+          const uint64_t ad = umma::smem_desc(a0 + (uint32_t)ks * 2u * 2048u, 2048u, 128u);
+          const uint64_t bd = umma::smem_desc(sB_u + (uint32_t)ks * 2u * (uint32_t)lp * 16u, (uint32_t)lp * 16u, 128u);
+          umma::mma_i8(tmem + (uint32_t)(acc * lp), ad, bd, idesc, ks > 0 ? 1u : 0u);
+        }
+        umma::commit(&aempty[s]);
+        umma::commit(&tfull[acc]);
+      }
+    }
+  } else {
+    // ----------------------------------------------------------- epilogue --
+    const int ew = warp - kEpi0;
+    // tcgen05.ld: warp w may only touch TMEM lanes 32*(w%4)..+31, so the row
+    // quadrant follows the hardware warp id (epilogue warps start at kEpi0)
+    const int quad = warp & 3, part = ew >> 2;            // TMEM lane quadrant, column half
+    const int n_parts = lp >= 32 ? 2 : 1;
+    const int cols = lp / n_parts;
+    const bool active = part < n_parts;
+    const int r_in = quad * 32 + lane;
+    const int K = p.K, L = p.L;
+    const float* E = reinterpret_cast<const float*>(p.gbase + p.cls.leaf_off);
+    ACC* red = reinterpret_cast<ACC*>(smem + p.red_off);  // [128][KT] part-1 partials
+    ACC acc[KT];
+#pragma unroll
+    for (int q = 0; q < KT; ++q) acc[q] = ACC(0);
+    // a5 is software-pipelined: the leaf values of item k are loaded while
+    // item k+1's accumulator is read from TMEM, and added one item later
+    float pv[KT];
+    bool pend = false;
+    auto add_pending = [&]() {
+      if (pend) {
+#pragma unroll
+        for (int q = 0; q < KT; ++q)
+          if (q < K) {
+            if (std::is_same<ACC, long long>::value) acc[q] += (ACC)__float2ll_rz(pv[q]);
+            else acc[q] += (ACC)pv[q];
+          }
+      }
+      pend = false;
+    };
+    int k = 0;
+    for (int ti = 0; ti < my_tiles; ++ti) {
+      const int64_t row = (int64_t)(blockIdx.x + ti * grid) * 128 + r_in;
+      for (int t = 0; t < nt; ++t, ++k) {
+        const int sacc = k & 1;
+        ptx::mbar_wait(&tfull[sacc], (k >> 1) & 1);
+        umma::fence_after();
+        const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(sacc * lp);
+        int leaf = -1;
+        if (active) {
+          int cb = part * cols;
+          const int ce = cb + cols;
+          for (; cb + 32 <= ce; cb += 32) {
+            uint32_t v[16], w[16];
+            umma::ld16(tbase + cb, v);
+            umma::ld16(tbase + cb + 16, w);
+            umma::wait_ld();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              if ((int32_t)v[j] == D) leaf = cb + j;  // a4: S'[l] == D at the reached leaf only
+              if ((int32_t)w[j] == D) leaf = cb + 16 + j;
+            }
+          }
+          if (cb < ce) {
+            uint32_t v[16];
+            umma::ld16(tbase + cb, v);
+            umma::wait_ld();
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if ((int32_t)v[j] == D) leaf = cb + j;
+          }
+        }
+        umma::fence_before();
+        ptx::mbar_arrive(&tempty[sacc]);
+        add_pending();
+        if (leaf >= 0) {  // a5 + a6: leaf-value gather, exact fixed-point accumulation
+          const float* e = E + ((size_t)t * L + leaf) * K;
+#pragma unroll
+          for (int q = 0; q < KT; ++q) pv[q] = q < K ? __ldg(e + q) : 0.0f;
+          pend = true;
+        }
+      }
+      add_pending();
+      // tile done: sum the two column parts, then finalize (a7) or hand on
+      if (n_parts > 1 && part == 1) {
+#pragma unroll
+        for (int q = 0; q < KT; ++q) red[r_in * KT + q] = acc[q];
+      }
+      asm volatile("bar.sync 2, %0;" ::"r"(kFzEpi * 32) : "memory");
+      if (part == 0 && row < p.n_rows) {
+        if (n_parts > 1) {
+#pragma unroll
+          for (int q = 0; q < KT; ++q) acc[q] += red[r_in * KT + q];
+        }
+        ACC* ab = static_cast<ACC*>(p.accbuf);
+        if (!p.first) {
+#pragma unroll
+          for (int q = 0; q < KT; ++q)
+            if (q < K) acc[q] += ab[row * K + q];
+        }
+        if (p.last) {
+          finalize_row<KT, ACC>(p.fin, row, acc);
+        } else {
+#pragma unroll
+          for (int q = 0; q < KT; ++q)
+            if (q < K) ab[row * K + q] = acc[q];
+        }
+      }
+      asm volatile("bar.sync 2, %0;" ::"r"(kFzEpi * 32) : "memory");
+#pragma unroll
+      for (int q = 0; q < KT; ++q) acc[q] = ACC(0);
+    }
+  }
+  __syncthreads();
+  umma::fence_after();
+  if (warp == kMma)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols) : "memory");
+}
+
 // ------------------------------------------------------------- host side ----
 static int dev_sms(int dev) {
   int n = 148;
@@ -414,6 +748,21 @@ bool gemm_build(bridger_model* m, const bridger_model_desc* d, const std::vector
       int32_t* dv = reinterpret_cast<int32_t*>(buf.data() + c.dv_off);
       for (int32_t l = 0; l < c.l_pad; ++l) dv[l] = l < L ? Dv[l] : 127;
     }
+    align(256);
+    c.cmat2_off = (int64_t)buf.size();
+    {
+      std::vector<int8_t> Cm((size_t)c.i_pad * c.l_pad);
+      path_matrix(D, c.i_pad, c.l_pad, Cm.data(), nullptr);
+      for (int32_t l = 0; l < c.l_pad; ++l) Cm[(size_t)I * c.l_pad + l] = l < L ? (int8_t)__builtin_popcount(l) : (int8_t)-64;
+      buf.resize(buf.size() + (size_t)c.i_pad * c.l_pad);
+      int8_t* dst = reinterpret_cast<int8_t*>(buf.data() + c.cmat2_off);
+      for (int32_t kc = 0; kc < c.i_pad / 16; ++kc)
+        for (int32_t l = 0; l < c.l_pad; ++l)
+          for (int32_t b = 0; b < 16; ++b) dst[((size_t)kc * c.l_pad + l) * 16 + b] = Cm[(size_t)(kc * 16 + b) * c.l_pad + l];
+    }
+    align(16);
+    c.node_off = (int64_t)buf.size();
+    buf.resize(buf.size() + 8 * (size_t)n * c.i_pad);
     align(16);
     c.feat_off = (int64_t)buf.size();
     buf.resize(buf.size() + 4 * (size_t)n * c.i_pad);
@@ -433,11 +782,23 @@ bool gemm_build(bridger_model* m, const bridger_model_desc* d, const std::vector
       for (int32_t i = 0; i < c.i_pad; ++i) {
         if (i < I) {
           fe[i] = pt.feature[i] | (pt.missing[i] ? (int32_t)0x80000000 : 0);
+          if (pt.missing[i]) h->has_missing = true;
           th[i] = pt.threshold[i];
         } else {
           fe[i] = 0;  // padding: x <= NaN is false, so P[i >= I] == 0 exactly
           th[i] = std::numeric_limits<float>::quiet_NaN();
         }
+      }
+      uint32_t* nr = reinterpret_cast<uint32_t*>(buf.data() + c.node_off) + (size_t)j * c.i_pad * 2;
+      for (int32_t i = 0; i < c.i_pad; ++i) {
+        float tv = th[i];
+        uint32_t fv = (uint32_t)fe[i];
+        if (i == I) {  // K5 constant-1 decision: the X tile's extra row F is all zeros, 0 <= +inf
+          tv = std::numeric_limits<float>::infinity();
+          fv = (uint32_t)d->n_features;
+        }
+        std::memcpy(&nr[2 * i + 1], &tv, 4);
+        nr[2 * i] = fv;
       }
       float* lv = reinterpret_cast<float*>(buf.data() + c.leaf_off) + (size_t)j * L * K;
       for (int32_t l = 0; l < L * K; ++l) lv[l] = m->acc_int ? std::ldexp(pt.leaf_value[l], -m->ex.q) : pt.leaf_value[l];
@@ -587,6 +948,108 @@ cudaError_t gemm_run(const bridger_model* m, const float* X, int64_t n_rows, voi
   cudaFreeAsync(P, st);
   cudaFreeAsync(leaf, st);
   cudaFreeAsync(accbuf, st);
+  return e;
+}
+
+// Shared-memory carve-up of K5: C'_D | X tile | A ring | node ring | partials | barriers.
+static bool fz_plan(const GemmClassDev& c, int32_t F, int32_t K, FzParams* p) {
+  int KT = 1;
+  while (KT < K) KT *= 2;
+  if (KT > 16) KT = 64;
+  const int a_bytes = 128 * c.i_pad;
+  p->b_bytes = c.i_pad * c.l_pad;
+  int off = (p->b_bytes + 1023) / 1024 * 1024;
+  p->x_off = off;
+  off += (kFzXStride * (F + 1) * 4 + 1023) / 1024 * 1024;  // + constant-zero row F
+  p->a_off = off;
+  // node ring: ~16 KB in flight covers the L2 latency of the per-tree bulk copies
+  p->nstages = std::max(4, std::min(kFzNodeMax, 16384 / (8 * c.i_pad)));
+  const int fixed = off + p->nstages * c.i_pad * 8 + 128 * KT * 8 + 512;
+  int stages = 6;
+  while (stages > 2 && fixed + stages * a_bytes > kSmemMax) --stages;
+  if (fixed + stages * a_bytes > kSmemMax) return false;  // X tile too wide for this depth
+  p->stages = stages;
+  off += stages * a_bytes;
+  p->n_off = off;
+  off += p->nstages * c.i_pad * 8;
+  p->red_off = off;
+  off += 128 * KT * 8;
+  p->bar_off = off;
+  off += (1 + 2 * stages + 4 + 2 * p->nstages) * 8 + 16;
+  p->smem = off;
+  return true;
+}
+
+// K5: one fused launch per depth class (accumulators carried in HBM between
+// classes only when the model mixes depths).
+cudaError_t gemm_run_fused(const bridger_model* m, const float* X, int64_t n_rows, void* out, int want,
+                           int32_t total_trees, cudaStream_t st) {
+  const GemmHost* h = static_cast<const GemmHost*>(m->gemm_host);
+  const uint8_t* gbase = static_cast<const uint8_t*>(m->d_gemm);
+  const int nc = (int)h->classes.size();
+  for (const GemmClassDev& c : h->classes) {
+    FzParams probe{};
+    if (!fz_plan(c, m->F, m->K, &probe))  // input too wide to stage next to C'_D: staged K1->K2->K3
+      return gemm_run(m, X, n_rows, out, want, total_trees, st);
+  }
+  void* accbuf = nullptr;
+  cudaError_t e = cudaSuccess;
+  if (nc > 1) e = cudaMallocAsync(&accbuf, (size_t)n_rows * m->K * 8, st);
+  FinalizeArgs fin{};
+  fin.task = m->task;
+  fin.agg = m->agg;
+  fin.post = m->post;
+  fin.K = m->K;
+  fin.total_trees = total_trees;
+  fin.q = m->ex.q;
+  fin.acc_int = m->acc_int ? 1 : 0;
+  fin.want = want;
+  fin.leaf_scale = m->leaf_scale;
+  fin.base = m->d_base;
+  fin.out = out;
+  const int64_t n_tiles64 = (n_rows + 127) / 128;
+  if (n_tiles64 > INT32_MAX) return cudaErrorInvalidValue;
+  for (int ci = 0; ci < nc && e == cudaSuccess; ++ci) {
+    const GemmClassDev& c = h->classes[ci];
+    FzParams p{};
+    p.X = X;
+    p.n_rows = n_rows;
+    p.F = m->F;
+    p.K = m->K;
+    p.L = 1 << c.depth;
+    p.n_tiles = (int32_t)n_tiles64;
+    p.gbase = gbase;
+    p.cls = c;
+    int cols = 32;
+    while (cols < 2 * c.l_pad) cols *= 2;
+    p.tmem_cols = cols;
+    p.first = ci == 0;
+    p.last = ci == nc - 1;
+    p.accbuf = accbuf;
+    p.fin = fin;
+    if (!fz_plan(c, m->F, m->K, &p)) return cudaErrorInvalidConfiguration;
+    const int smem = p.smem;
+    const int grid = (int)std::min<int64_t>(n_tiles64, dev_sms(m->device));
+    cudaEvent_t ev;
+    hot_begin(st, &ev);
+    auto launch = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+      kern<<<grid, kFzThreads, smem, st>>>(p);
+    };
+    BRIDGER_DISPATCH_KT(m->K, {
+      if (m->acc_int) {
+        if (h->has_missing) launch(fz_kernel<KT, long long, true>);
+        else launch(fz_kernel<KT, long long, false>);
+      } else {
+        if (h->has_missing) launch(fz_kernel<KT, double, true>);
+        else launch(fz_kernel<KT, double, false>);
+      }
+    });
+    hot_end_id(st, ev, 3);
+    count_launch();
+    e = cudaGetLastError();
+  }
+  if (accbuf) cudaFreeAsync(accbuf, st);
   return e;
 }
 

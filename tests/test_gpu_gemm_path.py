@@ -5,14 +5,17 @@ contraction, K3 leaf gather/reduce) against definitions the mathematics fixes:
   computed on the CPU from the library's own padded heap arrays, bitwise;
 * K2 S == P . C_D as a CPU int32 matmul (C_D from bridger_path_matrix, pinned by
   exhaustive enumeration in test_boundary_cpu.py), bitwise, on random 0/1 P;
-* end to end (variant "gemm"): labels / leaves / scores == oracle (same bar as
-  the traversal).
+* end to end, for both the fused K5 kernel (variant "gemm": decisions never
+  leave shared memory, a4 folded into the contraction) and the staged
+  K1 -> K2 -> K3 pipeline (variant "gemm_staged"): labels / scores / raw
+  accumulators == oracle (same bar as the traversal).
 """
 import numpy as np
 import pytest
 
 import oracle
 from synth import gen_x, inject_specials, make_config, perfect_ensemble, prune_ensemble
+from synth.trees import ModelDesc
 from tests.test_gpu_parity import check, dev
 
 pytestmark = pytest.mark.gpu
@@ -65,20 +68,58 @@ def test_k2_path_contraction_is_int_matmul(D):
     np.testing.assert_array_equal(S, ref)
 
 
+@pytest.mark.parametrize("variant", ["gemm", "gemm_staged"])
 @pytest.mark.parametrize("name,rows", [("C1", None), ("C2", 9001), ("C3", 5001)])
-def test_gemm_variant_end_to_end(name, rows):
+def test_gemm_variant_end_to_end(name, rows, variant):
     c, m = make_config(name, n_trees=None if name != "C3" else 120)
     if name == "C1":
         from synth import iris_like_x
         X = iris_like_x(1)
     else:
         X = gen_x(c.seed, 0, rows, c.n_features)
-    g, _ = check(m, X, variant="gemm", apply=False)
-    assert g.info()["variant"] == "gemm"
+    g, _ = check(m, X, variant=variant, apply=False)
+    assert g.info()["variant"] == variant
 
 
-def test_gemm_variant_pruned_missing_mixed_depth():
+@pytest.mark.parametrize("variant", ["gemm", "gemm_staged"])
+def test_gemm_variant_pruned_missing_mixed_depth(variant):
     m = perfect_ensemble(25, 40, 7, 13, kind="classification", n_classes=4, calib_rows=1024)
     m = prune_ensemble(m, 25, p=0.2, with_missing=True)
     X = inject_specials(gen_x(26, 0, 3001, 13), 26, rate=0.02)
+    check(m, X, variant=variant, apply=False)
+
+
+@pytest.mark.parametrize("D", [1, 2, 3, 4, 5, 6, 7, 8])
+def test_fused_every_depth(D):
+    # every K5 geometry (I_pad 32..256, L_pad 16..256, popc row I), ragged last tile
+    m = perfect_ensemble(40 + D, 9, D, 11, kind="classification", n_classes=3, calib_rows=512)
+    X = inject_specials(gen_x(60 + D, 0, 777, 11), 60 + D, rate=0.01)
     check(m, X, variant="gemm", apply=False)
+
+
+def test_fused_many_tiles_per_cta_regression():
+    # > 148 tiles: each persistent CTA walks several row tiles (accumulators reset
+    # per tile), GBDT SUM aggregation, E53 bitwise
+    m = perfect_ensemble(71, 30, 6, 17, kind="regression", calib_rows=1024)
+    check(m, gen_x(72, 0, 148 * 128 * 2 + 77, 17), variant="gemm", apply=False)
+
+
+def test_fused_multiclass_k8_and_fp64_tier():
+    m = perfect_ensemble(73, 25, 5, 12, kind="classification", n_classes=8, calib_rows=512)
+    check(m, gen_x(74, 0, 4099, 12), variant="gemm", apply=False)
+    # subnormal leaf values force the fp64 accumulation tier (reading c9): rtol 1e-5
+    v = m.value.copy()
+    v[::7] = np.float32(1e-40)
+    m2 = ModelDesc(**{**m.__dict__, "value": v})
+    g = B.Model(m2, variant="gemm")
+    assert g.info()["exact_tier"] == "F64"
+    check(m2, gen_x(74, 0, 2001, 12), variant="gemm", exact=False, apply=False)
+
+
+def test_fused_matches_staged_bitwise_full_c2_block():
+    # the two GEMM-form pipelines agree bit for bit on raw int64 accumulators
+    c, m = make_config("C2")
+    X = dev(gen_x(2, 0, 50000, 28))
+    a = B.Model(m, variant="gemm").predict_raw(X).cpu().numpy()
+    b = B.Model(m, variant="gemm_staged").predict_raw(X).cpu().numpy()
+    np.testing.assert_array_equal(a, b)

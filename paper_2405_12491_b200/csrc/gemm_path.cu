@@ -397,6 +397,7 @@ struct FzParams {
   GemmClassDev cls;
   int32_t stages;     // A ring depth
   int32_t nstages;    // node-record ring depth
+  int32_t tstages;    // TMEM accumulator ring depth
   int32_t tmem_cols;
   int32_t b_bytes;
   int32_t x_off, a_off, n_off, red_off, bar_off, smem;  // shared-memory carve-up (fz_plan)
@@ -421,9 +422,10 @@ __global__ void __launch_bounds__(kFzThreads, 1) fz_kernel(const FzParams p) {
   uint64_t* bfull = bars;                      // [1]
   uint64_t* afull = bars + 1;                  // [NS]
   uint64_t* aempty = afull + NS;               // [NS]
-  uint64_t* tfull = aempty + NS;               // [2]
-  uint64_t* tempty = tfull + 2;                // [2]
-  uint64_t* nfull = tempty + 2;                // [NN]
+  const int NT = p.tstages;
+  uint64_t* tfull = aempty + NS;               // [NT]
+  uint64_t* tempty = tfull + NT;               // [NT]
+  uint64_t* nfull = tempty + NT;               // [NN]
   uint64_t* nempty = nfull + NN;               // [NN]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(nempty + NN);
   constexpr int kLoader = kFzProd, kMma = kFzProd + 1, kEpi0 = kFzProd + 2;
@@ -434,7 +436,7 @@ __global__ void __launch_bounds__(kFzThreads, 1) fz_kernel(const FzParams p) {
       ptx::mbar_init(&afull[i], kFzProd * 32);
       ptx::mbar_init(&aempty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NT; ++i) {
       ptx::mbar_init(&tfull[i], 1);
       ptx::mbar_init(&tempty[i], kFzEpi * 32);
     }
@@ -569,8 +571,8 @@ __global__ void __launch_bounds__(kFzThreads, 1) fz_kernel(const FzParams p) {
       const uint32_t idesc = umma::idesc_i8(lp);
       const uint32_t sA_u = ptx::s2u(sA), sB_u = ptx::s2u(sB);
       for (int k = 0; k < n_items; ++k) {
-        const int s = k % NS, acc = k & 1;
-        ptx::mbar_wait(&tempty[acc], ((k >> 1) & 1) ^ 1);
+        const int s = k % NS, acc = k % NT;
+        ptx::mbar_wait(&tempty[acc], ((k / NT) & 1) ^ 1);
         ptx::mbar_wait(&afull[s], (k / NS) & 1);
         umma::fence_after();
         const uint32_t a0 = sA_u + (uint32_t)s * a_bytes;
@@ -618,8 +620,8 @@ __global__ void __launch_bounds__(kFzThreads, 1) fz_kernel(const FzParams p) {
     for (int ti = 0; ti < my_tiles; ++ti) {
       const int64_t row = (int64_t)(blockIdx.x + ti * grid) * 128 + r_in;
       for (int t = 0; t < nt; ++t, ++k) {
-        const int sacc = k & 1;
-        ptx::mbar_wait(&tfull[sacc], (k >> 1) & 1);
+        const int sacc = k % NT;
+        ptx::mbar_wait(&tfull[sacc], (k / NT) & 1);
         umma::fence_after();
         const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(sacc * lp);
         int leaf = -1;
@@ -958,6 +960,11 @@ static bool fz_plan(const GemmClassDev& c, int32_t F, int32_t K, FzParams* p) {
   if (KT > 16) KT = 64;
   const int a_bytes = 128 * c.i_pad;
   p->b_bytes = c.i_pad * c.l_pad;
+  // TMEM accumulator ring: as many L_pad-column stages as fit in 512 columns (<= 4)
+  p->tstages = std::max(2, std::min(4, 512 / c.l_pad));
+  int cols = 32;
+  while (cols < p->tstages * c.l_pad) cols *= 2;
+  p->tmem_cols = cols;
   int off = (p->b_bytes + 1023) / 1024 * 1024;
   p->x_off = off;
   off += (kFzXStride * (F + 1) * 4 + 1023) / 1024 * 1024;  // + constant-zero row F
@@ -975,7 +982,7 @@ static bool fz_plan(const GemmClassDev& c, int32_t F, int32_t K, FzParams* p) {
   p->red_off = off;
   off += 128 * KT * 8;
   p->bar_off = off;
-  off += (1 + 2 * stages + 4 + 2 * p->nstages) * 8 + 16;
+  off += (1 + 2 * stages + 2 * p->tstages + 2 * p->nstages) * 8 + 16;
   p->smem = off;
   return true;
 }
@@ -1020,9 +1027,6 @@ cudaError_t gemm_run_fused(const bridger_model* m, const float* X, int64_t n_row
     p.n_tiles = (int32_t)n_tiles64;
     p.gbase = gbase;
     p.cls = c;
-    int cols = 32;
-    while (cols < 2 * c.l_pad) cols *= 2;
-    p.tmem_cols = cols;
     p.first = ci == 0;
     p.last = ci == nc - 1;
     p.accbuf = accbuf;

@@ -37,7 +37,8 @@ class _Model(C.Structure):
                 ("tree_offsets", C.c_void_p), ("feature", C.c_void_p), ("threshold", C.c_void_p),
                 ("left", C.c_void_p), ("right", C.c_void_p), ("value", C.c_void_p),
                 ("missing_left", C.c_void_p), ("task", C.c_int32), ("agg", C.c_int32),
-                ("post", C.c_int32), ("base_score", C.c_void_p), ("leaf_scale", C.c_double)]
+                ("post", C.c_int32), ("base_score", C.c_void_p), ("leaf_scale", C.c_double),
+                ("tree_output", C.c_void_p)]
 
 
 _lib = None
@@ -80,10 +81,11 @@ def run(m, X: np.ndarray, n_threads: int | None = None, want=("leaf", "acc", "s"
                 l=np.ascontiguousarray(m.left, np.int32), r=np.ascontiguousarray(m.right, np.int32),
                 v=np.ascontiguousarray(m.value, np.float32),
                 ml=None if m.missing_left is None else np.ascontiguousarray(m.missing_left, np.uint8),
-                base=None if m.base_score is None else np.ascontiguousarray(m.base_score, np.float64))
+                base=None if m.base_score is None else np.ascontiguousarray(m.base_score, np.float64),
+                tout=None if getattr(m, "tree_output", None) is None else np.ascontiguousarray(m.tree_output, np.int32))
     mm = _Model(T, int(m.n_features), K, _ptr(keep["offs"]), _ptr(keep["feat"]), _ptr(keep["thr"]),
                 _ptr(keep["l"]), _ptr(keep["r"]), _ptr(keep["v"]), _ptr(keep["ml"]), int(m.task),
-                int(m.agg), int(m.post), _ptr(keep["base"]), float(m.leaf_scale))
+                int(m.agg), int(m.post), _ptr(keep["base"]), float(m.leaf_scale), _ptr(keep["tout"]))
     classif = int(m.task) == 1
     Cp = (2 if K == 1 else K)
     out = dict(

@@ -27,6 +27,13 @@
  *     classif. K >= 2:   label = smallest k maximising s[k]; proba = (float) s
  *     classif. K == 1:   p = 1/(1+exp(-s0)); label = (s0 > 0) (reading c7);
  *                        proba = [(float)(1-p), (float)p]
+ *     post == SOFTMAX:   proba[k] = (float)(exp(s[k] - max s) / sum_j exp(s[j] - max s))
+ *                        (exp / divide, Table 4; reading c15)
+ *
+ * Multiclass boosting (reading c15, sklearn _gradient_boosting.pyx
+ * predict_stages: out[i, k] += scale * tree[stage, k](x)): when tree_output is
+ * given, every tree has ONE scalar value per node (value[n_nodes]) and adds it
+ * to output tree_output[t] only:  acc[tree_output[t]] += (double) value_t[n].
  *
  * Built with -O2 -ffp-contract=off and no fast-math: no FMA contraction of
  * base + scale*acc, IEEE compares (reading c3).
@@ -51,6 +58,7 @@ typedef struct {
   int32_t post;                  /* 0 identity, 1 sigmoid */
   const double* base_score;      /* [n_outputs] or NULL */
   double leaf_scale;
+  const int32_t* tree_output;    /* [n_trees] or NULL (then value is [n_nodes * n_outputs]) */
 } oracle_model;
 
 typedef struct {
@@ -83,7 +91,8 @@ static void* run_rows(void* arg) {
         if (n < 0 || n >= size || ++steps > size) { j->err = 1; return NULL; }
       }
       if (j->leaf) j->leaf[r * T + t] = (int32_t)n;
-      for (int k = 0; k < K; ++k) a[k] += (double)m->value[(base + n) * K + k];
+      if (m->tree_output) a[m->tree_output[t]] += (double)m->value[base + n];
+      else for (int k = 0; k < K; ++k) a[k] += (double)m->value[(base + n) * K + k];
     }
     if (j->acc) for (int k = 0; k < K; ++k) j->acc[r * K + k] = a[k];
     double s[64];
@@ -110,7 +119,14 @@ static void* run_rows(void* arg) {
         for (int k = 1; k < K; ++k) if (s[k] > s[best]) best = k;
         j->label[r] = best;
       }
-      if (j->proba) for (int k = 0; k < K; ++k) j->proba[r * K + k] = (float)s[k];
+      if (j->proba && m->post == 2) {
+        double mx = s[0], e[64], z = 0.0;
+        for (int k = 1; k < K; ++k) if (s[k] > mx) mx = s[k];
+        for (int k = 0; k < K; ++k) { e[k] = exp(s[k] - mx); z += e[k]; }
+        for (int k = 0; k < K; ++k) j->proba[r * K + k] = (float)(e[k] / z);
+      } else if (j->proba) {
+        for (int k = 0; k < K; ++k) j->proba[r * K + k] = (float)s[k];
+      }
     }
   }
   return NULL;
@@ -124,6 +140,9 @@ int oracle_run(const oracle_model* m, const float* X, int64_t n_rows, int32_t n_
   if (!m || (!X && n_rows > 0) || n_features != m->n_features || m->n_outputs < 1 ||
       m->n_outputs > 64 || m->n_trees < 1)
     return 2;
+  if (m->tree_output)
+    for (int32_t t = 0; t < m->n_trees; ++t)
+      if (m->tree_output[t] < 0 || m->tree_output[t] >= m->n_outputs) return 2;
   if (n_threads < 1) n_threads = 1;
   if (n_threads > n_rows) n_threads = n_rows > 0 ? (int)n_rows : 1;
   job_t* jobs = (job_t*)calloc((size_t)n_threads, sizeof(job_t));

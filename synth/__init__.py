@@ -16,7 +16,7 @@ Both ``oracle/`` and ``paper_2405_12491_b200`` receive the same arrays; neither
 imports the other.
 """
 from .xgen import gen_x, gen_x_torch, splitmix64_np, inject_specials, iris_like_x
-from .trees import ModelDesc, perfect_ensemble, prune_ensemble, stump_model
+from .trees import ModelDesc, multiclass_gbdt, perfect_ensemble, prune_ensemble, stump_model
 from .configs import CONFIGS, make_config
 
 __all__ = [

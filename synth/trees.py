@@ -7,6 +7,8 @@ A ``ModelDesc`` holds, for T trees concatenated:
   left, right  int32[n]     tree-local child ids, both -1 at leaves, root = 0
   value        float32[n*K] read at leaves only
   missing_left uint8[n] | None   NaN routing per node (None => NaN goes right)
+  tree_output  int32[T] | None   multiclass boosting: tree t adds its SCALAR leaf
+                                 values (value float32[n]) to output tree_output[t]
 plus task / agg / post / base_score / leaf_scale.
 
 Thresholds are *calibrated* like a trainer would place them:
@@ -26,7 +28,7 @@ from .xgen import gen_x, splitmix64_np, _seed_key
 
 TASK_REGRESSION, TASK_CLASSIFICATION = 0, 1
 AGG_MEAN, AGG_SUM = 0, 1
-POST_IDENTITY, POST_SIGMOID = 0, 1
+POST_IDENTITY, POST_SIGMOID, POST_SOFTMAX = 0, 1, 2
 
 
 @dataclass
@@ -46,6 +48,12 @@ class ModelDesc:
     base_score: Optional[np.ndarray] = None
     leaf_scale: float = 1.0
     meta: dict = field(default_factory=dict)
+    tree_output: Optional[np.ndarray] = None
+
+    @property
+    def value_width(self) -> int:
+        """Values stored per node: 1 with tree_output (scalar leaves), else K."""
+        return 1 if self.tree_output is not None else self.n_outputs
 
     @property
     def n_trees(self) -> int:
@@ -57,7 +65,7 @@ class ModelDesc:
 
     def tree(self, t: int):
         a, b = int(self.tree_offsets[t]), int(self.tree_offsets[t + 1])
-        K = self.n_outputs
+        K = self.value_width
         return dict(feature=self.feature[a:b], threshold=self.threshold[a:b],
                     left=self.left[a:b], right=self.right[a:b],
                     value=self.value[a * K:b * K].reshape(b - a, K),
@@ -66,7 +74,6 @@ class ModelDesc:
     def subset(self, trees) -> "ModelDesc":
         """Model made of the listed trees (in that order); used for tree sharding."""
         trees = list(trees)
-        K = self.n_outputs
         parts = [self.tree(t) for t in trees]
         sizes = [len(p["feature"]) for p in parts]
         offs = np.zeros(len(trees) + 1, dtype=np.int64)
@@ -78,6 +85,7 @@ class ModelDesc:
             left=cat("left").astype(np.int32), right=cat("right").astype(np.int32),
             value=np.concatenate([p["value"].reshape(-1) for p in parts]).astype(np.float32),
             missing_left=None if self.missing_left is None else cat("missing_left").astype(np.uint8),
+            tree_output=None if self.tree_output is None else np.asarray(self.tree_output, np.int32)[trees],
             meta=dict(self.meta))
 
 
@@ -226,7 +234,7 @@ def prune_ensemble(m: ModelDesc, seed: int, p: float = 0.1, with_missing: bool =
     probability p (its subtree dropped); nodes are renumbered in DFS preorder
     (sklearn's order), so the result is non-perfect and not in heap order.
     with_missing=True adds a random per-node ``missing_left`` array."""
-    K = m.n_outputs
+    K = m.value_width
     out_f, out_t, out_l, out_r, out_v, out_m, offs = [], [], [], [], [], [], [0]
     for t in range(m.n_trees):
         tr = m.tree(t)
@@ -278,3 +286,18 @@ def stump_model(feature: int, threshold: float, n_features: int, left_value: flo
                      left=np.array([1, -1, -1], np.int32), right=np.array([2, -1, -1], np.int32),
                      value=np.array([0.0, left_value, right_value], np.float32),
                      task=TASK_REGRESSION, agg=AGG_MEAN, post=POST_IDENTITY)
+
+
+def multiclass_gbdt(seed: int, n_rounds: int, depth: int, n_features: int, n_classes: int, *,
+                    lr: float = 0.1, calib_rows: int = 2048) -> ModelDesc:
+    """Multiclass gradient boosting (reading c15): n_rounds x K perfect
+    regression trees, tree t = round t // K for class t % K, scalar leaves
+    lr*z, SUM aggregation, base_score = per-class log-prior-like constants,
+    softmax probabilities."""
+    K = int(n_classes)
+    m = perfect_ensemble(seed, n_rounds * K, depth, n_features, kind="regression", lr=lr,
+                         calib_rows=calib_rows)
+    base = np.log(np.arange(1, K + 1, dtype=np.float64) / (K * (K + 1) / 2))
+    return replace(m, n_outputs=K, task=TASK_CLASSIFICATION, agg=AGG_SUM, post=POST_SOFTMAX,
+                   base_score=base, tree_output=(np.arange(n_rounds * K) % K).astype(np.int32),
+                   meta=dict(m.meta, kind="multiclass_gbdt"))

@@ -43,7 +43,8 @@ def model_from_json(d) -> ModelDesc:
         task=int(d.get("task", 0)), agg=int(d.get("agg", 0)), post=int(d.get("post", 0)),
         missing_left=None if d.get("missing_left") is None else np.asarray(d["missing_left"], np.uint8),
         base_score=None if d.get("base_score") is None else np.asarray(d["base_score"], np.float64),
-        leaf_scale=float(d.get("leaf_scale", 1.0)))
+        leaf_scale=float(d.get("leaf_scale", 1.0)),
+        tree_output=None if d.get("tree_output") is None else np.asarray(d["tree_output"], np.int32))
 
 
 def model_from_trees(trees, n_features, n_outputs, with_missing, **kw) -> ModelDesc:

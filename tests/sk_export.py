@@ -41,3 +41,16 @@ def from_sklearn_gbr(est, n_features, X_for_init):
     init = float(np.asarray(est._raw_predict_init(X_for_init[:1].astype(np.float64))).reshape(-1)[0])
     return _trees_to_desc(trees, n_features, 1, lambda tr: tr.value[:, 0, 0], False,
                           task=0, agg=1, base_score=np.array([init]), leaf_scale=float(est.learning_rate))
+
+
+def from_sklearn_gbc_multiclass(est, n_features, X_for_init):
+    """GradientBoostingClassifier with K >= 3 classes: estimators_[stage, k] is the
+    class-k regression tree of a round; raw = init + lr * sum (predict_stages),
+    proba = softmax(raw) (reading c15).  Trees are laid out round-major, so tree
+    t = stage t // K adds to output t % K."""
+    S, K = est.estimators_.shape
+    trees = [est.estimators_[s, k].tree_ for s in range(S) for k in range(K)]
+    init = np.asarray(est._raw_predict_init(X_for_init[:1].astype(np.float64)), np.float64).reshape(-1)
+    return _trees_to_desc(trees, n_features, K, lambda tr: tr.value[:, 0, 0], False,
+                          task=1, agg=1, post=2, base_score=init, leaf_scale=float(est.learning_rate),
+                          tree_output=(np.arange(S * K) % K).astype(np.int32))

@@ -62,3 +62,14 @@ def test_gbdt_two_stumps_hand():
     assert o["label"].tolist() == g["expected"]["label"]
     np.testing.assert_allclose(o["proba"][:, 1], g["expected"]["p1"], rtol=1e-7)
     np.testing.assert_allclose(o["proba"][:, 0], 1 - np.asarray(g["expected"]["p1"]), rtol=1e-6)
+
+
+def test_gbdt_multiclass_softmax_hand():
+    g = load_golden("gbdt_multiclass_softmax_hand.json")
+    X = parse_x(g["X"])
+    o = oracle.run(model_from_json(g["model"]), X)
+    np.testing.assert_array_equal(o["acc"], np.asarray(g["expected"]["acc"]))
+    np.testing.assert_array_equal(o["s"], np.asarray(g["expected"]["s"]))
+    assert o["label"].tolist() == g["expected"]["label"]
+    np.testing.assert_allclose(o["proba"], np.asarray(g["expected"]["proba"]), rtol=1e-6)
+    np.testing.assert_allclose(o["proba"].sum(axis=1), 1.0, rtol=1e-6)

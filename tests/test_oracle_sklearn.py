@@ -8,10 +8,10 @@ import pytest
 
 import oracle
 from synth import gen_x, inject_specials
-from tests.sk_export import from_sklearn_forest, from_sklearn_gbr
+from tests.sk_export import from_sklearn_forest, from_sklearn_gbc_multiclass, from_sklearn_gbr
 
 sk = pytest.importorskip("sklearn")
-from sklearn.ensemble import GradientBoostingRegressor, RandomForestClassifier  # noqa: E402
+from sklearn.ensemble import GradientBoostingClassifier, GradientBoostingRegressor, RandomForestClassifier  # noqa: E402
 from sklearn.tree import DecisionTreeClassifier  # noqa: E402
 
 
@@ -69,3 +69,19 @@ def test_gradient_boosting_regressor():
     leaves = est.apply(Xt).reshape(len(Xt), -1)
     np.testing.assert_array_equal(o["leaf"], leaves)
     np.testing.assert_allclose(o["pred"][:, 0], est.predict(Xt), rtol=1e-5, atol=1e-6)
+
+
+def test_gradient_boosting_classifier_multiclass_softmax():
+    # multiclass boosting (reading c15): K trees per round, softmax probabilities
+    X, y, _ = _data(51, 3000, 6, 4)
+    est = GradientBoostingClassifier(n_estimators=20, max_depth=3, learning_rate=0.2,
+                                     random_state=0).fit(X, y)
+    m = from_sklearn_gbc_multiclass(est, 6, X)
+    Xt, _, _ = _data(52, 2000, 6, 4)
+    o = oracle.run(m, Xt)
+    leaves = est.apply(Xt)  # [n, stages, K]
+    np.testing.assert_array_equal(o["leaf"], leaves.reshape(len(Xt), -1))
+    np.testing.assert_allclose(o["s"], est.decision_function(Xt), rtol=1e-5, atol=1e-6)
+    p = est.predict_proba(Xt)
+    np.testing.assert_allclose(o["proba"], p, rtol=1e-5, atol=1e-6)
+    _check_labels(p, o["label"])

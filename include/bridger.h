@@ -57,7 +57,9 @@ typedef enum { BRIDGER_TASK_REGRESSION = 0, BRIDGER_TASK_CLASSIFICATION = 1 } br
 /* MEAN: s = sum_t v_t / T (decision tree, random forest).
  * SUM : s = base_score + leaf_scale * sum_t v_t (gradient boosting).   Reading c6. */
 typedef enum { BRIDGER_AGG_MEAN = 0, BRIDGER_AGG_SUM = 1 } bridger_agg;
-typedef enum { BRIDGER_POST_IDENTITY = 0, BRIDGER_POST_SIGMOID = 1 } bridger_post;
+/* SOFTMAX (multiclass boosting, reading c15): proba_k = exp(s_k - max s) / sum_j exp(s_j - max s),
+ * fp64, labels from s (pre-transform, exact). */
+typedef enum { BRIDGER_POST_IDENTITY = 0, BRIDGER_POST_SIGMOID = 1, BRIDGER_POST_SOFTMAX = 2 } bridger_post;
 
 /* Which lowering of steps a1..a4 runs. */
 typedef enum {
@@ -85,7 +87,8 @@ typedef struct {
   const float* threshold;      /* [n_nodes] go LEFT iff x <= threshold (reading c1); not NaN */
   const int32_t* left;         /* [n_nodes] tree-local left child, -1 at leaves */
   const int32_t* right;        /* [n_nodes] tree-local right child, -1 at leaves */
-  const float* value;          /* [n_nodes * K] read at leaves only; must be finite there */
+  const float* value;          /* [n_nodes * K] read at leaves only; must be finite there
+                                  ([n_nodes] scalars when tree_output is given) */
   const uint8_t* missing_left; /* optional [n_nodes]: NaN goes left iff != 0; NULL => NaN right (c2) */
   int32_t task;                /* bridger_task */
   int32_t agg;                 /* bridger_agg */
@@ -99,6 +102,12 @@ typedef struct {
   int32_t force_fixed_point;
   int32_t forced_scale_exp;    /* q */
   int32_t forced_tier;         /* bridger_exact_tier */
+  /* Optional [T] (multiclass boosting, reading c15; sklearn
+   * GradientBoostingClassifier / XGBoost / LightGBM multiclass): tree t has ONE
+   * scalar value per node and adds it to output tree_output[t] in [0, K).
+   * NULL => every leaf carries a K-vector.  Lowered at load to K-vectors that are
+   * zero outside tree_output[t] (identical sums: adding +0 is exact). */
+  const int32_t* tree_output;
 } bridger_model_desc;
 
 /* Exactness tiers (reading c9).  q = min over non-zero leaf values of the

@@ -40,7 +40,8 @@ class _Desc(C.Structure):
                 ("left", C.c_void_p), ("right", C.c_void_p), ("value", C.c_void_p),
                 ("missing_left", C.c_void_p), ("task", C.c_int32), ("agg", C.c_int32), ("post", C.c_int32),
                 ("base_score", C.c_void_p), ("leaf_scale", C.c_double),
-                ("force_fixed_point", C.c_int32), ("forced_scale_exp", C.c_int32), ("forced_tier", C.c_int32)]
+                ("force_fixed_point", C.c_int32), ("forced_scale_exp", C.c_int32), ("forced_tier", C.c_int32),
+                ("tree_output", C.c_void_p)]
 
 
 EXPORTS = [
@@ -135,13 +136,14 @@ class _DescKeep:
             v=np.ascontiguousarray(m.value, np.float32),
             ml=None if getattr(m, "missing_left", None) is None else np.ascontiguousarray(m.missing_left, np.uint8),
             base=None if getattr(m, "base_score", None) is None else np.ascontiguousarray(m.base_score, np.float64),
+            tout=None if getattr(m, "tree_output", None) is None else np.ascontiguousarray(m.tree_output, np.int32),
         )
         a = self.arrs
         p = lambda x: None if x is None else x.ctypes.data
         self.desc = _Desc(len(a["offs"]) - 1, int(m.n_features), int(m.n_outputs), p(a["offs"]), p(a["feat"]),
                           p(a["thr"]), p(a["l"]), p(a["r"]), p(a["v"]), p(a["ml"]), int(getattr(m, "task", 0)),
                           int(getattr(m, "agg", 0)), int(getattr(m, "post", 0)), p(a["base"]),
-                          float(getattr(m, "leaf_scale", 1.0)), 0, 0, 0)
+                          float(getattr(m, "leaf_scale", 1.0)), 0, 0, 0, p(a["tout"]))
         if force is not None:
             self.desc.force_fixed_point = 1
             self.desc.forced_scale_exp = int(force[0])
@@ -224,11 +226,13 @@ class Model:
 
     @classmethod
     def from_arrays(cls, *, n_features, n_outputs, tree_offsets, feature, threshold, left, right, value,
-                    missing_left=None, task=0, agg=0, post=0, base_score=None, leaf_scale=1.0, device=0):
+                    missing_left=None, task=0, agg=0, post=0, base_score=None, leaf_scale=1.0, tree_output=None,
+                    device=0):
         from types import SimpleNamespace
         d = SimpleNamespace(n_features=n_features, n_outputs=n_outputs, tree_offsets=tree_offsets, feature=feature,
                             threshold=threshold, left=left, right=right, value=value, missing_left=missing_left,
-                            task=task, agg=agg, post=post, base_score=base_score, leaf_scale=leaf_scale)
+                            task=task, agg=agg, post=post, base_score=base_score, leaf_scale=leaf_scale,
+                            tree_output=tree_output)
         return cls(d, device=device)
 
     def close(self):

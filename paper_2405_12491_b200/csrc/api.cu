@@ -228,7 +228,8 @@ bridger_status bridger_analyze_exactness(const bridger_model_desc* d, int32_t* s
                                          double* log2_M) {
   bridger_status s = validate_desc(d);
   if (s != BRIDGER_OK) return s;
-  Exactness ex = analyze_exactness(d);
+  const ExpandedDesc ed(d);
+  Exactness ex = analyze_exactness(ed.get());
   if (scale_exp) *scale_exp = ex.q;
   if (tier) *tier = ex.tier;
   if (log2_M) *log2_M = ex.log2_M;
@@ -253,6 +254,8 @@ bridger_status bridger_lower_tree(const bridger_model_desc* d, int32_t tree, int
                                   float* threshold, uint8_t* missing_left, int32_t* leaf_id, float* leaf_value) {
   bridger_status s = validate_desc(d);
   if (s != BRIDGER_OK) return s;
+  const ExpandedDesc ed(d);
+  d = ed.get();
   if (tree < 0 || tree >= d->n_trees) return fail(BRIDGER_E_SHAPE, "tree index out of range");
   if (!depth) return fail(BRIDGER_E_NULL_ARG, "depth is NULL");
   const int32_t D = tree_depth(d, tree);
@@ -270,10 +273,12 @@ bridger_status bridger_lower_tree(const bridger_model_desc* d, int32_t tree, int
   return BRIDGER_OK;
 }
 
-bridger_status bridger_model_load(const bridger_model_desc* d, int cuda_device, bridger_model** out) {
+bridger_status bridger_model_load(const bridger_model_desc* d_in, int cuda_device, bridger_model** out) {
   if (!out) return fail(BRIDGER_E_NULL_ARG, "out is NULL");
-  bridger_status s = validate_desc(d);
+  bridger_status s = validate_desc(d_in);
   if (s != BRIDGER_OK) return s;
+  const ExpandedDesc ed(d_in);  // per-tree scalar outputs -> K-vector leaves (reading c15)
+  const bridger_model_desc* d = ed.get();
   const int32_t T = d->n_trees;
   std::vector<int32_t> depth(T);
   int32_t Dmax = 0;

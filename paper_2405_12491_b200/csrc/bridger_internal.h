@@ -35,6 +35,16 @@ struct PaddedTree {
 };
 
 bridger_status validate_desc(const bridger_model_desc* d);
+
+// A validated desc with per-tree scalar outputs (tree_output, reading c15)
+// rewritten to K-vector leaves that are zero outside the tree's output: every
+// later stage sees one layout.  Sums are unchanged (x + 0.0 == x exactly).
+struct ExpandedDesc {
+  explicit ExpandedDesc(const bridger_model_desc* d);
+  const bridger_model_desc* get() const { return &desc; }
+  bridger_model_desc desc;
+  std::vector<float> value;
+};
 int32_t tree_depth(const bridger_model_desc* d, int32_t t);  // desc must be valid
 void pad_tree(const bridger_model_desc* d, int32_t t, int32_t D, PaddedTree* out);
 

@@ -5,7 +5,8 @@
 //   s   = MEAN ? a / T : base + leaf_scale * a     (fp64, explicit _rn: no FMA)
 //   regression      -> (float) s
 //   classification  -> label = argmax s (lowest index wins ties); K == 1: s > 0
-//   proba           -> (float) s, or sigmoid for K == 1: [(float)(1-p), (float)p]
+//   proba           -> (float) s, or sigmoid for K == 1: [(float)(1-p), (float)p],
+//                      or softmax (POST_SOFTMAX, reading c15)
 #pragma once
 #include <cstdint>
 
@@ -73,7 +74,22 @@ __device__ __forceinline__ void finalize_row(const FinalizeArgs& f, int64_t row,
     static_cast<int32_t*>(f.out)[row] = label;
     return;
   }
-  if (K == 1) {
+  if (f.post == BRIDGER_POST_SOFTMAX) {  // reading c15: fp64, max-shifted
+    double mx = s[0];
+#pragma unroll
+    for (int k = 1; k < KT; ++k)
+      if (k < K && s[k] > mx) mx = s[k];
+    double e[KT], z = 0.0;
+#pragma unroll
+    for (int k = 0; k < KT; ++k) {
+      e[k] = k < K ? exp(s[k] - mx) : 0.0;
+      z += e[k];
+    }
+    float* o = static_cast<float*>(f.out) + row * K;
+#pragma unroll
+    for (int k = 0; k < KT; ++k)
+      if (k < K) o[k] = __double2float_rn(e[k] / z);
+  } else if (K == 1) {
     const double p = 1.0 / (1.0 + exp(-s[0]));
     float* o = static_cast<float*>(f.out) + row * 2;
     o[0] = __double2float_rn(1.0 - p);

@@ -18,6 +18,18 @@ namespace bridger {
 
 static inline bool finite_f(float v) { return std::isfinite(v); }
 
+ExpandedDesc::ExpandedDesc(const bridger_model_desc* d) : desc(*d) {
+  if (!d->tree_output) return;
+  const int32_t K = d->n_outputs;
+  const int64_t n = d->tree_offsets[d->n_trees];
+  value.assign((size_t)n * K, 0.0f);
+  for (int32_t t = 0; t < d->n_trees; ++t)
+    for (int64_t g = d->tree_offsets[t]; g < d->tree_offsets[t + 1]; ++g)
+      value[(size_t)g * K + d->tree_output[t]] = d->value[g];
+  desc.value = value.data();
+  desc.tree_output = nullptr;
+}
+
 bridger_status validate_desc(const bridger_model_desc* d) {
   if (!d) return fail(BRIDGER_E_NULL_ARG, "desc is NULL");
   if (!d->tree_offsets || !d->feature || !d->threshold || !d->left || !d->right || !d->value)
@@ -28,13 +40,19 @@ bridger_status validate_desc(const bridger_model_desc* d) {
   if (d->task != BRIDGER_TASK_REGRESSION && d->task != BRIDGER_TASK_CLASSIFICATION)
     return fail(BRIDGER_E_UNSUPPORTED, "unknown task");
   if (d->agg != BRIDGER_AGG_MEAN && d->agg != BRIDGER_AGG_SUM) return fail(BRIDGER_E_UNSUPPORTED, "unknown agg");
-  if (d->post != BRIDGER_POST_IDENTITY && d->post != BRIDGER_POST_SIGMOID)
+  if (d->post != BRIDGER_POST_IDENTITY && d->post != BRIDGER_POST_SIGMOID && d->post != BRIDGER_POST_SOFTMAX)
     return fail(BRIDGER_E_UNSUPPORTED, "unknown post");
+  if (d->post == BRIDGER_POST_SOFTMAX && (d->task != BRIDGER_TASK_CLASSIFICATION || d->n_outputs < 2))
+    return fail(BRIDGER_E_UNSUPPORTED, "softmax post-transform needs a K >= 2 classifier");
+  if (d->tree_output)
+    for (int32_t t = 0; t < d->n_trees; ++t)
+      if (d->tree_output[t] < 0 || d->tree_output[t] >= d->n_outputs)
+        return fail(BRIDGER_E_SHAPE, "tree_output[" + std::to_string(t) + "] out of [0,K)");
   if (d->post == BRIDGER_POST_SIGMOID && (d->task != BRIDGER_TASK_CLASSIFICATION || d->n_outputs != 1))
     return fail(BRIDGER_E_UNSUPPORTED, "sigmoid post-transform needs a K == 1 classifier");
   if (!std::isfinite(d->leaf_scale)) return fail(BRIDGER_E_SHAPE, "leaf_scale not finite");
   if (d->tree_offsets[0] != 0) return fail(BRIDGER_E_INVALID_TREE, "tree_offsets[0] != 0");
-  const int32_t F = d->n_features, K = d->n_outputs;
+  const int32_t F = d->n_features, K = d->tree_output ? 1 : d->n_outputs;  // values stored per node
   std::vector<int32_t> parents;
   std::vector<uint8_t> seen;
   std::vector<int32_t> stack;

@@ -17,7 +17,7 @@ import pytest
 
 import oracle
 import paper_2405_12491_b200 as B
-from synth import gen_x, inject_specials, make_config, perfect_ensemble, prune_ensemble
+from synth import multiclass_gbdt, gen_x, inject_specials, make_config, perfect_ensemble, prune_ensemble
 from synth.trees import ModelDesc
 
 HDR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "bridger.h")
@@ -132,6 +132,29 @@ def test_validation_rejects_malformed_trees():
     assert _bad(m, tree_offsets=o) == B.E_INVALID_TREE       # offsets not increasing
     assert _bad(m, n_outputs=0) == B.E_SHAPE
     assert _bad(m, post=1) == B.E_UNSUPPORTED                # sigmoid on K=3
+    mr = make_config("C3", n_trees=4)[1]
+    assert _bad(mr, post=2) == B.E_UNSUPPORTED               # softmax on a regressor
+    mc = multiclass_gbdt(7, 2, 3, 5, 3)
+    B.validate(mc)
+    assert _bad(mc, n_outputs=1, post=0) == B.E_SHAPE        # tree_output >= K
+    to = mc.tree_output.copy(); to[0] = -1
+    assert _bad(mc, tree_output=to) == B.E_SHAPE
+    vv = mc.value.copy(); vv[np.flatnonzero(mc.left == -1)[0]] = np.nan
+    assert _bad(mc, value=vv) == B.E_INVALID_TREE            # scalar leaves checked at width 1
+
+
+def test_multiclass_lowering_expands_scalar_leaves():
+    # reading c15: a tree with tree_output k lowers to K-vector leaves that are
+    # zero outside column k, carrying its scalar leaf values in column k
+    mc = multiclass_gbdt(8, 3, 4, 6, 4)
+    for t in range(mc.n_trees):
+        p = B.lower_tree(mc, t)
+        k = int(mc.tree_output[t])
+        lv = p["leaf_value"]
+        assert lv.shape == (16, 4)
+        np.testing.assert_array_equal(np.delete(lv, k, axis=1), 0.0)
+        a = int(mc.tree_offsets[t])
+        np.testing.assert_array_equal(lv[:, k], mc.value[a + p["leaf_id"]])
 
 
 def _lsb_exp(v):

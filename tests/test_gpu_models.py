@@ -133,3 +133,25 @@ def test_sparse_layout_forced_matches_heap(monkeypatch):
     assert g.layout()["format"] == "sparse"
     np.testing.assert_array_equal(g.predict(dev(X)).cpu().numpy(), a)
     check(m, X)
+
+
+@pytest.mark.parametrize("variant", ["traverse", "gemm", "gemm_staged"])
+def test_multiclass_gbdt_softmax(variant):
+    # reading c15: K scalar-leaf trees per round, SUM aggregation, softmax proba
+    from synth import multiclass_gbdt
+    m = multiclass_gbdt(81, 30, 6, 14, 5)
+    X = inject_specials(gen_x(82, 0, 6001, 14), 82, rate=0.01)
+    g, o = check(m, X, variant=variant, apply=variant == "traverse")
+    assert g.info()["exact_tier"] == "E53"
+
+
+def test_sklearn_gradient_boosting_classifier_multiclass():
+    from sklearn.ensemble import GradientBoostingClassifier
+    from tests.sk_export import from_sklearn_gbc_multiclass
+    X, y, _ = _data(37, 5000, 8, 4)
+    est = GradientBoostingClassifier(n_estimators=40, max_depth=4, learning_rate=0.2, random_state=0).fit(X, y)
+    m = from_sklearn_gbc_multiclass(est, 8, X)
+    Xt, _, _ = _data(38, 3000, 8, 4)
+    g, _ = check(m, Xt, exact=False)
+    np.testing.assert_array_equal(g.apply(dev(Xt)).cpu().numpy(), est.apply(Xt).reshape(len(Xt), -1))
+    np.testing.assert_allclose(g.predict_proba(dev(Xt)).cpu().numpy(), est.predict_proba(Xt), rtol=1e-5, atol=1e-6)

@@ -155,3 +155,16 @@ def test_sklearn_gradient_boosting_classifier_multiclass():
     g, _ = check(m, Xt, exact=False)
     np.testing.assert_array_equal(g.apply(dev(Xt)).cpu().numpy(), est.apply(Xt).reshape(len(Xt), -1))
     np.testing.assert_allclose(g.predict_proba(dev(Xt)).cpu().numpy(), est.predict_proba(Xt), rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("name", ["xgboost_binary_logistic.json", "xgboost_multiclass_softprob.json",
+                                  "lightgbm_binary_dump.json"])
+def test_imported_formats_on_gpu(name):
+    from paper_2405_12491_b200 import importers as I
+    from tests.helpers import load_golden, parse_x
+    g = load_golden(name)
+    m = I.from_lightgbm_json(g["model"]) if name.startswith("lightgbm") else I.from_xgboost_json(g["model"])
+    X = parse_x(g["X"])
+    # the hand rows, then a larger seeded batch with specials through the same model
+    Xb = np.concatenate([X, inject_specials(gen_x(93, 0, 3000, m.n_features), 93, rate=0.05)])
+    check(m, Xb, exact=False)

@@ -77,6 +77,7 @@ struct TravChunk {
   int64_t g_nodes;     // hybrid: first deep-level record of the chunk (global)
   int64_t g_leaves;    // hybrid: first leaf value of the chunk (global)
 };
+static_assert(sizeof(TravChunk) <= 64, "tree-streamed ring slots carry a chunk descriptor in a 64-byte header");
 
 // Sparse (pointer) tree descriptor (§8(f3)): unbounded / unbalanced trees.
 struct SparseTree {
@@ -97,6 +98,10 @@ struct TravLayout {
   bool pretransposed = false;   // fp32 input transposed once into feature-major blocks (wide X, many chunks)
   bool hybrid = false;          // top levels in shared memory, deep levels + leaves in global memory
   bool split = false;           // split nodes: fp32 threshold array + 1-byte feature array (F <= 127)
+  bool stream = false;          // tree-streamed: row tiles resident, chunk node records streamed (K4s)
+  int32_t stream_ns = 0;        //   node-record ring depth
+  int32_t stream_stage = 0;     //   bytes per ring slot (>= every chunk's node bytes)
+  int32_t stream_warps = 0;     //   walking warps (rows per tile / 32)
   std::vector<uint32_t> hyb_nodes;  // [records][2] deep levels of every tree (slot order)
   std::vector<float> hyb_leaves;    // [slots][L][K]
   std::vector<SparseTree> sparse_trees;

@@ -558,6 +558,34 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
   out->n_warps = nw;
   out->group = G;
   out->chunk_budget = budget;
+  out->stream = false;
+  if (out->global_trees && !out->sparse) {
+    // Tree-streamed mode (traverse.cuh K4s): rows resident, node records of
+    // chunks of <= 4 equal-depth trees streamed through a 3-slot ring; leaves
+    // stay in global memory.  Default on (BRIDGER_STREAM=0 keeps the older
+    // global-tree walker for comparison).
+    const char* env = std::getenv("BRIDGER_STREAM");
+    const bool want_stream = !(env && env[0] == '0');
+    const int64_t tree_nodes = (((int64_t)1 << Dmax) - 1) * 8;
+    const int32_t ns = 3;
+    // one slot = 64-byte chunk header + node records
+    const int64_t stage = std::max<int64_t>((tree_nodes + 15) / 16 * 16, 16384) + 64;
+    int32_t warps = 16;
+    while (warps > 4 && (int64_t)warps * 32 * F * 4 + ns * stage + 1024 > kSmemMax) warps /= 2;
+    if (want_stream && (int64_t)warps * 32 * F * 4 + ns * stage + 1024 <= kSmemMax && warps >= 4) {
+      out->stream = true;
+      out->stream_ns = ns;
+      out->stream_stage = (int32_t)stage;
+      out->stream_warps = warps;
+      std::vector<Run> pieces;
+      for (const Run& r : bal) {
+        const int64_t per = std::max<int64_t>(1, std::min<int64_t>(4, (stage - 64) / ((((int64_t)1 << r.D) - 1) * 8)));
+        for (int32_t s0 = 0; s0 < r.n; s0 += (int32_t)per)
+          pieces.push_back({r.start + s0, (int32_t)std::min<int64_t>(per, r.n - s0), r.D});
+      }
+      bal.swap(pieces);
+    }
+  }
   {
     // wide inputs walked by many chunks: transpose X once into feature-major
     // blocks instead of once per chunk CTA (measured: C5-shaped models)

@@ -43,6 +43,17 @@ BRIDGER_TRAV_EXTERN(long long, false, false, 5)
 BRIDGER_TRAV_EXTERN(long long, true, false, 5)
 BRIDGER_TRAV_EXTERN(double, false, false, 5)
 BRIDGER_TRAV_EXTERN(double, true, false, 5)
+#define BRIDGER_STREAM_EXTERN(ACC, ML)                                                                        \
+  extern template cudaError_t launch_stream_t<1, ACC, ML>(const TravParams&, int, int, int, cudaStream_t);  \
+  extern template cudaError_t launch_stream_t<2, ACC, ML>(const TravParams&, int, int, int, cudaStream_t);  \
+  extern template cudaError_t launch_stream_t<4, ACC, ML>(const TravParams&, int, int, int, cudaStream_t);  \
+  extern template cudaError_t launch_stream_t<8, ACC, ML>(const TravParams&, int, int, int, cudaStream_t);  \
+  extern template cudaError_t launch_stream_t<16, ACC, ML>(const TravParams&, int, int, int, cudaStream_t); \
+  extern template cudaError_t launch_stream_t<64, ACC, ML>(const TravParams&, int, int, int, cudaStream_t);
+BRIDGER_STREAM_EXTERN(long long, false)
+BRIDGER_STREAM_EXTERN(long long, true)
+BRIDGER_STREAM_EXTERN(double, false)
+BRIDGER_STREAM_EXTERN(double, true)
 BRIDGER_TRAV_EXTERN(long long, false, true, 2)
 BRIDGER_TRAV_EXTERN(long long, true, true, 2)
 BRIDGER_TRAV_EXTERN(double, false, true, 2)
@@ -194,6 +205,51 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
   fin.base = m->d_base;
   fin.out = out;
   p.fin = fin;
+  if (L.stream) {
+    // tree-streamed mode: X transposed once into feature-major 32-row blocks,
+    // then row tiles resident / chunk node records streamed (traverse.cuh K4s)
+    const int64_t nbk = (n_rows + 31) / 32;
+    void* xt = nullptr;
+    cudaError_t err = cudaMallocAsync(&xt, (size_t)nbk * 32 * m->F * 4, st);
+    if (err != cudaSuccess) return err;
+    int nwx = 16;
+    while (nwx > 1 && nwx * 32 * (m->F | 1) * 4 > 200 * 1024) --nwx;
+    const int xsmem = nwx * 32 * (m->F | 1) * 4;
+    static bool x_attr_s = false;
+    if (!x_attr_s) {
+      cudaFuncSetAttribute(xpose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+      x_attr_s = true;
+    }
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, xpose_kernel, nwx * 32, xsmem);
+    const int xgrid = (int)std::max<int64_t>(1, std::min<int64_t>((nbk + nwx - 1) / nwx, (int64_t)sms * std::max(1, occ)));
+    xpose_kernel<<<xgrid, nwx * 32, xsmem, st>>>(X, n_rows, m->F, static_cast<float*>(xt));
+    count_launch();
+    err = cudaGetLastError();
+    if (err == cudaSuccess) {
+      p.X = static_cast<const float*>(xt);
+      p.mode = want == 3 ? TRAV_APPLY : TRAV_FINAL;
+      p.out_leaf = static_cast<int32_t*>(out);
+      p.stream_ns = L.stream_ns;
+      p.stream_stage = L.stream_stage;
+      const int rb = L.stream_warps * 32;
+      p.stream_x_bytes = rb * m->F * 4;
+      const int smem_s = p.stream_x_bytes + L.stream_ns * L.stream_stage + (1 + 2 * L.stream_ns) * 8 + 16;
+      const int64_t n_tiles = (n_rows + rb - 1) / rb;
+      const int grid_s = (int)std::max<int64_t>(1, std::min<int64_t>(n_tiles, sms));
+      const int block_s = (L.stream_warps + 1) * 32;
+      BRIDGER_DISPATCH_KT(m->K, {
+        if (m->acc_int)
+          err = L.has_missing ? launch_stream_t<KT, long long, true>(p, grid_s, block_s, smem_s, st)
+                              : launch_stream_t<KT, long long, false>(p, grid_s, block_s, smem_s, st);
+        else
+          err = L.has_missing ? launch_stream_t<KT, double, true>(p, grid_s, block_s, smem_s, st)
+                              : launch_stream_t<KT, double, false>(p, grid_s, block_s, smem_s, st);
+      });
+    }
+    cudaFreeAsync(xt, st);
+    return err;
+  }
   const int NW = L.n_warps, G = L.group, NB = NW / G;
   const int block = NW * 32;
   p.group = G;

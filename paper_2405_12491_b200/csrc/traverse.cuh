@@ -72,6 +72,9 @@ struct TravParams {
   int32_t group;      // warps sharing one 32-row block (tree split)
   int32_t red_off;    // byte offset of the intra-group partials
   int32_t slot_off;   // byte offset of the DSMEM reduction slots (TRAV_CLUSTER)
+  int32_t stream_ns;      // tree-streamed mode: node-record ring depth
+  int32_t stream_stage;   //                     bytes per ring slot
+  int32_t stream_x_bytes; //                     X tile bytes (rows_per_tile * F * 4)
   FinalizeArgs fin;   // (TRAV_FINAL, TRAV_CLUSTER)
 };
 
@@ -700,6 +703,213 @@ cudaError_t launch_trav_t(const TravParams& p, int grid_ctas, int block, int sme
   return cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------------------
+// Tree-streamed traversal (K4s) for ensembles too large for shared-memory
+// residency (C4: depth-12 trees of 32 KB nodes + 128 KB 8-class leaves, 164 MB
+// in total).  The loop order is the transpose of the resident kernel's: a CTA
+// keeps a TILE of rows (one row per thread, 512 rows) resident in shared memory
+// -- feature-major 32-row blocks of the pre-transposed input, so x = Xs[f*32 +
+// lane] is conflict free -- and STREAMS every chunk's node records through a
+// ring of bulk copies (TMA engine) issued by a dedicated loader warp.  Per-row
+// accumulators stay in registers across the whole ensemble: no per-chunk
+// partials, no combine pass.  Leaf values are read from global memory (L2):
+// every CTA walks the same chunk at about the same time, so a chunk's nodes and
+// leaves are L2-resident while it is in flight.  Leaf gathers are
+// software-pipelined by one pass (loads of pass p land while pass p+1 walks).
+template <int NI, bool ML>
+__device__ __forceinline__ void stream_walk(const uint2* nb, const float* xl, int I, int D, int (&idx)[4]) {
+  constexpr uint32_t kFeatMask = ML ? 0x7fffffffu : 0xffffffffu;
+#pragma unroll
+  for (int u = 0; u < NI; ++u) idx[u] = 0;
+  for (int lvl = 0; lvl < D; ++lvl) {
+    uint2 a[NI];
+#pragma unroll
+    for (int u = 0; u < NI; ++u) a[u] = nb[u * I + idx[u]];
+    float x[NI];
+#pragma unroll
+    for (int u = 0; u < NI; ++u) x[u] = xl[(a[u].y & kFeatMask) * 32];
+#pragma unroll
+    for (int u = 0; u < NI; ++u) idx[u] = 2 * idx[u] + 1 + go_right<ML>(x[u], a[u]);
+  }
+#pragma unroll
+  for (int u = 0; u < NI; ++u) idx[u] -= I;  // leaf index
+}
+
+template <int KT, typename ACC, bool ML>
+__global__ void __launch_bounds__(544, 1) trav_stream_kernel(const TravParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int NWc = (blockDim.x >> 5) - 1;  // walking warps; the last warp is the loader
+  const int RB = NWc * 32;                // rows per tile
+  const int NS = p.stream_ns, F = p.F, K = p.K, nC = p.n_chunks;
+  float* Xs = reinterpret_cast<float*>(smem);
+  uint8_t* ring = smem + p.stream_x_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)NS * p.stream_stage);
+  uint64_t* xbar = bars;
+  uint64_t* full = bars + 1;
+  uint64_t* empty = full + NS;
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(xbar, 1);
+    for (int i = 0; i < NS; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], NWc);
+    }
+    ptx::fence_barrier_init();
+    ptx::fence_proxy_async();
+  }
+  __syncthreads();
+  const int64_t n_rows = p.n_rows;
+  const int64_t n_tiles = (n_rows + RB - 1) / RB;
+  const int64_t my_tiles = n_tiles > blockIdx.x ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t n_items = my_tiles * nC;
+
+  if (warp == NWc) {
+    // loader: chunk node records, in item order, into the ring
+    // Each slot = [64-byte header: the chunk descriptor][node records]; the
+    // header is written with plain stores before the (release) arrive, so the
+    // walkers never issue a global load for it.
+    if (lane == 0) {
+      for (int64_t k = 0; k < n_items; ++k) {
+        const int s = (int)(k % NS);
+        const TravChunk c = p.chunks[k % nC];
+        ptx::mbar_wait(&empty[s], (uint32_t)(((k / NS) & 1) ^ 1));
+        uint8_t* slot = ring + (size_t)s * p.stream_stage;
+        *reinterpret_cast<TravChunk*>(slot) = c;
+        ptx::fence_proxy_async();
+        ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)c.leaf_offset);
+        ptx::bulk_g2s(slot + 64, p.data + c.offset, (uint32_t)c.leaf_offset, &full[s]);
+      }
+    }
+    return;
+  }
+
+  const int64_t n_blocks = (n_rows + 31) / 32;
+  uint32_t xphase = 0;
+  int64_t k = 0;
+  for (int64_t ti = 0; ti < my_tiles; ++ti) {
+    const int64_t tile = blockIdx.x + ti * gridDim.x;
+    const int64_t blk0 = tile * (RB / 32);
+    const int nblk = (int)(n_blocks - blk0 < RB / 32 ? n_blocks - blk0 : RB / 32);
+    // every walking warp is done with the previous tile: reload X
+    asm volatile("bar.sync 1, %0;" ::"r"(RB) : "memory");
+    if (threadIdx.x == 0) {
+      const uint32_t bytes = (uint32_t)nblk * 32u * (uint32_t)F * 4u;
+      ptx::fence_proxy_async();
+      ptx::mbar_arrive_expect_tx(xbar, bytes);
+      const uint8_t* src = reinterpret_cast<const uint8_t*>(p.X) + blk0 * 32 * (int64_t)F * 4;
+      for (uint32_t o = 0; o < bytes; o += 65536u)
+        ptx::bulk_g2s(reinterpret_cast<uint8_t*>(Xs) + o, src + o, min(65536u, bytes - o), xbar);
+    }
+    ptx::mbar_wait(xbar, xphase);
+    xphase ^= 1;
+    const int64_t row = tile * RB + warp * 32 + lane;
+    const float* xl = Xs + (size_t)warp * F * 32 + lane;
+    ACC acc[KT];
+#pragma unroll
+    for (int q = 0; q < KT; ++q) acc[q] = ACC(0);
+    // pass width (trees walked together) = pending leaf-value slots
+    constexpr int PD = KT <= 4 ? 4 : (KT <= 8 ? 2 : 1);
+    float pv[PD][KT];
+    int npend = 0;
+    // dep: a value produced by the walk that follows the loads (always >= 0).
+    // AND-ing it into the pending values keeps the compiler from hoisting the
+    // adds (and so the wait for the loads) above that walk.
+    auto flush = [&](int dep) {
+      const uint32_t keep = ~(uint32_t)(dep >> 31);
+#pragma unroll
+      for (int u = 0; u < PD; ++u)
+        if (u < npend) {
+#pragma unroll
+          for (int q = 0; q < KT; ++q)
+            if (q < K) acc[q] += leaf_to_acc<ACC>(__uint_as_float(__float_as_uint(pv[u][q]) & keep));
+        }
+      npend = 0;
+    };
+    for (int c = 0; c < nC; ++c, ++k) {
+      const int s = (int)(k % NS);
+      const uint8_t* slot = ring + (size_t)s * p.stream_stage;
+      ptx::mbar_wait(&full[s], (uint32_t)((k / NS) & 1));
+      const TravChunk ch = *reinterpret_cast<const TravChunk*>(slot);
+      const int D = ch.depth, I = (1 << D) - 1, L = 1 << D;
+      const uint2* nodes = reinterpret_cast<const uint2*>(slot + 64);
+      const float* leaves = reinterpret_cast<const float*>(p.data + ch.offset + ch.leaf_offset);
+      for (int j = 0; j < ch.n_trees;) {
+        const int n = min(PD, ch.n_trees - j);
+        int idx[4];
+        switch (n) {
+          case 1: stream_walk<1, ML>(nodes + (size_t)j * I, xl, I, D, idx); break;
+          case 2: stream_walk<(PD >= 2 ? 2 : 1), ML>(nodes + (size_t)j * I, xl, I, D, idx); break;
+          case 3: stream_walk<(PD >= 3 ? 3 : 1), ML>(nodes + (size_t)j * I, xl, I, D, idx); break;
+          default: stream_walk<(PD >= 4 ? 4 : 1), ML>(nodes + (size_t)j * I, xl, I, D, idx); break;
+        }
+        if (p.mode == TRAV_APPLY) {
+          if (row < n_rows)
+            for (int u = 0; u < n; ++u) {
+              const int sl = ch.first_slot + j + u;
+              p.out_leaf[row * p.T + p.slot_tree[sl]] = p.leaf_ids[p.slot_leafid_off[sl] + idx[u]];
+            }
+        } else {
+          flush(idx[0]);  // previous pass's leaf values have landed by now
+#pragma unroll
+          for (int u = 0; u < PD; ++u)
+            if (u < n) {
+              const float* e = leaves + ((size_t)(j + u) * L + idx[u]) * K;
+              if (KT == K && (KT % 4) == 0) {
+#pragma unroll
+                for (int q = 0; q < KT; q += 4) {
+                  const float4 v = __ldg(reinterpret_cast<const float4*>(e) + q / 4);
+                  pv[u][q] = v.x;
+                  pv[u][q + 1 < KT ? q + 1 : 0] = v.y;
+                  pv[u][q + 2 < KT ? q + 2 : 0] = v.z;
+                  pv[u][q + 3 < KT ? q + 3 : 0] = v.w;
+                }
+              } else {
+#pragma unroll
+                for (int q = 0; q < KT; ++q) pv[u][q] = q < K ? __ldg(e + q) : 0.0f;
+              }
+            }
+          npend = n;
+        }
+        j += n;
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&empty[s]);  // this warp is done with the slot
+    }
+    if (p.mode != TRAV_APPLY) {
+      flush(0);
+      if (row < n_rows) finalize_row<KT, ACC>(p.fin, row, acc);
+    }
+  }
+}
+
+template <int KT, typename ACC, bool ML>
+cudaError_t launch_stream_t(const TravParams& p, int grid, int block, int smem, cudaStream_t st) {
+  auto kern = trav_stream_kernel<KT, ACC, ML>;
+  static int configured = 0;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    if (e != cudaSuccess) return e;
+    configured = 1;
+  }
+  if (std::getenv("BRIDGER_DEBUG"))
+    std::fprintf(stderr, "[bridger] trav_stream_kernel grid=%d block=%d smem=%d chunks=%d ns=%d stage=%d\n", grid,
+                 block, smem, p.n_chunks, p.stream_ns, p.stream_stage);
+  cudaEvent_t ev;
+  hot_begin(st, &ev);
+  kern<<<grid, block, smem, st>>>(p);
+  hot_end(st, ev);
+  count_launch();
+  return cudaGetLastError();
+}
+
+#define BRIDGER_STREAM_INSTANTIATE(ACC, ML)                                                                  \
+  template cudaError_t launch_stream_t<1, ACC, ML>(const TravParams&, int, int, int, cudaStream_t);  \
+  template cudaError_t launch_stream_t<2, ACC, ML>(const TravParams&, int, int, int, cudaStream_t);  \
+  template cudaError_t launch_stream_t<4, ACC, ML>(const TravParams&, int, int, int, cudaStream_t);  \
+  template cudaError_t launch_stream_t<8, ACC, ML>(const TravParams&, int, int, int, cudaStream_t);  \
+  template cudaError_t launch_stream_t<16, ACC, ML>(const TravParams&, int, int, int, cudaStream_t); \
+  template cudaError_t launch_stream_t<64, ACC, ML>(const TravParams&, int, int, int, cudaStream_t);
 
 #define BRIDGER_TRAV_INSTANTIATE(ACC, ML, GT, FMT)                                                                  \
   template cudaError_t launch_trav_t<1, ACC, ML, GT, FMT>(const TravParams&, int, int, int, int, cudaStream_t);  \

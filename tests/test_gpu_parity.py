@@ -221,3 +221,22 @@ def test_split_node_format(monkeypatch):
     check(m, X)
     c, m2 = make_config("C2", n_trees=100)
     check(m2, gen_x(2, 0, 9001, 28), apply=False)
+
+
+@pytest.mark.parametrize("n_rows", [77, 513, 148 * 512 + 333])
+def test_tree_streamed_c4_shape(n_rows):
+    # C4-shaped trees (depth 12, 8 classes: 164 KB per tree) exceed shared
+    # memory: tree-streamed mode (row tiles resident, node records streamed)
+    c, m = make_config("C4", n_trees=6)
+    g = B.Model(m)
+    assert g.layout()["format"] == "stream"
+    check(m, gen_x(4, 0, n_rows, 64), apply=n_rows < 1000)
+
+
+@pytest.mark.parametrize("ml", [False, True])
+def test_tree_streamed_pruned_missing_mixed_depth(ml):
+    m = perfect_ensemble(95, 9, 12, 64, kind="classification", n_classes=8, calib_rows=2048)
+    m = prune_ensemble(m, 95, p=0.003, with_missing=ml)  # heavier pruning selects the sparse layout
+    g = B.Model(m)
+    assert g.layout()["format"] == "stream"
+    check(m, inject_specials(gen_x(96, 0, 2001, 64), 96, rate=0.02))

@@ -570,19 +570,28 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
     const int32_t ns = 3;
     // one slot = 64-byte chunk header + node records
     const int64_t stage = std::max<int64_t>((tree_nodes + 15) / 16 * 16, 16384) + 64;
+    std::vector<Run> pieces;
+    int32_t min_n = INT32_MAX;
+    for (const Run& r : bal) {
+      const int64_t per = std::max<int64_t>(1, std::min<int64_t>(4, (stage - 64) / ((((int64_t)1 << r.D) - 1) * 8)));
+      for (int32_t s0 = 0; s0 < r.n; s0 += (int32_t)per) {
+        pieces.push_back({r.start + s0, (int32_t)std::min<int64_t>(per, r.n - s0), r.D});
+        min_n = std::min(min_n, pieces.back().n);
+      }
+    }
+    const int32_t w = (min_n >= 2 && K <= 8) ? 2 : 1;  // trees per pass (every chunk holds >= w)
+    // shared memory: X tile (32 rows per warp) + ring + per-thread leaf slots
+    auto fits = [&](int32_t wp) {
+      return (int64_t)wp * 32 * F * 4 + ns * stage + (int64_t)wp * 32 * w * K * 4 + 1024 <= kSmemMax;
+    };
     int32_t warps = 16;
-    while (warps > 4 && (int64_t)warps * 32 * F * 4 + ns * stage + 1024 > kSmemMax) warps /= 2;
-    if (want_stream && (int64_t)warps * 32 * F * 4 + ns * stage + 1024 <= kSmemMax && warps >= 4) {
+    while (warps > 4 && !fits(warps)) --warps;
+    if (want_stream && fits(warps)) {
       out->stream = true;
       out->stream_ns = ns;
       out->stream_stage = (int32_t)stage;
       out->stream_warps = warps;
-      std::vector<Run> pieces;
-      for (const Run& r : bal) {
-        const int64_t per = std::max<int64_t>(1, std::min<int64_t>(4, (stage - 64) / ((((int64_t)1 << r.D) - 1) * 8)));
-        for (int32_t s0 = 0; s0 < r.n; s0 += (int32_t)per)
-          pieces.push_back({r.start + s0, (int32_t)std::min<int64_t>(per, r.n - s0), r.D});
-      }
+      out->stream_w = w;
       bal.swap(pieces);
     }
   }

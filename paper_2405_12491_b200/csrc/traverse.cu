@@ -43,17 +43,22 @@ BRIDGER_TRAV_EXTERN(long long, false, false, 5)
 BRIDGER_TRAV_EXTERN(long long, true, false, 5)
 BRIDGER_TRAV_EXTERN(double, false, false, 5)
 BRIDGER_TRAV_EXTERN(double, true, false, 5)
-#define BRIDGER_STREAM_EXTERN(ACC, ML)                                                                        \
-  extern template cudaError_t launch_stream_t<1, ACC, ML>(const TravParams&, int, int, int, cudaStream_t);  \
-  extern template cudaError_t launch_stream_t<2, ACC, ML>(const TravParams&, int, int, int, cudaStream_t);  \
-  extern template cudaError_t launch_stream_t<4, ACC, ML>(const TravParams&, int, int, int, cudaStream_t);  \
-  extern template cudaError_t launch_stream_t<8, ACC, ML>(const TravParams&, int, int, int, cudaStream_t);  \
-  extern template cudaError_t launch_stream_t<16, ACC, ML>(const TravParams&, int, int, int, cudaStream_t); \
-  extern template cudaError_t launch_stream_t<64, ACC, ML>(const TravParams&, int, int, int, cudaStream_t);
-BRIDGER_STREAM_EXTERN(long long, false)
-BRIDGER_STREAM_EXTERN(long long, true)
-BRIDGER_STREAM_EXTERN(double, false)
-BRIDGER_STREAM_EXTERN(double, true)
+#define BRIDGER_STREAM_EXTERN_W(ACC, ML, W)                                                                         \
+  extern template cudaError_t launch_stream_t<1, ACC, ML, W, false>(const TravParams&, int, int, int, cudaStream_t);  \
+  extern template cudaError_t launch_stream_t<2, ACC, ML, W, false>(const TravParams&, int, int, int, cudaStream_t);  \
+  extern template cudaError_t launch_stream_t<4, ACC, ML, W, false>(const TravParams&, int, int, int, cudaStream_t);  \
+  extern template cudaError_t launch_stream_t<8, ACC, ML, W, false>(const TravParams&, int, int, int, cudaStream_t);  \
+  extern template cudaError_t launch_stream_t<16, ACC, ML, W, false>(const TravParams&, int, int, int, cudaStream_t); \
+  extern template cudaError_t launch_stream_t<64, ACC, ML, W, false>(const TravParams&, int, int, int, cudaStream_t); \
+  extern template cudaError_t launch_stream_t<1, ACC, ML, W, true>(const TravParams&, int, int, int, cudaStream_t);
+BRIDGER_STREAM_EXTERN_W(long long, false, 1)
+BRIDGER_STREAM_EXTERN_W(long long, true, 1)
+BRIDGER_STREAM_EXTERN_W(double, false, 1)
+BRIDGER_STREAM_EXTERN_W(double, true, 1)
+BRIDGER_STREAM_EXTERN_W(long long, false, 2)
+BRIDGER_STREAM_EXTERN_W(long long, true, 2)
+BRIDGER_STREAM_EXTERN_W(double, false, 2)
+BRIDGER_STREAM_EXTERN_W(double, true, 2)
 BRIDGER_TRAV_EXTERN(long long, false, true, 2)
 BRIDGER_TRAV_EXTERN(long long, true, true, 2)
 BRIDGER_TRAV_EXTERN(double, false, true, 2)
@@ -234,18 +239,28 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
       p.stream_stage = L.stream_stage;
       const int rb = L.stream_warps * 32;
       p.stream_x_bytes = rb * m->F * 4;
-      const int smem_s = p.stream_x_bytes + L.stream_ns * L.stream_stage + (1 + 2 * L.stream_ns) * 8 + 16;
+      const int W = L.stream_w;
+      p.stream_lbuf_bytes = (rb * W * m->K * 4 + 15) / 16 * 16;
+      const int smem_s = p.stream_x_bytes + L.stream_ns * L.stream_stage + p.stream_lbuf_bytes + (1 + 2 * L.stream_ns) * 8 + 16;
       const int64_t n_tiles = (n_rows + rb - 1) / rb;
       const int grid_s = (int)std::max<int64_t>(1, std::min<int64_t>(n_tiles, sms));
       const int block_s = (L.stream_warps + 1) * 32;
-      BRIDGER_DISPATCH_KT(m->K, {
-        if (m->acc_int)
-          err = L.has_missing ? launch_stream_t<KT, long long, true>(p, grid_s, block_s, smem_s, st)
-                              : launch_stream_t<KT, long long, false>(p, grid_s, block_s, smem_s, st);
-        else
-          err = L.has_missing ? launch_stream_t<KT, double, true>(p, grid_s, block_s, smem_s, st)
-                              : launch_stream_t<KT, double, false>(p, grid_s, block_s, smem_s, st);
-      });
+      const bool w2 = W == 2;
+      const bool ml = L.has_missing;
+      if (want == 3) {
+        err = ml ? (w2 ? launch_stream_t<1, long long, true, 2, true>(p, grid_s, block_s, smem_s, st)
+                       : launch_stream_t<1, long long, true, 1, true>(p, grid_s, block_s, smem_s, st))
+                 : (w2 ? launch_stream_t<1, long long, false, 2, true>(p, grid_s, block_s, smem_s, st)
+                       : launch_stream_t<1, long long, false, 1, true>(p, grid_s, block_s, smem_s, st));
+      } else {
+#define BRIDGER_ST(ACC)                                                                      \
+  (ml ? (w2 ? launch_stream_t<KT, ACC, true, 2, false>(p, grid_s, block_s, smem_s, st)      \
+            : launch_stream_t<KT, ACC, true, 1, false>(p, grid_s, block_s, smem_s, st))     \
+      : (w2 ? launch_stream_t<KT, ACC, false, 2, false>(p, grid_s, block_s, smem_s, st)     \
+            : launch_stream_t<KT, ACC, false, 1, false>(p, grid_s, block_s, smem_s, st)))
+        BRIDGER_DISPATCH_KT(m->K, { err = m->acc_int ? BRIDGER_ST(long long) : BRIDGER_ST(double); });
+#undef BRIDGER_ST
+      }
     }
     cudaFreeAsync(xt, st);
     return err;

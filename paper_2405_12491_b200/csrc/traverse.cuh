@@ -75,6 +75,7 @@ struct TravParams {
   int32_t stream_ns;      // tree-streamed mode: node-record ring depth
   int32_t stream_stage;   //                     bytes per ring slot
   int32_t stream_x_bytes; //                     X tile bytes (rows_per_tile * F * 4)
+  int32_t stream_lbuf_bytes; //                  leaf-value landing slots (rows_per_tile * W * K * 4)
   FinalizeArgs fin;   // (TRAV_FINAL, TRAV_CLUSTER)
 };
 
@@ -717,26 +718,30 @@ cudaError_t launch_trav_t(const TravParams& p, int grid_ctas, int block, int sme
 // every CTA walks the same chunk at about the same time, so a chunk's nodes and
 // leaves are L2-resident while it is in flight.  Leaf gathers are
 // software-pipelined by one pass (loads of pass p land while pass p+1 walks).
-template <int NI, bool ML>
-__device__ __forceinline__ void stream_walk(const uint2* nb, const float* xl, int I, int D, int (&idx)[4]) {
+template <int W, bool ML>
+__device__ __forceinline__ void stream_walk(const uint2* nb, const float* xl, int I, int D, int (&idx)[W]) {
   constexpr uint32_t kFeatMask = ML ? 0x7fffffffu : 0xffffffffu;
 #pragma unroll
-  for (int u = 0; u < NI; ++u) idx[u] = 0;
+  for (int u = 0; u < W; ++u) idx[u] = 0;
   for (int lvl = 0; lvl < D; ++lvl) {
-    uint2 a[NI];
+    uint2 a[W];
 #pragma unroll
-    for (int u = 0; u < NI; ++u) a[u] = nb[u * I + idx[u]];
-    float x[NI];
+    for (int u = 0; u < W; ++u) a[u] = nb[u * I + idx[u]];
+    float x[W];
 #pragma unroll
-    for (int u = 0; u < NI; ++u) x[u] = xl[(a[u].y & kFeatMask) * 32];
+    for (int u = 0; u < W; ++u) x[u] = xl[(a[u].y & kFeatMask) * 32];
 #pragma unroll
-    for (int u = 0; u < NI; ++u) idx[u] = 2 * idx[u] + 1 + go_right<ML>(x[u], a[u]);
+    for (int u = 0; u < W; ++u) idx[u] = 2 * idx[u] + 1 + go_right<ML>(x[u], a[u]);
   }
 #pragma unroll
-  for (int u = 0; u < NI; ++u) idx[u] -= I;  // leaf index
+  for (int u = 0; u < W; ++u) idx[u] -= I;  // leaf index
 }
 
-template <int KT, typename ACC, bool ML>
+// W: trees walked together per pass (= the chunk width chosen at lowering; a
+// chunk's last pass masks trees past its end).  The steady-state loop has no
+// divergent branch: ptxas drains every load scoreboard at one, which would
+// serialise the leaf-gather latency the pipelining hides.
+template <int KT, typename ACC, bool ML, int W, bool APPLY>
 __global__ void __launch_bounds__(544, 1) trav_stream_kernel(const TravParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -745,7 +750,9 @@ __global__ void __launch_bounds__(544, 1) trav_stream_kernel(const TravParams p)
   const int NS = p.stream_ns, F = p.F, K = p.K, nC = p.n_chunks;
   float* Xs = reinterpret_cast<float*>(smem);
   uint8_t* ring = smem + p.stream_x_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)NS * p.stream_stage);
+  // per-thread landing slot of the previous pass's leaf values (cp.async)
+  float* lbuf_all = reinterpret_cast<float*>(ring + (size_t)NS * p.stream_stage);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(lbuf_all) + p.stream_lbuf_bytes);
   uint64_t* xbar = bars;
   uint64_t* full = bars + 1;
   uint64_t* empty = full + NS;
@@ -753,7 +760,7 @@ __global__ void __launch_bounds__(544, 1) trav_stream_kernel(const TravParams p)
     ptx::mbar_init(xbar, 1);
     for (int i = 0; i < NS; ++i) {
       ptx::mbar_init(&full[i], 1);
-      ptx::mbar_init(&empty[i], NWc);
+      ptx::mbar_init(&empty[i], RB);  // every walking thread arrives (no elected-lane branch)
     }
     ptx::fence_barrier_init();
     ptx::fence_proxy_async();
@@ -765,20 +772,26 @@ __global__ void __launch_bounds__(544, 1) trav_stream_kernel(const TravParams p)
   const int64_t n_items = my_tiles * nC;
 
   if (warp == NWc) {
-    // loader: chunk node records, in item order, into the ring
-    // Each slot = [64-byte header: the chunk descriptor][node records]; the
-    // header is written with plain stores before the (release) arrive, so the
-    // walkers never issue a global load for it.
+    // loader: chunk node records, in item order, into the ring.  Each slot =
+    // [64-byte header: the chunk descriptor][node records]; the header is
+    // written with plain stores before the (release) arrive, so the walkers
+    // never issue a global load for it.
     if (lane == 0) {
+      int s = 0, c_i = 0;
+      uint32_t ph = 0;
       for (int64_t k = 0; k < n_items; ++k) {
-        const int s = (int)(k % NS);
-        const TravChunk c = p.chunks[k % nC];
-        ptx::mbar_wait(&empty[s], (uint32_t)(((k / NS) & 1) ^ 1));
+        const TravChunk c = p.chunks[c_i];
+        if (++c_i == nC) c_i = 0;
+        ptx::mbar_wait(&empty[s], ph ^ 1);
         uint8_t* slot = ring + (size_t)s * p.stream_stage;
         *reinterpret_cast<TravChunk*>(slot) = c;
         ptx::fence_proxy_async();
         ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)c.leaf_offset);
         ptx::bulk_g2s(slot + 64, p.data + c.offset, (uint32_t)c.leaf_offset, &full[s]);
+        if (++s == NS) {
+          s = 0;
+          ph ^= 1;
+        }
       }
     }
     return;
@@ -786,7 +799,9 @@ __global__ void __launch_bounds__(544, 1) trav_stream_kernel(const TravParams p)
 
   const int64_t n_blocks = (n_rows + 31) / 32;
   uint32_t xphase = 0;
-  int64_t k = 0;
+  // ring position kept incrementally: no 64-bit division in the loop
+  int s = 0;
+  uint32_t ph = 0;
   for (int64_t ti = 0; ti < my_tiles; ++ti) {
     const int64_t tile = blockIdx.x + ti * gridDim.x;
     const int64_t blk0 = tile * (RB / 32);
@@ -808,84 +823,90 @@ __global__ void __launch_bounds__(544, 1) trav_stream_kernel(const TravParams p)
     ACC acc[KT];
 #pragma unroll
     for (int q = 0; q < KT; ++q) acc[q] = ACC(0);
-    // pass width (trees walked together) = pending leaf-value slots
-    constexpr int PD = KT <= 4 ? 4 : (KT <= 8 ? 2 : 1);
-    float pv[PD][KT];
-    int npend = 0;
-    // dep: a value produced by the walk that follows the loads (always >= 0).
-    // AND-ing it into the pending values keeps the compiler from hoisting the
-    // adds (and so the wait for the loads) above that walk.
-    auto flush = [&](int dep) {
-      const uint32_t keep = ~(uint32_t)(dep >> 31);
+    // The previous pass's leaf values land in this thread's shared-memory slot
+    // through cp.async: their completion is tracked by the async-copy group,
+    // not by a register scoreboard, so the walk's loops and branches (where
+    // ptxas drains outstanding loads) do not serialise the gather latency.
+    float* lbuf = lbuf_all + (size_t)threadIdx.x * W * K;
+    uint32_t pmask[W];
 #pragma unroll
-      for (int u = 0; u < PD; ++u)
-        if (u < npend) {
+    for (int u = 0; u < W; ++u) pmask[u] = 0u;
+    auto flush = [&]() {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
 #pragma unroll
-          for (int q = 0; q < KT; ++q)
-            if (q < K) acc[q] += leaf_to_acc<ACC>(__uint_as_float(__float_as_uint(pv[u][q]) & keep));
-        }
-      npend = 0;
+      for (int u = 0; u < W; ++u) {
+        const uint32_t m = pmask[u];
+#pragma unroll
+        for (int q = 0; q < KT; ++q)
+          if (q < K) acc[q] += leaf_to_acc<ACC>(__uint_as_float(__float_as_uint(lbuf[u * K + q]) & m));
+        pmask[u] = 0u;
+      }
     };
-    for (int c = 0; c < nC; ++c, ++k) {
-      const int s = (int)(k % NS);
+    ptx::mbar_wait(&full[s], ph);
+    for (int c = 0; c < nC; ++c) {
       const uint8_t* slot = ring + (size_t)s * p.stream_stage;
-      ptx::mbar_wait(&full[s], (uint32_t)((k / NS) & 1));
       const TravChunk ch = *reinterpret_cast<const TravChunk*>(slot);
       const int D = ch.depth, I = (1 << D) - 1, L = 1 << D;
       const uint2* nodes = reinterpret_cast<const uint2*>(slot + 64);
       const float* leaves = reinterpret_cast<const float*>(p.data + ch.offset + ch.leaf_offset);
-      for (int j = 0; j < ch.n_trees;) {
-        const int n = min(PD, ch.n_trees - j);
-        int idx[4];
-        switch (n) {
-          case 1: stream_walk<1, ML>(nodes + (size_t)j * I, xl, I, D, idx); break;
-          case 2: stream_walk<(PD >= 2 ? 2 : 1), ML>(nodes + (size_t)j * I, xl, I, D, idx); break;
-          case 3: stream_walk<(PD >= 3 ? 3 : 1), ML>(nodes + (size_t)j * I, xl, I, D, idx); break;
-          default: stream_walk<(PD >= 4 ? 4 : 1), ML>(nodes + (size_t)j * I, xl, I, D, idx); break;
-        }
-        if (p.mode == TRAV_APPLY) {
-          if (row < n_rows)
-            for (int u = 0; u < n; ++u) {
-              const int sl = ch.first_slot + j + u;
+      for (int j = 0; j < ch.n_trees; j += W) {
+        int idx[W];
+        // trees past the chunk's end re-walk its last tree (masked below)
+        const int jw = min(j, ch.n_trees - W < 0 ? 0 : ch.n_trees - W);
+        stream_walk<W, ML>(nodes + (size_t)jw * I, xl, I, D, idx);
+        if (APPLY) {
+#pragma unroll
+          for (int u = 0; u < W; ++u) {
+            const int t = jw + u;
+            if (t >= j && t < ch.n_trees && row < n_rows) {
+              const int sl = ch.first_slot + t;
               p.out_leaf[row * p.T + p.slot_tree[sl]] = p.leaf_ids[p.slot_leafid_off[sl] + idx[u]];
             }
+          }
         } else {
-          flush(idx[0]);  // previous pass's leaf values have landed by now
+          flush();  // the previous pass's leaf values have landed by now
+          const bool last_pass = j + W >= ch.n_trees;
+          if (last_pass && c + 1 < nC) {
+            // next slot's node records: waited for while no leaf load is in flight
+            const int s2 = s + 1 == NS ? 0 : s + 1;
+            ptx::mbar_wait(&full[s2], s2 == 0 ? ph ^ 1 : ph);
+          }
 #pragma unroll
-          for (int u = 0; u < PD; ++u)
-            if (u < n) {
-              const float* e = leaves + ((size_t)(j + u) * L + idx[u]) * K;
-              if (KT == K && (KT % 4) == 0) {
+          for (int u = 0; u < W; ++u) {
+            const int t = jw + u;
+            pmask[u] = (t >= j && t < ch.n_trees) ? 0xffffffffu : 0u;
+            const float* e = leaves + ((size_t)t * L + idx[u]) * K;
+            const uint32_t d = ptx::s2u(lbuf + u * K);
+            if (KT == K && (KT % 4) == 0) {
 #pragma unroll
-                for (int q = 0; q < KT; q += 4) {
-                  const float4 v = __ldg(reinterpret_cast<const float4*>(e) + q / 4);
-                  pv[u][q] = v.x;
-                  pv[u][q + 1 < KT ? q + 1 : 0] = v.y;
-                  pv[u][q + 2 < KT ? q + 2 : 0] = v.z;
-                  pv[u][q + 3 < KT ? q + 3 : 0] = v.w;
-                }
-              } else {
+              for (int q = 0; q < KT; q += 4)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 4 * q), "l"(e + q) : "memory");
+            } else {
 #pragma unroll
-                for (int q = 0; q < KT; ++q) pv[u][q] = q < K ? __ldg(e + q) : 0.0f;
-              }
+              for (int q = 0; q < KT; ++q)
+                if (q < K) asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d + 4 * q), "l"(e + q) : "memory");
             }
-          npend = n;
+          }
+          asm volatile("cp.async.commit_group;" ::: "memory");
         }
-        j += n;
       }
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&empty[s]);  // this warp is done with the slot
+      ptx::mbar_arrive(&empty[s]);  // this thread is done with the slot
+      if (APPLY && c + 1 < nC) ptx::mbar_wait(&full[s + 1 == NS ? 0 : s + 1], s + 1 == NS ? ph ^ 1 : ph);
+      if (++s == NS) {
+        s = 0;
+        ph ^= 1;
+      }
     }
-    if (p.mode != TRAV_APPLY) {
-      flush(0);
+    if (!APPLY) {
+      flush();
       if (row < n_rows) finalize_row<KT, ACC>(p.fin, row, acc);
     }
   }
 }
 
-template <int KT, typename ACC, bool ML>
+template <int KT, typename ACC, bool ML, int W, bool APPLY>
 cudaError_t launch_stream_t(const TravParams& p, int grid, int block, int smem, cudaStream_t st) {
-  auto kern = trav_stream_kernel<KT, ACC, ML>;
+  auto kern = trav_stream_kernel<KT, ACC, ML, W, APPLY>;
   static int configured = 0;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
@@ -893,8 +914,8 @@ cudaError_t launch_stream_t(const TravParams& p, int grid, int block, int smem, 
     configured = 1;
   }
   if (std::getenv("BRIDGER_DEBUG"))
-    std::fprintf(stderr, "[bridger] trav_stream_kernel grid=%d block=%d smem=%d chunks=%d ns=%d stage=%d\n", grid,
-                 block, smem, p.n_chunks, p.stream_ns, p.stream_stage);
+    std::fprintf(stderr, "[bridger] trav_stream_kernel W=%d grid=%d block=%d smem=%d chunks=%d ns=%d stage=%d\n", W,
+                 grid, block, smem, p.n_chunks, p.stream_ns, p.stream_stage);
   cudaEvent_t ev;
   hot_begin(st, &ev);
   kern<<<grid, block, smem, st>>>(p);
@@ -903,13 +924,18 @@ cudaError_t launch_stream_t(const TravParams& p, int grid, int block, int smem, 
   return cudaGetLastError();
 }
 
-#define BRIDGER_STREAM_INSTANTIATE(ACC, ML)                                                                  \
-  template cudaError_t launch_stream_t<1, ACC, ML>(const TravParams&, int, int, int, cudaStream_t);  \
-  template cudaError_t launch_stream_t<2, ACC, ML>(const TravParams&, int, int, int, cudaStream_t);  \
-  template cudaError_t launch_stream_t<4, ACC, ML>(const TravParams&, int, int, int, cudaStream_t);  \
-  template cudaError_t launch_stream_t<8, ACC, ML>(const TravParams&, int, int, int, cudaStream_t);  \
-  template cudaError_t launch_stream_t<16, ACC, ML>(const TravParams&, int, int, int, cudaStream_t); \
-  template cudaError_t launch_stream_t<64, ACC, ML>(const TravParams&, int, int, int, cudaStream_t);
+#define BRIDGER_STREAM_INSTANTIATE_W(ACC, ML, W)                                                                  \
+  template cudaError_t launch_stream_t<1, ACC, ML, W, false>(const TravParams&, int, int, int, cudaStream_t);  \
+  template cudaError_t launch_stream_t<2, ACC, ML, W, false>(const TravParams&, int, int, int, cudaStream_t);  \
+  template cudaError_t launch_stream_t<4, ACC, ML, W, false>(const TravParams&, int, int, int, cudaStream_t);  \
+  template cudaError_t launch_stream_t<8, ACC, ML, W, false>(const TravParams&, int, int, int, cudaStream_t);  \
+  template cudaError_t launch_stream_t<16, ACC, ML, W, false>(const TravParams&, int, int, int, cudaStream_t); \
+  template cudaError_t launch_stream_t<64, ACC, ML, W, false>(const TravParams&, int, int, int, cudaStream_t);
+#define BRIDGER_STREAM_INSTANTIATE(ACC, ML)                                                                   \
+  BRIDGER_STREAM_INSTANTIATE_W(ACC, ML, 1)                                                                    \
+  BRIDGER_STREAM_INSTANTIATE_W(ACC, ML, 2)                                                                    \
+  template cudaError_t launch_stream_t<1, ACC, ML, 1, true>(const TravParams&, int, int, int, cudaStream_t); \
+  template cudaError_t launch_stream_t<1, ACC, ML, 2, true>(const TravParams&, int, int, int, cudaStream_t);
 
 #define BRIDGER_TRAV_INSTANTIATE(ACC, ML, GT, FMT)                                                                  \
   template cudaError_t launch_trav_t<1, ACC, ML, GT, FMT>(const TravParams&, int, int, int, int, cudaStream_t);  \

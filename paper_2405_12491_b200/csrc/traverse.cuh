@@ -827,7 +827,11 @@ __global__ void __launch_bounds__(544, 1) trav_stream_kernel(const TravParams p)
     // through cp.async: their completion is tracked by the async-copy group,
     // not by a register scoreboard, so the walk's loops and branches (where
     // ptxas drains outstanding loads) do not serialise the gather latency.
-    float* lbuf = lbuf_all + (size_t)threadIdx.x * W * K;
+    // element-major: value v of this thread at lbuf[v * RB] (float4 units when
+    // K % 4 == 0), so a warp's copies and reads touch consecutive words
+    constexpr bool V4 = (KT % 4) == 0;
+    const bool v4 = V4 && KT == K;
+    float* lbuf = lbuf_all + (size_t)threadIdx.x * (v4 ? 4 : 1);
     uint32_t pmask[W];
 #pragma unroll
     for (int u = 0; u < W; ++u) pmask[u] = 0u;
@@ -836,9 +840,20 @@ __global__ void __launch_bounds__(544, 1) trav_stream_kernel(const TravParams p)
 #pragma unroll
       for (int u = 0; u < W; ++u) {
         const uint32_t m = pmask[u];
+        if (v4) {
 #pragma unroll
-        for (int q = 0; q < KT; ++q)
-          if (q < K) acc[q] += leaf_to_acc<ACC>(__uint_as_float(__float_as_uint(lbuf[u * K + q]) & m));
+          for (int q = 0; q < KT; q += 4) {
+            const float4 v = *reinterpret_cast<const float4*>(lbuf + (size_t)(u * (KT / 4) + q / 4) * RB * 4);
+            acc[q] += leaf_to_acc<ACC>(__uint_as_float(__float_as_uint(v.x) & m));
+            acc[q + 1 < KT ? q + 1 : 0] += leaf_to_acc<ACC>(__uint_as_float(__float_as_uint(v.y) & m));
+            acc[q + 2 < KT ? q + 2 : 0] += leaf_to_acc<ACC>(__uint_as_float(__float_as_uint(v.z) & m));
+            acc[q + 3 < KT ? q + 3 : 0] += leaf_to_acc<ACC>(__uint_as_float(__float_as_uint(v.w) & m));
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < KT; ++q)
+            if (q < K) acc[q] += leaf_to_acc<ACC>(__uint_as_float(__float_as_uint(lbuf[(size_t)(u * K + q) * RB]) & m));
+        }
         pmask[u] = 0u;
       }
     };
@@ -876,15 +891,19 @@ __global__ void __launch_bounds__(544, 1) trav_stream_kernel(const TravParams p)
             const int t = jw + u;
             pmask[u] = (t >= j && t < ch.n_trees) ? 0xffffffffu : 0u;
             const float* e = leaves + ((size_t)t * L + idx[u]) * K;
-            const uint32_t d = ptx::s2u(lbuf + u * K);
-            if (KT == K && (KT % 4) == 0) {
+            if (v4) {
 #pragma unroll
-              for (int q = 0; q < KT; q += 4)
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 4 * q), "l"(e + q) : "memory");
+              for (int q = 0; q < KT; q += 4) {
+                const uint32_t d = ptx::s2u(lbuf + (size_t)(u * (KT / 4) + q / 4) * RB * 4);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(e + q) : "memory");
+              }
             } else {
 #pragma unroll
               for (int q = 0; q < KT; ++q)
-                if (q < K) asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d + 4 * q), "l"(e + q) : "memory");
+                if (q < K) {
+                  const uint32_t d = ptx::s2u(lbuf + (size_t)(u * K + q) * RB);
+                  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(e + q) : "memory");
+                }
             }
           }
           asm volatile("cp.async.commit_group;" ::: "memory");

@@ -101,3 +101,40 @@ def run(m, X: np.ndarray, n_threads: int | None = None, want=("leaf", "acc", "s"
     if rc != 0:
         raise ValueError(f"oracle_run failed with code {rc}")
     return {k: v for k, v in out.items() if v is not None}
+
+
+class _Linear(C.Structure):
+    _fields_ = [("n_features", C.c_int32), ("n_outputs", C.c_int32), ("coef", C.c_void_p),
+                ("intercept", C.c_void_p), ("mean", C.c_void_p), ("scale", C.c_void_p),
+                ("task", C.c_int32), ("post", C.c_int32)]
+
+
+def run_linear(m, X: np.ndarray):
+    """Linear model (oracle.c oracle_linear_run): ``m`` has n_features, n_outputs,
+    coef [K,F] fp64, intercept [K] | None, mean/scale [F] | None (StandardScaler),
+    task, post.  Returns s [n,K] fp64 and label/proba (classification) or pred."""
+    lib = _load()
+    if not hasattr(lib, "_lin_ready"):
+        lib.oracle_linear_run.restype = C.c_int
+        lib.oracle_linear_run.argtypes = [C.POINTER(_Linear), C.c_void_p, C.c_int64, C.c_int32,
+                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        lib._lin_ready = True
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    n, F = X.shape
+    K = int(m.n_outputs)
+    keep = dict(coef=np.ascontiguousarray(m.coef, np.float64).reshape(K, F),
+                b=None if m.intercept is None else np.ascontiguousarray(m.intercept, np.float64),
+                mean=None if m.mean is None else np.ascontiguousarray(m.mean, np.float64),
+                scale=None if m.scale is None else np.ascontiguousarray(m.scale, np.float64))
+    mm = _Linear(int(m.n_features), K, _ptr(keep["coef"]), _ptr(keep["b"]), _ptr(keep["mean"]),
+                 _ptr(keep["scale"]), int(m.task), int(m.post))
+    classif = int(m.task) == 1
+    out = dict(s=np.empty((n, K), np.float64),
+               label=np.empty(n, np.int32) if classif else None,
+               proba=np.empty((n, 2 if K == 1 else K), np.float32) if classif else None,
+               pred=None if classif else np.empty((n, K), np.float32))
+    rc = lib.oracle_linear_run(C.byref(mm), X.ctypes.data, n, F, _ptr(out["s"]), _ptr(out["label"]),
+                               _ptr(out["proba"]), _ptr(out["pred"]))
+    if rc != 0:
+        raise ValueError(f"oracle_linear_run failed with code {rc}")
+    return {k: v for k, v in out.items() if v is not None}

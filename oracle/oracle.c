@@ -161,3 +161,79 @@ int oracle_run(const oracle_model* m, const float* X, int64_t n_rows, int32_t n_
   free(jobs); free(th);
   return err ? 1 : 0;
 }
+
+/* ------------------------------------------------------------------------ *
+ * Linear models (the paper's other GPU-evaluated CML models,
+ * PAPER.md:800-801, 861-862; LogisticRegression / SGDClassifier / LinearRegression
+ * / Ridge, optionally behind a StandardScaler).  Plain definition, fp64:
+ *
+ *   scaler (optional, reading c16 = sklearn 1.9 StandardScaler.transform on an
+ *   fp32 X: X -= mean_.astype(float32); X /= scale_.astype(float32)):
+ *     x'_f = ((float)x_f - (float)mean_f) / (float)scale_f      (fp32 ops)
+ *   s_k = intercept_k + sum_{f = 0..F-1} coef[k][f] * x'_f     (fp64, f in order,
+ *                                                                no FMA)
+ *   regression:   pred[k] = (float) s_k
+ *   classif K==1: label = (s_0 > 0); proba = sigmoid (reading c7, c10)
+ *   classif K>=2: label = smallest k maximising s_k; proba = softmax (c15)
+ *                 (post = IDENTITY: proba = (float) s_k)
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  int32_t n_features, n_outputs;
+  const double* coef;       /* [K][F] */
+  const double* intercept;  /* [K] or NULL */
+  const double* mean;       /* [F] or NULL (no scaler) */
+  const double* scale;      /* [F] or NULL */
+  int32_t task, post;
+} oracle_linear;
+
+int oracle_linear_run(const oracle_linear* m, const float* X, int64_t n_rows, int32_t n_features,
+                      double* s_out, int32_t* label, float* proba, float* pred) {
+  if (!m || n_features != m->n_features || m->n_outputs < 1 || m->n_outputs > 64) return 2;
+  const int32_t F = m->n_features, K = m->n_outputs;
+  for (int64_t r = 0; r < n_rows; ++r) {
+    const float* x = X + r * (int64_t)F;
+    double s[64];
+    for (int k = 0; k < K; ++k) {
+      double acc = m->intercept ? m->intercept[k] : 0.0;
+      for (int f = 0; f < F; ++f) {
+        float xv = x[f];
+        if (m->mean) {
+          const float m32 = (float)m->mean[f], s32 = (float)m->scale[f];
+          const float c = xv - m32;  /* fp32 subtract (FLT_EVAL_METHOD 0) */
+          xv = c / s32;              /* fp32 divide */
+        }
+        const double prod = m->coef[(int64_t)k * F + f] * (double)xv;
+        acc = acc + prod;
+      }
+      s[k] = acc;
+      if (s_out) s_out[r * K + k] = acc;
+    }
+    if (m->task == 0) {
+      if (pred) for (int k = 0; k < K; ++k) pred[r * K + k] = (float)s[k];
+    } else if (K == 1) {
+      if (label) label[r] = s[0] > 0.0 ? 1 : 0;
+      if (proba) {
+        const double p = 1.0 / (1.0 + exp(-s[0]));
+        proba[r * 2 + 0] = (float)(1.0 - p);
+        proba[r * 2 + 1] = (float)p;
+      }
+    } else {
+      if (label) {
+        int best = 0;
+        for (int k = 1; k < K; ++k) if (s[k] > s[best]) best = k;
+        label[r] = best;
+      }
+      if (proba) {
+        if (m->post == 2) {
+          double mx = s[0], e[64], z = 0.0;
+          for (int k = 1; k < K; ++k) if (s[k] > mx) mx = s[k];
+          for (int k = 0; k < K; ++k) { e[k] = exp(s[k] - mx); z += e[k]; }
+          for (int k = 0; k < K; ++k) proba[r * K + k] = (float)(e[k] / z);
+        } else {
+          for (int k = 0; k < K; ++k) proba[r * K + k] = (float)s[k];
+        }
+      }
+    }
+  }
+  return 0;
+}

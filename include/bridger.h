@@ -214,6 +214,49 @@ bridger_status bridger_analyze_exactness(const bridger_model_desc* desc, int32_t
 /* Validation only (E_INVALID_TREE etc. exactly as load). */
 bridger_status bridger_validate(const bridger_model_desc* desc);
 
+/* ---------------------------------------------------------------------------
+ * Linear models (the paper's other GPU-evaluated classical-ML
+ * models, PAPER.md:800-801, 861-862 -- LogisticRegression, SGDClassifier,
+ * LinearRegression, Ridge -- optionally behind a StandardScaler).  What is
+ * computed (oracle.c oracle_linear_run is the definition):
+ *   x'_f = ((float)x_f - (float)mean_f) / (float)scale_f   fp32 ops (reading c16),
+ *                                                          only with a scaler
+ *   s_k  = intercept_k + sum_{f=0..F-1} coef[k][f] * x'_f   fp64, f ascending, no FMA
+ *   regression: out[r,k] = (float) s_k
+ *   classification K == 1: label = [s_0 > 0]; proba = [1-p, p], p = sigmoid(s_0)
+ *   classification K >= 2: label = lowest k maximising s_k; proba = softmax
+ *                          (post SOFTMAX) or (float) s_k (post IDENTITY)
+ * Scores are bit-identical to the oracle's (same fp64 operation order), so
+ * labels are exact; sigmoid/softmax probabilities agree within 1e-5 (c10).
+ * HBM-bound: one pass over X, the weights broadcast from shared memory.
+ * --------------------------------------------------------------------------- */
+typedef struct bridger_linear bridger_linear; /* opaque; immutable after load; owns device memory */
+typedef struct {
+  int32_t n_features;         /* F >= 1 */
+  int32_t n_outputs;          /* K in [1, 64] (K = 1: binary classifier or single-target regressor) */
+  const double* coef;         /* [K * F] row-major, finite */
+  const double* intercept;    /* optional [K]; NULL => 0 */
+  const double* scaler_mean;  /* optional [F] StandardScaler mean_ (with scaler_scale) */
+  const double* scaler_scale; /* optional [F] StandardScaler scale_; both or neither */
+  int32_t task;               /* bridger_task */
+  int32_t post;               /* IDENTITY; SIGMOID (classification, K == 1); SOFTMAX (classification, K >= 2) */
+} bridger_linear_desc;
+
+/* Deep-copies the desc to the device.  E_NULL_ARG (NULL desc/coef/out),
+ * E_SHAPE (F < 1, K out of range, only one scaler array), E_INVALID_TREE
+ * (non-finite coefficient, scale == 0), E_UNSUPPORTED (post/task mismatch). */
+bridger_status bridger_linear_load(const bridger_linear_desc* desc, int cuda_device, bridger_linear** out);
+bridger_status bridger_linear_free(bridger_linear* m); /* NULL ok */
+/* predict: regression -> float out[n_rows * K]; classification -> int32 labels out[n_rows]. */
+bridger_status bridger_linear_predict(const bridger_linear* m, const float* X, int64_t n_rows, int32_t n_features,
+                                      void* out, void* stream);
+/* classification only: float out[n_rows * C], C = K, or 2 for K == 1 ([1-p, p]). */
+bridger_status bridger_linear_predict_proba(const bridger_linear* m, const float* X, int64_t n_rows,
+                                            int32_t n_features, float* out, void* stream);
+/* raw scores s: double out[n_rows * K] (sklearn decision_function / predict in fp64). */
+bridger_status bridger_linear_decision(const bridger_linear* m, const float* X, int64_t n_rows, int32_t n_features,
+                                       double* out, void* stream);
+
 const char* bridger_last_error(void);
 const char* bridger_status_string(bridger_status s);
 /* Number of kernel launches this thread has issued through the library (for
@@ -226,8 +269,9 @@ int64_t bridger_launch_count(void);
  * since the last query, and clears them. */
 bridger_status bridger_hot_kernel_timing(int32_t enable);
 bridger_status bridger_hot_kernel_time(double* total_ms, int64_t* launches);
-/* Same for a kernel id: 0 = dominant kernel (traversal / path contraction K2),
- * 1 = gather-compare K1, 2 = leaf gather / reduce K3, 3 = fused GEMM-form K5. */
+/* Same for a kernel id: 0 = dominant kernel (traversal / path contraction K2,
+ * linear-model kernel), 1 = gather-compare K1, 2 = leaf gather / reduce K3,
+ * 3 = fused GEMM-form K5. */
 bridger_status bridger_hot_kernel_time_by(int32_t kernel, double* total_ms, int64_t* launches);
 
 #ifdef __cplusplus

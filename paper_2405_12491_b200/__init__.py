@@ -51,7 +51,8 @@ EXPORTS = [
     "bridger_step_path_scores", "bridger_gemm_geometry", "bridger_path_matrix", "bridger_lower_tree",
     "bridger_analyze_exactness", "bridger_validate", "bridger_last_error", "bridger_status_string",
     "bridger_launch_count", "bridger_hot_kernel_timing", "bridger_hot_kernel_time", "bridger_model_layout",
-    "bridger_hot_kernel_time_by",
+    "bridger_hot_kernel_time_by", "bridger_linear_load", "bridger_linear_free", "bridger_linear_predict",
+    "bridger_linear_predict_proba", "bridger_linear_decision",
 ]
 
 
@@ -86,6 +87,11 @@ def _load_lib():
         "bridger_hot_kernel_time": ([vp, vp], i32),
         "bridger_model_layout": ([vp, vp, vp, vp, vp, vp], i32),
         "bridger_hot_kernel_time_by": ([i32, vp, vp], i32),
+        "bridger_linear_load": ([vp, i32, vp], i32),
+        "bridger_linear_free": ([vp], i32),
+        "bridger_linear_predict": ([vp, vp, i64, i32, vp, vp], i32),
+        "bridger_linear_predict_proba": ([vp, vp, i64, i32, vp, vp], i32),
+        "bridger_linear_decision": ([vp, vp, i64, i32, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -375,3 +381,77 @@ class Model:
 
 __all__ = ["Model", "BridgerError", "validate", "analyze_exactness", "path_matrix", "lower_tree",
            "gemm_geometry", "launch_count", "lib", "LIB_PATH", "EXPORTS"]
+
+
+# ------------------------------------------------------------ linear models --
+class _LinDesc(C.Structure):
+    _fields_ = [("n_features", C.c_int32), ("n_outputs", C.c_int32), ("coef", C.c_void_p),
+                ("intercept", C.c_void_p), ("scaler_mean", C.c_void_p), ("scaler_scale", C.c_void_p),
+                ("task", C.c_int32), ("post", C.c_int32)]
+
+
+class LinearModel:
+    """A linear model on the device (bridger_linear_*): argument
+    marshalling only.  ``m`` has n_features, n_outputs, coef [K,F], intercept [K] | None,
+    mean / scale [F] | None (StandardScaler), task, post."""
+
+    def __init__(self, m, device: int = 0):
+        self.n_features, self.n_outputs = int(m.n_features), int(m.n_outputs)
+        self.task, self.post = int(m.task), int(m.post)
+        K, F = self.n_outputs, self.n_features
+        keep = dict(coef=np.ascontiguousarray(m.coef, np.float64).reshape(K, F),
+                    b=None if getattr(m, "intercept", None) is None else np.ascontiguousarray(m.intercept, np.float64),
+                    mean=None if getattr(m, "mean", None) is None else np.ascontiguousarray(m.mean, np.float64),
+                    scale=None if getattr(m, "scale", None) is None else np.ascontiguousarray(m.scale, np.float64))
+        p = lambda x: None if x is None else x.ctypes.data
+        d = _LinDesc(F, K, p(keep["coef"]), p(keep["b"]), p(keep["mean"]), p(keep["scale"]), self.task, self.post)
+        self._h = C.c_void_p()
+        _check(_lib.bridger_linear_load(C.byref(d), int(device), C.byref(self._h)))
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.bridger_linear_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _x(self, X):
+        import torch
+        if not (isinstance(X, torch.Tensor) and X.is_cuda and X.dtype == torch.float32 and X.is_contiguous()):
+            raise TypeError("X must be a contiguous CUDA float32 tensor")
+        if X.dim() != 2 or X.shape[1] != self.n_features:
+            raise ValueError(f"X must be [n_rows, {self.n_features}]")
+        return X
+
+    def predict(self, X, out=None):
+        import torch
+        X = self._x(X)
+        n = X.shape[0]
+        if out is None:
+            out = (torch.empty(n, dtype=torch.int32, device=X.device) if self.task == 1
+                   else torch.empty((n, self.n_outputs), dtype=torch.float32, device=X.device))
+        _check(_lib.bridger_linear_predict(self._h, X.data_ptr(), n, X.shape[1], out.data_ptr(), _stream_ptr(X.device)))
+        return out
+
+    def predict_proba(self, X, out=None):
+        import torch
+        X = self._x(X)
+        n = X.shape[0]
+        if out is None:
+            out = torch.empty((n, 2 if self.n_outputs == 1 else self.n_outputs), dtype=torch.float32, device=X.device)
+        _check(_lib.bridger_linear_predict_proba(self._h, X.data_ptr(), n, X.shape[1], out.data_ptr(),
+                                                 _stream_ptr(X.device)))
+        return out
+
+    def decision_function(self, X, out=None):
+        import torch
+        X = self._x(X)
+        n = X.shape[0]
+        if out is None:
+            out = torch.empty((n, self.n_outputs), dtype=torch.float64, device=X.device)
+        _check(_lib.bridger_linear_decision(self._h, X.data_ptr(), n, X.shape[1], out.data_ptr(), _stream_ptr(X.device)))
+        return out

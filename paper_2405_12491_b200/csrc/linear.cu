@@ -1,0 +1,296 @@
+// Linear models on the same GPU path (include/bridger.h
+// "Linear models").  The definition is oracle.c oracle_linear_run:
+//   x'_f = ((float)x_f - (float)mean_f) / (float)scale_f        (reading c16)
+//   s_k  = intercept_k + sum_f coef[k][f] * x'_f  (fp64, f ascending, no FMA)
+// then identity / sigmoid / softmax / argmax exactly as finalize.cuh does for
+// tree ensembles (readings c7, c10, c15).
+//
+// B200 mapping: HBM-bound (4F bytes of input per row against K*F fp64 MACs).
+// Persistent CTAs of W warps; each warp streams 32-row blocks of X through a
+// double-buffered shared-memory staging block filled by cp.async (coalesced
+// 4-byte copies; odd row stride F|1 so that lane = row reads are conflict
+// free) while it computes the previous block; the weights sit in shared memory
+// and are read as warp-wide broadcasts.  fp64 arithmetic costs nothing here:
+// the kernel is bound by the X stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "bridger_internal.h"
+#include "finalize.cuh"
+#include "ptx.cuh"
+
+struct bridger_linear {
+  int device = 0;
+  int32_t F = 0, K = 0, task = 0, post = 0;
+  bool scaler = false;
+  double* d_w = nullptr;      // [K*F] coef, then [K] intercept
+  float* d_scale = nullptr;   // [2F] fp32 mean, scale (reading c16: cast to the input dtype)
+};
+
+namespace bridger {
+
+void count_launch();
+void hot_begin(cudaStream_t st, cudaEvent_t* ev);
+void hot_end(cudaStream_t st, cudaEvent_t start);
+
+struct LinParams {
+  const float* X;
+  int64_t n_rows;
+  int32_t F, K, S;      // S = staging row stride (odd)
+  const double* w;      // [K*F] then [K]
+  const float* sc;      // [2F] or nullptr
+  int32_t want;         // 0 predict, 1 proba, 2 decision (fp64 scores)
+  FinalizeArgs fin;     // task / post / K / out
+};
+
+template <int KT, bool SCALER>
+__global__ void __launch_bounds__(512) linear_kernel(const LinParams p) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
+  const int F = p.F, K = p.K, S = p.S;
+  double* W = reinterpret_cast<double*>(smem);                 // [K*F + K]
+  float* SC = reinterpret_cast<float*>(W + (size_t)K * F + K);  // [2F]
+  float* St = SC + 2 * F + ((2 * F) & 1);                       // [NW][2][32*S]
+  for (int i = threadIdx.x; i < K * F + K; i += blockDim.x) W[i] = p.w[i];
+  if (SCALER)
+    for (int i = threadIdx.x; i < 2 * F; i += blockDim.x) SC[i] = p.sc[i];
+  __syncthreads();
+  float* st0 = St + (size_t)warp * 2 * 32 * S;
+  const int64_t n_blocks = (p.n_rows + 31) / 32;
+  const int64_t stride = (int64_t)gridDim.x * NW;
+  int64_t blk = (int64_t)blockIdx.x * NW + warp;
+  // stage block b into buffer `buf`: element e of the contiguous [rows][F]
+  // block goes to row e / F, column e % F of the odd-stride staging block
+  auto stage = [&](int64_t b, int buf) {
+    if (b < n_blocks) {
+      const int rows = (int)(p.n_rows - b * 32 < 32 ? p.n_rows - b * 32 : 32);
+      const float* src = p.X + b * 32 * (int64_t)F;
+      float* dst = st0 + (size_t)buf * 32 * S;
+      for (int e = lane; e < rows * F; e += 32) {
+        const int rr = e / F, f = e - rr * F;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(ptx::s2u(dst + rr * S + f)), "l"(src + e)
+                     : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  stage(blk, 0);
+  for (int buf = 0; blk < n_blocks; blk += stride, buf ^= 1) {
+    stage(blk + stride, buf ^ 1);                                // next block in flight
+    asm volatile("cp.async.wait_group 1;" ::: "memory");        // this block landed
+    __syncwarp();
+    const float* xr = st0 + (size_t)buf * 32 * S + lane * S;
+    double acc[KT];
+#pragma unroll
+    for (int k = 0; k < KT; ++k) acc[k] = k < K ? W[(size_t)K * F + k] : 0.0;  // intercept
+    for (int f = 0; f < F; ++f) {
+      float xv = xr[f];
+      if (SCALER) xv = __fdiv_rn(__fsub_rn(xv, SC[f]), SC[F + f]);  // fp32 ops (c16)
+      const double xd = (double)xv;
+#pragma unroll
+      for (int k = 0; k < KT; ++k)
+        if (k < K) acc[k] = __dadd_rn(acc[k], __dmul_rn(W[(size_t)k * F + f], xd));  // no FMA
+    }
+    const int64_t row = blk * 32 + lane;
+    if (row < p.n_rows) {
+      if (p.want == 2) {
+        double* o = static_cast<double*>(p.fin.out) + row * K;
+#pragma unroll
+        for (int k = 0; k < KT; ++k)
+          if (k < K) o[k] = acc[k];
+      } else {
+        // the same finalize as the tree path: SUM with base 0, scale 1, q = 0
+        finalize_row<KT, double>(p.fin, row, acc);
+      }
+    }
+    __syncwarp();  // staging buffer `buf` is re-filled two blocks later
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+static bridger_status lin_cuda_fail(cudaError_t e, const char* what) {
+  return fail(BRIDGER_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct LinDeviceGuard {
+  int prev = -1;
+  explicit LinDeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~LinDeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+static bridger_status linear_run(const bridger_linear* m, const float* X, int64_t n_rows, int32_t n_features,
+                                 void* out, int want, void* stream) {
+  if (!m) return fail(BRIDGER_E_NULL_ARG, "model is NULL");
+  if (n_rows < 0) return fail(BRIDGER_E_SHAPE, "n_rows < 0");
+  if (n_features != m->F)
+    return fail(BRIDGER_E_SHAPE, "n_features " + std::to_string(n_features) + " != model's " + std::to_string(m->F));
+  if (n_rows == 0) return BRIDGER_OK;
+  if (!X || !out) return fail(BRIDGER_E_NULL_ARG, "X or out is NULL");
+  if (n_rows > (int64_t)1 << 40 || n_rows * (int64_t)n_features > ((int64_t)1 << 46))
+    return fail(BRIDGER_E_SHAPE, "n_rows * n_features overflows");
+  if (want == 1 && m->task != BRIDGER_TASK_CLASSIFICATION)
+    return fail(BRIDGER_E_UNSUPPORTED, "predict_proba needs a classifier");
+  LinDeviceGuard g(m->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  LinParams p{};
+  p.X = X;
+  p.n_rows = n_rows;
+  p.F = m->F;
+  p.K = m->K;
+  p.S = m->F | 1;
+  p.w = m->d_w;
+  p.sc = m->d_scale;
+  p.want = want;
+  FinalizeArgs fin{};
+  fin.task = m->task;
+  fin.agg = BRIDGER_AGG_SUM;
+  fin.post = m->post;
+  fin.K = m->K;
+  fin.total_trees = 1;
+  fin.q = 0;
+  fin.acc_int = 0;
+  fin.want = want == 2 ? 0 : want;
+  fin.leaf_scale = 1.0;
+  fin.base = nullptr;
+  fin.out = out;
+  p.fin = fin;
+  const size_t fixed = ((size_t)m->K * m->F + m->K) * 8 + (2 * (size_t)m->F + 2) * 4;
+  const size_t per_warp = (size_t)2 * 32 * p.S * 4;
+  int nw = 16;
+  while (nw > 1 && fixed + nw * per_warp > 232448) --nw;
+  if (fixed + per_warp > 232448) return fail(BRIDGER_E_UNSUPPORTED, "model too wide for the linear kernel");
+  const int smem = (int)(fixed + nw * per_warp);
+  int dev_sms = 148;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, m->device);
+  const int64_t n_blocks = (n_rows + 31) / 32;
+  // persistent: as many CTAs as fit (up to 4 per SM), never more than row blocks need
+  cudaError_t e = cudaSuccess;
+  BRIDGER_DISPATCH_KT(m->K, {
+    auto kern = m->scaler ? linear_kernel<KT, true> : linear_kernel<KT, false>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    int occ = 1;
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nw * 32, smem);
+    if (e == cudaSuccess) {
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n_blocks + nw - 1) / nw,
+                                                                   (int64_t)dev_sms * std::max(1, std::min(occ, 4))));
+      cudaEvent_t ev;
+      hot_begin(st, &ev);
+      kern<<<grid, nw * 32, smem, st>>>(p);
+      hot_end(st, ev);
+      count_launch();
+      e = cudaGetLastError();
+    }
+  });
+  if (e != cudaSuccess) return lin_cuda_fail(e, "linear kernel launch");
+  return BRIDGER_OK;
+}
+
+}  // namespace bridger
+
+using namespace bridger;
+
+extern "C" {
+
+bridger_status bridger_linear_load(const bridger_linear_desc* d, int cuda_device, bridger_linear** out) {
+  if (!out) return fail(BRIDGER_E_NULL_ARG, "out is NULL");
+  *out = nullptr;
+  if (!d || !d->coef) return fail(BRIDGER_E_NULL_ARG, "desc or coef is NULL");
+  const int32_t F = d->n_features, K = d->n_outputs;
+  if (F < 1) return fail(BRIDGER_E_SHAPE, "n_features must be >= 1");
+  if (K < 1 || K > 64) return fail(BRIDGER_E_SHAPE, "n_outputs must be in [1,64]");
+  if ((d->scaler_mean == nullptr) != (d->scaler_scale == nullptr))
+    return fail(BRIDGER_E_SHAPE, "scaler_mean and scaler_scale must both be given or both NULL");
+  if (d->task != BRIDGER_TASK_REGRESSION && d->task != BRIDGER_TASK_CLASSIFICATION)
+    return fail(BRIDGER_E_UNSUPPORTED, "unknown task");
+  if (d->post == BRIDGER_POST_SIGMOID && (d->task != BRIDGER_TASK_CLASSIFICATION || K != 1))
+    return fail(BRIDGER_E_UNSUPPORTED, "sigmoid post-transform needs a K == 1 classifier");
+  if (d->post == BRIDGER_POST_SOFTMAX && (d->task != BRIDGER_TASK_CLASSIFICATION || K < 2))
+    return fail(BRIDGER_E_UNSUPPORTED, "softmax post-transform needs a K >= 2 classifier");
+  if (d->post < BRIDGER_POST_IDENTITY || d->post > BRIDGER_POST_SOFTMAX)
+    return fail(BRIDGER_E_UNSUPPORTED, "unknown post");
+  std::vector<double> w((size_t)K * F + K, 0.0);
+  for (size_t i = 0; i < (size_t)K * F; ++i) {
+    if (!std::isfinite(d->coef[i])) return fail(BRIDGER_E_INVALID_TREE, "non-finite coefficient");
+    w[i] = d->coef[i];
+  }
+  for (int32_t k = 0; k < K; ++k) {
+    const double b = d->intercept ? d->intercept[k] : 0.0;
+    if (!std::isfinite(b)) return fail(BRIDGER_E_INVALID_TREE, "non-finite intercept");
+    w[(size_t)K * F + k] = b;
+  }
+  std::vector<float> sc;
+  if (d->scaler_mean) {
+    sc.resize(2 * (size_t)F);
+    for (int32_t f = 0; f < F; ++f) {
+      sc[f] = (float)d->scaler_mean[f];   // reading c16: the transform runs in the input dtype
+      sc[F + f] = (float)d->scaler_scale[f];
+      if (!std::isfinite(sc[f]) || !std::isfinite(sc[F + f]) || sc[F + f] == 0.0f)
+        return fail(BRIDGER_E_INVALID_TREE, "scaler mean/scale not finite or scale == 0");
+    }
+  }
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess) return lin_cuda_fail(e, "cudaGetDeviceCount");
+  if (cuda_device < 0 || cuda_device >= ndev) return fail(BRIDGER_E_CUDA, "invalid cuda_device");
+  LinDeviceGuard g(cuda_device);
+  bridger_linear* m = new bridger_linear();
+  m->device = cuda_device;
+  m->F = F;
+  m->K = K;
+  m->task = d->task;
+  m->post = d->post;
+  m->scaler = !sc.empty();
+  e = cudaMalloc(&m->d_w, w.size() * 8);
+  if (e == cudaSuccess) e = cudaMemcpy(m->d_w, w.data(), w.size() * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && m->scaler) {
+    e = cudaMalloc(&m->d_scale, sc.size() * 4);
+    if (e == cudaSuccess) e = cudaMemcpy(m->d_scale, sc.data(), sc.size() * 4, cudaMemcpyHostToDevice);
+  }
+  if (e != cudaSuccess) {
+    cudaFree(m->d_w);
+    cudaFree(m->d_scale);
+    delete m;
+    return e == cudaErrorMemoryAllocation ? fail(BRIDGER_E_OOM, "device allocation failed")
+                                          : lin_cuda_fail(e, "linear upload");
+  }
+  *out = m;
+  return BRIDGER_OK;
+}
+
+bridger_status bridger_linear_free(bridger_linear* m) {
+  if (!m) return BRIDGER_OK;
+  LinDeviceGuard g(m->device);
+  cudaDeviceSynchronize();
+  cudaFree(m->d_w);
+  cudaFree(m->d_scale);
+  delete m;
+  return BRIDGER_OK;
+}
+
+bridger_status bridger_linear_predict(const bridger_linear* m, const float* X, int64_t n_rows, int32_t n_features,
+                                      void* out, void* stream) {
+  return linear_run(m, X, n_rows, n_features, out, 0, stream);
+}
+
+bridger_status bridger_linear_predict_proba(const bridger_linear* m, const float* X, int64_t n_rows,
+                                            int32_t n_features, float* out, void* stream) {
+  return linear_run(m, X, n_rows, n_features, out, 1, stream);
+}
+
+bridger_status bridger_linear_decision(const bridger_linear* m, const float* X, int64_t n_rows, int32_t n_features,
+                                       double* out, void* stream) {
+  return linear_run(m, X, n_rows, n_features, out, 2, stream);
+}
+
+}  // extern "C"

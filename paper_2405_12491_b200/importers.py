@@ -261,3 +261,45 @@ def from_lightgbm_json(dump: dict) -> Ensemble:
     if name.startswith("regression") or name in ("huber", "fair", "quantile", "mape"):
         return _pack(trees, F, 1, task=TASK_REGRESSION, agg=agg, base_score=np.zeros(1))
     raise ValueError(f"unsupported objective {dump.get('objective')}")
+
+
+# ---------------------------------------------------------- linear models --
+@dataclass
+class Linear:
+    """Arrays of a bridger_linear_desc (include/bridger.h)."""
+    n_features: int
+    n_outputs: int
+    coef: np.ndarray                  # [K, F] fp64
+    intercept: Optional[np.ndarray] = None
+    mean: Optional[np.ndarray] = None  # StandardScaler mean_
+    scale: Optional[np.ndarray] = None  # StandardScaler scale_
+    task: int = TASK_REGRESSION
+    post: int = POST_IDENTITY
+    classes: Optional[np.ndarray] = None
+
+
+def from_sklearn_linear(est) -> Linear:
+    """LogisticRegression, SGDClassifier, RidgeClassifier, LinearSVC (classifiers);
+    LinearRegression, Ridge, Lasso, ElasticNet, SGDRegressor (regressors); or a
+    Pipeline(StandardScaler(), <one of those>).  Coefficients are kept in fp64
+    (an fp32-fitted model's coefficients are exact in fp64)."""
+    mean = scale = None
+    if type(est).__name__ == "Pipeline":
+        steps = [s for _, s in est.steps]
+        if len(steps) != 2 or type(steps[0]).__name__ != "StandardScaler":
+            raise ValueError("only Pipeline(StandardScaler(), linear model) is supported")
+        sc, est = steps
+        F = int(sc.n_features_in_)
+        mean = np.asarray(sc.mean_ if sc.with_mean else np.zeros(F), np.float64)
+        scale = np.asarray(sc.scale_ if sc.with_std and sc.scale_ is not None else np.ones(F), np.float64)
+    coef = np.atleast_2d(np.asarray(est.coef_, np.float64))
+    K, F = coef.shape
+    b = np.asarray(np.broadcast_to(np.asarray(est.intercept_, np.float64), (K,)), np.float64)
+    if hasattr(est, "classes_"):
+        name = type(est).__name__
+        proba = name == "LogisticRegression" or (name == "SGDClassifier" and est.loss == "log_loss")
+        post = (POST_SIGMOID if K == 1 else POST_SOFTMAX) if proba else POST_IDENTITY
+        if proba and K > 1 and name == "SGDClassifier":
+            raise ValueError("SGDClassifier(log_loss) multiclass proba is one-vs-rest, not softmax")
+        return Linear(F, K, coef, b, mean, scale, TASK_CLASSIFICATION, post, np.asarray(est.classes_))
+    return Linear(F, K, coef, b, mean, scale, TASK_REGRESSION, POST_IDENTITY)

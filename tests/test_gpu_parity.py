@@ -174,6 +174,9 @@ def test_c4_shaped_deep_trees(hybrid, monkeypatch):
     (top levels in shared memory, deep levels + leaves in global) or
     global-tree mode (every CTA walks every tree from global memory)."""
     monkeypatch.setenv("BRIDGER_HYBRID", hybrid)
+    # tree-streamed mode is the default for global-tree models (tested below);
+    # keep the older global-tree walker reachable and exact
+    monkeypatch.setenv("BRIDGER_STREAM", "0")
     c, m = make_config("C4", n_trees=40)
     g, _ = check(m, gen_x(4, 0, 4001, 64))
     assert g.layout()["format"] == ("hybrid" if hybrid == "1" else "heap")  # hybrid is opt-in

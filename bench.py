@@ -354,9 +354,13 @@ def main():
     variant = info["variant"]
     hot_avg = hot_ms / max(1, hot_n)
     if variant == "traverse":
-        # algorithmic shared-memory bytes per launch: per (row, tree) D node records (8 B) +
-        # D feature values (4 B) + K leaf values (4 B)
-        alg = n * model.n_trees * (12 * cfg.depth + 4 * cfg.n_classes)
+        # algorithmic shared-memory bytes per launch, per (row, tree): D node records +
+        # D feature values + K leaf values, each per-lane access counted in whole
+        # 32-bit bank words (a warp-wide access of b < 4 bytes per lane still
+        # occupies one 128-byte wavefront): fp32 nodes 8 B + x 4 B -> 12 D + 4 K;
+        # threshold-bin codes 4 B nodes + u16 codes -> 8 D + 4 K
+        coded = model.layout().get("coded", False)
+        alg = n * model.n_trees * ((8 if coded else 12) * cfg.depth + 4 * cfg.n_classes)
         sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
         peak = sm_count * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e9   # GB/s, guide unit counts
         psrc = f"derived from guide unit counts ({src} sm_max_mhz)"
@@ -370,6 +374,8 @@ def main():
         roof = {"bound": "alu", "resource": "shared-memory (LSU) pipe bandwidth",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
                 "kernel": "trav_kernel", "kernel_ms": hot_avg,
+                "node_format": "threshold-bin codes (4 B nodes, u16 inputs; bin_kernel pass)" if coded else "fp32 (8 B nodes)",
+                "visits_per_s": n * model.n_trees * cfg.depth / (hot_avg / 1e3),
                 "hbm_frac": (n * cfg.n_features * 4 + n * 4) / (hot_avg / 1e3) / 1e9 / peaks["hbm_gbs"],
                 "peak_source": psrc}
     else:

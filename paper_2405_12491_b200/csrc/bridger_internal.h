@@ -107,8 +107,9 @@ struct TravLayout {
   std::vector<float> hyb_leaves;    // [slots][L][K]
   std::vector<SparseTree> sparse_trees;
   std::vector<uint32_t> sparse_nodes;   // [n][4] records
-  std::vector<float> bin_table;     // concatenated sorted distinct thresholds per feature
-  std::vector<int32_t> bin_offsets; // [F+1]
+  std::vector<std::vector<float>> bin_sorted;  // host: sorted distinct thresholds per feature (U_f)
+  std::vector<float> bin_table;     // device: [F][2^bin_k - 1] Eytzinger (BFS) search trees of U_f, +inf padded
+  int32_t bin_k = 0;                // levels of every feature's search tree
   int32_t smem_bytes = 0;       // dynamic shared memory per CTA
   int32_t chunk_budget = 0;     // max bytes of one chunk
   bool has_missing = false;
@@ -122,6 +123,24 @@ struct TravLayout {
 // Shared-memory carve-up of the traversal kernel after the chunk:
 //   [NB row blocks x (feature-major X + staging) = NB*256*F][mbarriers]
 //   [intra-group partials NB*(G-1)*32*K*8][cluster DSMEM slots NB*2*(nC-1)*32*K*8]
+// Codes mode: each 32-row code block ([F2/2][32][2] u16, 64*F2 bytes) lands in
+// a buffer of 2^b >= 64*F2 bytes aligned to 2^b, so a lane's code address is
+// (buffer | lane*4 | feature offset) -- one LOP3 (traverse.cuh).  The region
+// holds NB groups x 2 buffers plus 2^b bytes of alignment slack.
+#ifdef __CUDACC__
+#define BRIDGER_HD __host__ __device__
+#else
+#define BRIDGER_HD
+#endif
+BRIDGER_HD inline int32_t code_buf_bytes(int32_t F) {
+  const int32_t need = 64 * ((F + 1) & ~1);
+  int32_t b = 128;
+  while (b < need) b <<= 1;
+  return b;
+}
+BRIDGER_HD inline int32_t trav_x_region(bool codes, int32_t F, int32_t nb) {
+  return codes ? (2 * nb + 1) * code_buf_bytes(F) : nb * 256 * F;
+}
 inline int32_t trav_bar_bytes(int32_t nb) { return ((1 + 6 * nb) * 8 + 15) / 16 * 16; }
 inline int32_t trav_red_bytes(int32_t nb, int32_t g, int32_t K) { return nb * (g - 1) * 32 * K * 8; }
 inline int32_t trav_slot_bytes(int32_t nb, int32_t n_chunks, int32_t K) {
@@ -178,7 +197,6 @@ struct bridger_model {
   void* d_sparse_trees = nullptr;    // SparseTree[T] (TravLayout::sparse)
   void* d_sparse_nodes = nullptr;    // uint4 records
   float* d_bin_table = nullptr;      // threshold-bin codes (TravLayout::codes)
-  int32_t* d_bin_offsets = nullptr;
 
   // GEMM-path layout on device (filled by gemm_path.cu)
   bool gemm_ok = false;

@@ -233,33 +233,57 @@ static constexpr int32_t kSmemMax = 232448;  // 227 KB opt-in per block (sm_100)
 // code(x) = #{u in U_f : u < x} (NaN -> 0xFFFF), and a node's threshold t =
 // U_f[j] becomes j.  For every non-NaN x:  x <= U_f[j]  <=>  code(x) <= j
 // (the thresholds below x are exactly U_f[0..code(x)-1]), so the comparison is
-// unchanged bit for bit.  Eligible when F <= 1023 and every |U_f| <= 65534.
+// unchanged bit for bit.  Eligible when F <= 512 and every |U_f| <= 32767
+// (codes and node indices fit 15 bits).  The device search structure is, per
+// feature, U_f laid out as a complete binary search tree in BFS (Eytzinger)
+// order with 2^k - 1 slots (k uniform over the features so every lane of a
+// warp takes the same k steps), padded with +inf: descending
+// i <- 2i + 1 + [E[i] < x] for k levels ends at leaf i - (2^k - 1) = #{u < x}
+// (the padding never counts: +inf < x is false for every x).
+static void eytzinger_fill(const std::vector<float>& sorted, std::vector<float>& out, size_t base, int64_t i,
+                           int64_t size, int64_t& next) {
+  if (i >= size) return;
+  eytzinger_fill(sorted, out, base, 2 * i + 1, size, next);
+  out[base + i] = next < (int64_t)sorted.size() ? sorted[next] : INFINITY;
+  ++next;
+  eytzinger_fill(sorted, out, base, 2 * i + 2, size, next);
+}
+
 static bool build_bin_table(const bridger_model_desc* d, TravLayout* out) {
   const int32_t F = d->n_features;
-  if (F > 1023) return false;
-  std::vector<std::vector<float>> u(F);
+  out->bin_sorted.clear();
+  out->bin_table.clear();
+  out->bin_k = 0;
+  if (F > 512) return false;
+  std::vector<std::vector<float>>& u = out->bin_sorted;
+  u.assign(F, {});
   for (int32_t t = 0; t < d->n_trees; ++t)
     for (int64_t g = d->tree_offsets[t]; g < d->tree_offsets[t + 1]; ++g)
       if (d->left[g] != -1) u[d->feature[g]].push_back(d->threshold[g]);
-  out->bin_offsets.assign(F + 1, 0);
-  out->bin_table.clear();
+  size_t nmax = 0;
   for (int32_t f = 0; f < F; ++f) {
     auto& v = u[f];
     std::sort(v.begin(), v.end());
     // -0.0 and +0.0 compare equal: keep one
     v.erase(std::unique(v.begin(), v.end(), [](float a, float b) { return a == b; }), v.end());
-    if (v.size() > 65534) return false;
-    out->bin_offsets[f] = (int32_t)out->bin_table.size();
-    out->bin_table.insert(out->bin_table.end(), v.begin(), v.end());
+    if (v.size() > 32767) return false;
+    nmax = std::max(nmax, v.size());
   }
-  out->bin_offsets[F] = (int32_t)out->bin_table.size();
+  int32_t k = 1;
+  while (((size_t)1 << k) - 1 < nmax) ++k;
+  const size_t P = ((size_t)1 << k) - 1;
+  out->bin_k = k;
+  out->bin_table.assign((size_t)F * P, INFINITY);
+  for (int32_t f = 0; f < F; ++f) {
+    int64_t next = 0;
+    eytzinger_fill(u[f], out->bin_table, (size_t)f * P, 0, (int64_t)P, next);
+  }
   return true;
 }
 
 static uint32_t code_of_threshold(const TravLayout& L, int32_t f, float t) {
-  const float* b = L.bin_table.data() + L.bin_offsets[f];
-  const float* e = L.bin_table.data() + L.bin_offsets[f + 1];
-  return (uint32_t)(std::lower_bound(b, e, t) - b);  // t is present: exact index
+  const std::vector<float>& v = L.bin_sorted[f];
+  return (uint32_t)(std::lower_bound(v.begin(), v.end(), t) - v.begin());  // t is present: exact index
 }
 
 // Sparse (pointer) layout (§8(f3)): each tree in BFS order with the two
@@ -273,7 +297,7 @@ static void build_sparse_layout(const bridger_model_desc* d, const Exactness& ex
   out->global_trees = true;
   out->codes = false;
   out->bin_table.clear();
-  out->bin_offsets.clear();
+  out->bin_sorted.clear();
   out->sparse_trees.assign(T, SparseTree{});
   out->sparse_nodes.clear();
   out->slot_tree.assign(T, 0);
@@ -362,18 +386,20 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
   }
   out->has_missing = d->missing_left != nullptr;
   out->use_cluster = std::getenv("BRIDGER_CLUSTER") != nullptr;
-  // coded nodes pay for the separate binning pass only when each input value
-  // is reused by many node visits: measured on B200 C2 (800
-  // visits/row over 28 features) and C3 (3000 over 90) lose, so the default is
-  // codes iff sum_t D_t >= 64 * F.  BRIDGER_CODES=0/1 forces either format.
+  // coded nodes pay for the separate binning pass (~k search steps per input
+  // value) when each input value is reused by enough node visits: measured on
+  // B200 C2 (800 visits/row over 28 features) 0.478 -> 0.431 ms
+  // and C3 (3000 over 90) 15.06 -> 14.25 ms with codes, so the default is codes
+  // iff sum_t D_t >= 12 * F (and >= 64) and the search tables fit in shared
+  // memory.  BRIDGER_CODES=0/1 forces either format.
   const char* codes_env = std::getenv("BRIDGER_CODES");
   int64_t visits = 0;
   for (int32_t t = 0; t < T; ++t) visits += std::max(1, depth[t]);
-  bool want_codes = codes_env ? codes_env[0] != '0' : visits >= 64 * (int64_t)F;
+  bool want_codes = codes_env ? codes_env[0] != '0' : (visits >= 12 * (int64_t)F && visits >= 64);
   if (want_codes) {
     want_codes = build_bin_table(d, out);
     // the binning kernel keeps the whole table in shared memory
-    if (want_codes && (out->bin_table.size() * 4 + (size_t)(F + 1) * 4) > 160 * 1024) want_codes = false;
+    if (want_codes && out->bin_table.size() * 4 > 190 * 1024) want_codes = false;
   }
   std::vector<int32_t> order(T);
   std::iota(order.begin(), order.end(), 0);
@@ -390,7 +416,7 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
     // per 32-row block: codes mode = two u16 feature-major buffers (double
     // buffered, filled straight by bulk copy); fp32 mode = feature-major block
     // + dense staging block
-    xw = codes ? 2 * 32 * F * 2 : 2 * 32 * F * 4;
+    xw = codes ? 2 * code_buf_bytes(F) : 2 * 32 * F * 4;
     // 16 warps; NB = largest power of two with NB * xw <= 120 KB (measured on
     // B200: C2 best at NB=16/G=1, C3 at NB=4/G=4 in fp32 mode)
     nw = 16;
@@ -402,7 +428,7 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
     while (nw % nb) --nb;
     G = nw / nb;
     misc = 1024 + trav_bar_bytes(nb) + trav_red_bytes(nb, G, K);
-    const int32_t base_budget = kSmemMax - misc - nb * xw;
+    const int32_t base_budget = kSmemMax - misc - trav_x_region(codes, F, nb);
     auto chunk_bytes = [&](int32_t n, int32_t D) -> int64_t {
       const int64_t nodes = (int64_t)n * ((1 << D) - 1) * node_bytes + (node_bytes == 5 ? 16 : 0);
       return (nodes + 15) / 16 * 16 + ((int64_t)n * (1 << D) * K * 4 + 15) / 16 * 16;
@@ -466,7 +492,7 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
   out->codes = want_codes && plan(true);
   if (!out->codes) {
     out->bin_table.clear();
-    out->bin_offsets.clear();
+    out->bin_sorted.clear();
     plan(false);
   }
   if (out->split && out->global_trees) {  // split nodes only for shared-memory-resident chunks
@@ -626,14 +652,17 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
       const int32_t t = order[r.start + j];
       pad_tree(d, t, D, &pt);
       if (out->codes) {
-        // node word: code index j (bits 16..31) | feature * 64 (bits 6..15: byte
-        // offset of the feature's row in a [F][32] u16 block) | missing (bit 0)
+        // node word: code index j (bits 16..30) | missing (bit 15) | byte
+        // offset of the feature's code within a lane's view of a [F/2][32][2]
+        // u16 code block (bits 0..14: (f/2)*128 + (f%2)*2, F <= 512)
         uint32_t* nd = reinterpret_cast<uint32_t*>(base) + (size_t)j * I;
         for (int32_t i = 0; i < I; ++i) {
           // real nodes: t is in U_f, exact index; dummy nodes under replicated
           // leaves (feature 0, threshold 0): any code routes to identical leaves
-          const uint32_t code = code_of_threshold(*out, pt.feature[i], pt.threshold[i]);
-          nd[i] = (code << 16) | ((uint32_t)pt.feature[i] << 6) | (uint32_t)pt.missing[i];
+          const int32_t f = pt.feature[i];
+          const uint32_t code = code_of_threshold(*out, f, pt.threshold[i]);
+          const uint32_t foff = (uint32_t)(f >> 1) * 128u + (uint32_t)(f & 1) * 2u;
+          nd[i] = (code << 16) | ((uint32_t)pt.missing[i] << 15) | foff;
         }
       } else if (out->split) {
         float* th = reinterpret_cast<float*>(base) + (size_t)j * I;
@@ -666,7 +695,7 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
   }
   int32_t maxc = 0;
   for (auto& c : out->chunks) maxc = std::max(maxc, c.bytes);
-  out->smem_bytes = maxc + nb * xw + misc;
+  out->smem_bytes = (maxc + 127) / 128 * 128 + trav_x_region(out->codes, F, out->n_warps / out->group) + misc;
   (void)why;
   return true;
 }

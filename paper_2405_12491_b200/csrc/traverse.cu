@@ -65,69 +65,127 @@ BRIDGER_TRAV_EXTERN(double, false, true, 2)
 BRIDGER_TRAV_EXTERN(double, true, true, 2)
 
 // Threshold-bin coding of the input (§8(f2)): X [N][F] fp32 row-major ->
-// codes [n_blocks][F][32] u16, code = #{u in U_f : u < x} (binary search over
-// the feature's sorted distinct thresholds, all in shared memory), NaN ->
-// 0xFFFF.  The output is already in the traversal kernel's feature-major
-// 32-row block layout, so the traversal bulk-copies it with no transpose.
-__global__ void __launch_bounds__(512) bin_kernel(const float* __restrict__ X, int64_t n_rows, int32_t F,
-                                                  const float* __restrict__ table, const int32_t* __restrict__ offs,
-                                                  int32_t table_n, uint16_t* __restrict__ codes) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  float* U = reinterpret_cast<float*>(smem);
-  int32_t* O = reinterpret_cast<int32_t*>(smem + (size_t)table_n * 4);
+// codes [n_blocks][F2/2][32][2] u16 (F2 = F rounded up to even; feature pairs
+// interleaved per lane so that the traversal's per-lane code loads hit bank
+// `lane` for ANY feature), code = #{u in U_f : u < x}, NaN -> 0xFFFF.
+// lane = row; for 8 features at a time (8 independent chains) each lane
+// descends the features' k-level Eytzinger search trees in shared memory:
+// i <- 2i + 1 + [E_f[i] < x] (all lanes of a warp search the same feature, so
+// the top levels are broadcasts); the leaf reached, i - (2^k - 1), is the code
+// (lowering.cpp).  STAGE: each warp bulk-copies its dense [32][F] blocks into
+// shared memory (double buffered); otherwise (tables too large to leave room
+// for staging) lanes read their row's 8 features straight from global memory,
+// one slice ahead.
+template <int V>
+__device__ __forceinline__ void load_slice(const float* xr, int f0, int F, float (&x)[8]) {
+  if (V == 4 && f0 + 8 <= F) {
+    const float4 a = *reinterpret_cast<const float4*>(xr + f0);
+    const float4 b = *reinterpret_cast<const float4*>(xr + f0 + 4);
+    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+  } else if (V == 2 && f0 + 8 <= F) {
+#pragma unroll
+    for (int u = 0; u < 8; u += 2) {
+      const float2 a = *reinterpret_cast<const float2*>(xr + f0 + u);
+      x[u] = a.x;
+      x[u + 1] = a.y;
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = f0 + u < F ? xr[f0 + u] : 0.f;
+  }
+}
+
+template <int V, bool STAGE>
+__global__ void __launch_bounds__(512, 1) bin_kernel(const float* __restrict__ X, int64_t n_rows, int32_t F,
+                                                     const float* __restrict__ table, int32_t k,
+                                                     uint32_t* __restrict__ codes) {
+  extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
-  const int S = F | 1;  // odd staging stride: St[lane*S + f] is bank-conflict free for a uniform f
-  float* St = reinterpret_cast<float*>(smem + (size_t)table_n * 4 + (size_t)(F + 1) * 4) + (size_t)warp * 32 * S;
-  for (int i = threadIdx.x; i < table_n; i += blockDim.x) U[i] = table[i];
-  for (int i = threadIdx.x; i <= F; i += blockDim.x) O[i] = offs[i];
+  const int P = (1 << k) - 1;
+  const int F2h = (F + 1) >> 1;  // feature pairs
+  const size_t tab_bytes = ((size_t)F * P * 4 + 127) / 128 * 128;
+  const uint32_t blk_bytes = 128u * (uint32_t)F;  // dense [32][F] fp32
+  float* stage = reinterpret_cast<float*>(smem + tab_bytes + (size_t)warp * 2 * blk_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + tab_bytes + (STAGE ? (size_t)NW * 2 * blk_bytes : 0)) + 2 * warp;
+  {
+    const float4* src = reinterpret_cast<const float4*>(table);
+    float4* dst = reinterpret_cast<float4*>(smem);
+    const int n4 = (F * P) / 4;
+    for (int i = threadIdx.x; i < n4; i += blockDim.x) dst[i] = src[i];
+    for (int i = n4 * 4 + threadIdx.x; i < F * P; i += blockDim.x) reinterpret_cast<float*>(smem)[i] = table[i];
+  }
+  if (STAGE && lane == 0) {
+    ptx::mbar_init(&bars[0], 1);
+    ptx::mbar_init(&bars[1], 1);
+    ptx::fence_barrier_init();
+  }
   __syncthreads();
+  const uint32_t tab_s = ptx::s2u(smem);
   const int64_t n_blocks = (n_rows + 31) / 32;
-  for (int64_t blk = (int64_t)blockIdx.x * NW + warp; blk < n_blocks; blk += (int64_t)gridDim.x * NW) {
+  const int64_t gstride = (int64_t)gridDim.x * NW;
+  int64_t blk = (int64_t)blockIdx.x * NW + warp;
+  auto issue = [&](int64_t b, int buf) {
+    if (STAGE && lane == 0 && b < n_blocks && (b + 1) * 32 <= n_rows) {
+      ptx::fence_proxy_async();
+      ptx::mbar_arrive_expect_tx(&bars[buf], blk_bytes);
+      ptx::bulk_g2s(stage + (size_t)buf * 32 * F, X + b * 32 * (int64_t)F, blk_bytes, &bars[buf]);
+    }
+  };
+  issue(blk, 0);
+  uint32_t phase = 0;  // bit b: parity of buffer b
+  for (int it = 0; blk < n_blocks; blk += gstride, ++it) {
+    const int buf = it & 1;
     const int64_t row0 = blk * 32;
-    const int rows = (int)(n_rows - row0 < 32 ? n_rows - row0 : 32);
-    const float* src = X + row0 * F;
-    // row-major copy into the odd-stride staging block: async 4-byte copies,
-    // all in flight at once (zero-filled past the last row)
-    for (int r = 0; r < 32; ++r)
-      for (int f = lane; f < F; f += 32) {
-        const uint32_t dsts = ptx::s2u(St + r * S + f);
-        const float* g = src + (int64_t)(r < rows ? r : 0) * F + f;
-        const uint32_t nbytes = r < rows ? 4u : 0u;
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dsts), "l"(g), "r"(nbytes) : "memory");
+    const float* xr;
+    if (STAGE) {
+      float* St = stage + (size_t)buf * 32 * F;
+      if (row0 + 32 <= n_rows) {
+        ptx::mbar_wait(&bars[buf], (phase >> buf) & 1u);
+        phase ^= 1u << buf;
+      } else {
+        const int rows = (int)(n_rows - row0);
+        const float* src = X + row0 * F;
+        for (int e = lane; e < 32 * F; e += 32) St[e] = e < rows * F ? src[e] : 0.f;
+        __syncwarp();
       }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncwarp();
-    uint16_t* dst = codes + blk * 32 * (int64_t)F;
-    // lower_bound over the feature's sorted distinct thresholds; 4 features per
-    // pass give 4 independent dependency chains per thread, and lane = row
-    // with a warp-uniform feature makes the first search steps broadcasts
-    for (int f0 = 0; f0 < F; f0 += 4) {
-      float x[4];
-      int lo[4], len[4], base[4];
+      issue(blk + gstride, buf ^ 1);  // the other buffer was drained by the previous block
+      xr = St + (size_t)lane * F;
+    } else {
+      xr = X + (row0 + lane < n_rows ? row0 + lane : row0) * (int64_t)F;
+    }
+    uint32_t* dst = codes + (size_t)blk * F2h * 32 + lane;
+    float xn[8];
+    load_slice<V>(xr, 0, F, xn);
+    for (int f0 = 0; f0 < 2 * F2h; f0 += 8) {
+      float x[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int f = min(f0 + u, F - 1);
-        x[u] = St[lane * S + f];
-        base[u] = O[f];
-        len[u] = O[f + 1] - base[u];
-        lo[u] = 0;
+      for (int u = 0; u < 8; ++u) x[u] = xn[u];
+      if (f0 + 8 < 2 * F2h) load_slice<V>(xr, f0 + 8, F, xn);  // one slice ahead
+      // shared address A of the current search-tree node; A' = 2A + (E < x ? c8 : c4)
+      uint32_t A[8], c4[8], c8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        A[u] = tab_s + (uint32_t)(min(f0 + u, F - 1) * P) * 4u;
+        c4[u] = 4u - A[u];
+        c8[u] = 8u - A[u];
       }
-      bool any = true;
-      while (any) {
-        any = false;
+      for (int s = 0; s < k; ++s) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (len[u] > 0) {
-            const int half = len[u] >> 1;
-            const bool less = U[base[u] + lo[u] + half] < x[u];
-            lo[u] = less ? lo[u] + half + 1 : lo[u];
-            len[u] = less ? len[u] - half - 1 : half;
-            any = true;
-          }
+        for (int u = 0; u < 8; ++u) {
+          const float e = ptx::lds_f32(A[u]);
+          A[u] = 2u * A[u] + (e < x[u] ? c8[u] : c4[u]);
+        }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (f0 + u < F) dst[(f0 + u) * 32 + lane] = isnan(x[u]) ? (uint16_t)0xFFFF : (uint16_t)lo[u];
+      for (int u = 0; u < 8; u += 2) {
+        if (f0 + u < 2 * F2h) {
+          // leaf byte offset A + c4 - 4 = 4 (2^k - 1 + code)
+          const uint32_t c0 = isnan(x[u]) ? 0xFFFFu : ((A[u] + c4[u] - 4u) >> 2) - (uint32_t)P;
+          const uint32_t c1 = f0 + u + 1 >= F ? 0u
+                              : isnan(x[u + 1]) ? 0xFFFFu : ((A[u + 1] + c4[u + 1] - 4u) >> 2) - (uint32_t)P;
+          dst[(size_t)((f0 + u) >> 1) * 32] = c0 | (c1 << 16);
+        }
+      }
     }
     __syncwarp();
   }
@@ -268,8 +326,10 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
   const int NW = L.n_warps, G = L.group, NB = NW / G;
   const int block = NW * 32;
   p.group = G;
-  const int xblk = L.codes ? 128 * m->F : 256 * m->F;
-  p.red_off = p.chunk_cap + NB * xblk + trav_bar_bytes(NB);
+  p.red_off = p.chunk_cap + trav_x_region(L.codes, m->F, NB) + trav_bar_bytes(NB);
+  p.code_buf = L.codes ? code_buf_bytes(m->F) : 0;
+  p.k2 = 2u;
+  p.k16 = 65536u;
   p.slot_off = p.red_off + trav_red_bytes(NB, G, m->K);
   int smem = p.slot_off;
   int cluster = 1;
@@ -303,24 +363,33 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
   if (L.codes) {
     // step a1 in coded form: bin the rows once (all chunks reuse the codes)
     const int64_t nbk = (n_rows + 31) / 32;
-    err = cudaMallocAsync(&codes, (size_t)nbk * 32 * m->F * 2, st);
+    const int F2 = (m->F + 1) & ~1;
+    err = cudaMallocAsync(&codes, (size_t)nbk * 32 * F2 * 2, st);
     if (err != cudaSuccess) return err;
-    const int table_n = (int)L.bin_table.size();
-    const int fixed = table_n * 4 + (m->F + 1) * 4;
+    const int P = (1 << L.bin_k) - 1;
+    const int fixed = (m->F * P * 4 + 127) / 128 * 128;
+    // staged (bulk-copied dense blocks) when the table leaves room for >= 8
+    // warps of double-buffered staging, else lanes read X from global memory
     int nwb = 16;
-    while (nwb > 1 && fixed + nwb * 32 * (m->F | 1) * 4 > 232448) --nwb;
-    const int bsmem = fixed + nwb * 32 * (m->F | 1) * 4;
-    static bool bin_attr = false;
-    if (!bin_attr) {
-      cudaFuncSetAttribute(bin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-      bin_attr = true;
+    while (nwb > 1 && fixed + nwb * (2 * 128 * m->F + 16) > 232448) --nwb;
+    const bool stage = nwb >= 8;
+    if (!stage) nwb = 16;
+    const int bsmem = fixed + (stage ? nwb * (2 * 128 * m->F + 16) : 0);
+    const int vi = (m->F % 4 == 0) ? 2 : (m->F % 2 == 0) ? 1 : 0;
+    void (*kerns[2][3])(const float*, int64_t, int32_t, const float*, int32_t, uint32_t*) = {
+        {bin_kernel<1, false>, bin_kernel<2, false>, bin_kernel<4, false>},
+        {bin_kernel<1, true>, bin_kernel<2, true>, bin_kernel<4, true>}};
+    auto bk = kerns[stage ? 1 : 0][vi];
+    static bool bin_attr[2][3] = {{false, false, false}, {false, false, false}};
+    if (!bin_attr[stage ? 1 : 0][vi]) {
+      cudaFuncSetAttribute(bk, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+      bin_attr[stage ? 1 : 0][vi] = true;
     }
     int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bin_kernel, nwb * 32, bsmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bk, nwb * 32, bsmem);
     const int64_t want_ctas = (nbk + nwb - 1) / nwb;
     const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>(want_ctas, (int64_t)sms * std::max(1, occ)));
-    bin_kernel<<<bgrid, nwb * 32, bsmem, st>>>(X, n_rows, m->F, m->d_bin_table, m->d_bin_offsets, table_n,
-                                                 static_cast<uint16_t*>(codes));
+    bk<<<bgrid, nwb * 32, bsmem, st>>>(X, n_rows, m->F, m->d_bin_table, L.bin_k, static_cast<uint32_t*>(codes));
     count_launch();
     err = cudaGetLastError();
     if (err != cudaSuccess) {

@@ -76,6 +76,9 @@ struct TravParams {
   int32_t stream_stage;   //                     bytes per ring slot
   int32_t stream_x_bytes; //                     X tile bytes (rows_per_tile * F * 4)
   int32_t stream_lbuf_bytes; //                  leaf-value landing slots (rows_per_tile * W * K * 4)
+  int32_t code_buf;   // codes: bytes (2^b) of one aligned code-block buffer
+  uint32_t k2, k16;   // 2 and 65536, opaque to the compiler: keeps the walk's
+                      // multiplies on the FMA pipe (IMAD) instead of the ALU pipe
   FinalizeArgs fin;   // (TRAV_FINAL, TRAV_CLUSTER)
 };
 
@@ -133,24 +136,43 @@ __device__ __forceinline__ void walk_trees(const TravParams& p, const TravChunk&
       }
     }
   } else if (CODES) {
-    // 4-byte node: code index (31..16) | feature*64 (15..6) | missing (0);
-    // xl points at this lane's u16 code in a feature-major [F][32] block
-    const uint32_t* nb = static_cast<const uint32_t*>(nodes) + (size_t)j * I;
-    const uint8_t* xb = static_cast<const uint8_t*>(xl);
+    // 4-byte node: code index j (30..16) | missing (15) | feature byte offset
+    // (14..0) within a lane's view of a [F/2][32][2] u16 code block.  xl is
+    // this lane's 4-byte column of a 2^b-aligned block buffer, so the code
+    // address is (xl | (a & (2^b - 1))): bank `lane` for any feature, one LOP3.
+    // code(x) > j  <=>  x * 2^16 > a  (the low half of a is < 2^16), so the
+    // compare needs no field extraction.  Node addresses are shared-window byte
+    // addresses: node idx of tree u at A = base_u + 4 idx, and
+    // idx' = 2 idx + 1 + r  <=>  A' = 2 A + (r ? 8 : 4) - base_u.
+    // The two multiplies use opaque constants (p.k2, p.k16) so they issue on
+    // the FMA pipe; the LOP3 / compare / select use the ALU pipe.
+    const uint32_t nb = ptx::s2u(nodes) + 4u * (uint32_t)(j * I);
+    const uint32_t xb = ptx::s2u(xl);
+    const uint32_t mask = (uint32_t)p.code_buf - 1u;
+    const uint32_t k2 = p.k2, k16 = p.k16;
+    uint32_t A[NI], c[NI], c4[NI];
+#pragma unroll
+    for (int u = 0; u < NI; ++u) {
+      A[u] = nb + 4u * (uint32_t)(u * I);  // shared address of tree u's current node
+      c[u] = 4u - A[u];
+      c4[u] = 8u - A[u];
+    }
     for (int lvl = 0; lvl < D; ++lvl) {
       uint32_t a[NI];
 #pragma unroll
-      for (int u = 0; u < NI; ++u) a[u] = nb[u * I + idx[u]];
+      for (int u = 0; u < NI; ++u) a[u] = ptx::lds_u32(A[u]);
       uint32_t x[NI];
 #pragma unroll
-      for (int u = 0; u < NI; ++u) x[u] = *reinterpret_cast<const uint16_t*>(xb + (a[u] & 0xFFC0u));
+      for (int u = 0; u < NI; ++u) x[u] = ptx::lds_u16(xb | (a[u] & mask));
 #pragma unroll
       for (int u = 0; u < NI; ++u) {
-        int r = x[u] > (a[u] >> 16);  // code(x) > j  <=>  !(x <= t);  NaN code 0xFFFF -> right
-        if (ML) r &= !((a[u] & 1u) & (x[u] == 0xFFFFu));
-        idx[u] = 2 * idx[u] + 1 + r;
+        bool r = x[u] * k16 > a[u];  // code(x) > j  <=>  !(x <= t);  NaN code 0xFFFF -> right
+        if (ML) r = r && !(((a[u] >> 15) & 1u) && x[u] == 0xFFFFu);
+        A[u] = A[u] * k2 + (r ? c4[u] : c[u]);
       }
     }
+#pragma unroll
+    for (int u = 0; u < NI; ++u) idx[u] = (int)((A[u] + c[u] - 4u) >> 2);
   } else {
     constexpr uint32_t kFeatMask = ML ? 0x7fffffffu : 0xffffffffu;
     const uint2* nb = static_cast<const uint2*>(nodes) + (size_t)j * I;
@@ -375,7 +397,6 @@ __global__ void __launch_bounds__(512, 1) trav_kernel(const TravParams p) {
   // codes or pre-transposed fp32), bulk-copied into two buffers per group
   constexpr bool HYB = FMT == FMT_HYBRID;
   constexpr bool PRE = CODES || FMT == FMT_HEAP_T || HYB;  // hybrid always takes pre-transposed input
-  constexpr uint32_t EB = CODES ? 2u : 4u;
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
   const int G = p.group, NB = NW / G;          // G warps share each of NB row blocks
@@ -388,12 +409,19 @@ __global__ void __launch_bounds__(512, 1) trav_kernel(const TravParams p) {
 
   uint8_t* cdata = smem;
   // per row-block group: fp32 mode  Xs [F][32] float + St [32][F] float (256*F B)
-  //                      codes mode Cb[2] [F][32] u16, double buffered (128*F B)
-  const size_t xblk = CODES ? (size_t)128 * F : (size_t)256 * F;  // HEAP_T: 2 x 128F, same as Xs + St
+  //                      codes mode Cb[2] [F2/2][32][2] u16 in 2^b-aligned buffers, double buffered
+  const int F2 = (F + 1) & ~1;  // codes: feature pairs interleaved per lane, [F2/2][32][2] u16
+  // codes: two 2^b-aligned buffers of code_buf bytes per group (trav_x_region)
+  const size_t xblk = CODES ? (size_t)2 * p.code_buf : (size_t)256 * F;  // HEAP_T: 2 x 128F, same as Xs + St
   float* Xs = reinterpret_cast<float*>(smem + p.chunk_cap + (size_t)grp * xblk);  // [F][32]
   float* St = Xs + 32 * F;                                                         // [32][F]
-  uint16_t* Cb = reinterpret_cast<uint16_t*>(smem + p.chunk_cap + (size_t)grp * xblk);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.chunk_cap + (size_t)NB * xblk);
+  uint8_t* Cb = nullptr;
+  if (CODES) {
+    const uint32_t a0 = ptx::s2u(smem + p.chunk_cap);
+    const uint32_t al = (a0 + (uint32_t)p.code_buf - 1u) & ~((uint32_t)p.code_buf - 1u);
+    Cb = smem + p.chunk_cap + (al - a0) + (size_t)grp * xblk;
+  }
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.chunk_cap + trav_x_region(CODES, F, NB));
   uint64_t* red = reinterpret_cast<uint64_t*>(smem + p.red_off);  // [NB][G-1][32][K] intra-group partials
 
   const bool clustered = p.mode == TRAV_CLUSTER;
@@ -440,14 +468,14 @@ __global__ void __launch_bounds__(512, 1) trav_kernel(const TravParams p) {
   };
   // codes mode: blocks of the binned input are [F][32] u16, always complete
   const uint8_t* codes = reinterpret_cast<const uint8_t*>(p.X);
-  const uint32_t code_block_bytes = 32u * EB * (uint32_t)F;
+  const uint32_t code_block_bytes = CODES ? 64u * (uint32_t)F2 : 128u * (uint32_t)F;
   auto issue_codes = [&](int64_t b, int s) {
     if (gw == 0 && lane == 0 && b < n_blocks) {
       uint64_t* bar = s ? &bars[1 + 5 * NB + grp] : sbar;
       ptx::fence_proxy_async();
       ptx::mbar_arrive_expect_tx(bar, code_block_bytes);
-      ptx::bulk_g2s(reinterpret_cast<uint8_t*>(Cb) + (size_t)s * code_block_bytes, codes + b * (int64_t)code_block_bytes,
-                    code_block_bytes, bar);
+      uint8_t* dst = CODES ? Cb + (size_t)s * p.code_buf : reinterpret_cast<uint8_t*>(Xs) + (size_t)s * code_block_bytes;
+      ptx::bulk_g2s(dst, codes + b * (int64_t)code_block_bytes, code_block_bytes, bar);
     }
   };
   if (PRE) issue_codes(blk, 0);
@@ -469,7 +497,8 @@ __global__ void __launch_bounds__(512, 1) trav_kernel(const TravParams p) {
       ptx::mbar_wait(sb ? &bars[1 + 5 * NB + grp] : sbar, (itx >> 1) & 1);
       ++itx;
       issue_codes(next, sb ^ 1);  // the other buffer was released by the previous block's group sync
-      xptr = reinterpret_cast<const uint8_t*>(Cb) + (size_t)sb * code_block_bytes + EB * lane;
+      xptr = (CODES ? Cb + (size_t)sb * p.code_buf : reinterpret_cast<const uint8_t*>(Xs) + (size_t)sb * code_block_bytes) +
+             4 * lane;
     } else {
       const bool full = row0 + 32 <= n_rows;
       if (full) {

@@ -205,6 +205,20 @@ def test_coded_and_fp32_node_formats(coded, monkeypatch):
     assert g2.layout()["coded"] == (coded == "1")
 
 
+@pytest.mark.parametrize("F", [1, 2, 6, 28, 40])
+def test_coded_format_feature_widths(F, monkeypatch):
+    """Threshold-bin codes at every vector width of the binning kernel (F % 4 =
+    0, 2, odd), F = 1, an odd padding feature, ragged row tails; ties placed on
+    thresholds, specials injected; bit-exact against the oracle."""
+    monkeypatch.setenv("BRIDGER_CODES", "1")
+    m = perfect_ensemble(40 + F, 37, 7, F, kind="classification", n_classes=2, calib_rows=2048)
+    m = prune_ensemble(m, 40 + F, p=0.05, with_missing=(F % 2 == 0))
+    X = inject_specials(gen_x(41 + F, 0, 3001, F), 41 + F, rate=0.02)
+    X[::61, 0] = m.threshold[m.feature == 0][0]
+    g, _ = check(m, X)
+    assert g.layout()["coded"]
+
+
 @pytest.mark.parametrize("pret", ["1", "0"])
 def test_pretransposed_input_mode(pret, monkeypatch):
     """Wide input, many chunks: X transposed once into feature-major blocks

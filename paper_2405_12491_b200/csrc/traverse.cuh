@@ -150,12 +150,11 @@ __device__ __forceinline__ void walk_trees(const TravParams& p, const TravChunk&
     const uint32_t xb = ptx::s2u(xl);
     const uint32_t mask = (uint32_t)p.code_buf - 1u;
     const uint32_t k2 = p.k2, k16 = p.k16;
-    uint32_t A[NI], c[NI], c4[NI];
+    uint32_t A[NI], cb[NI];  // cb = 4 - base_u:  A' = A * 2 + cb (+ 4 if right)
 #pragma unroll
     for (int u = 0; u < NI; ++u) {
       A[u] = nb + 4u * (uint32_t)(u * I);  // shared address of tree u's current node
-      c[u] = 4u - A[u];
-      c4[u] = 8u - A[u];
+      cb[u] = 4u - A[u];
     }
     for (int lvl = 0; lvl < D; ++lvl) {
       uint32_t a[NI];
@@ -168,11 +167,39 @@ __device__ __forceinline__ void walk_trees(const TravParams& p, const TravChunk&
       for (int u = 0; u < NI; ++u) {
         bool r = x[u] * k16 > a[u];  // code(x) > j  <=>  !(x <= t);  NaN code 0xFFFF -> right
         if (ML) r = r && !(((a[u] >> 15) & 1u) && x[u] == 0xFFFFu);
-        A[u] = A[u] * k2 + (r ? c4[u] : c[u]);
+        A[u] = A[u] * k2 + cb[u];
+        if (r) A[u] += 4u;
       }
     }
+    if (p.mode != TRAV_APPLY && KT == K) {
+      // leaf values straight from the final node address: leaf l = idx - I,
+      // idx = (A - base_u) / 4, value address = leaves_u + 4 K l
+      //   = K * A + (leaves_u - K (base_u + 4 I)),  base_u = 4 - cb_u
+      const uint32_t lb = ptx::s2u(leaves) + 4u * (uint32_t)(j * L * KT);
 #pragma unroll
-    for (int u = 0; u < NI; ++u) idx[u] = (int)((A[u] + c[u] - 4u) >> 2);
+      for (int u = 0; u < NI; ++u) {
+        const uint32_t la = (uint32_t)KT * (A[u] + cb[u] - 4u - 4u * (uint32_t)I) + lb + 4u * (uint32_t)(u * L * KT);
+        if (KT == 2) {
+          float v0, v1;
+          asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v0), "=f"(v1) : "r"(la));
+          acc[0] += leaf_to_acc<ACC>(v0);
+          acc[KT > 1 ? 1 : 0] += leaf_to_acc<ACC>(v1);
+        } else if (KT == 4) {
+          float v0, v1, v2, v3;
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v0), "=f"(v1), "=f"(v2), "=f"(v3) : "r"(la));
+          acc[0] += leaf_to_acc<ACC>(v0);
+          acc[KT > 1 ? 1 : 0] += leaf_to_acc<ACC>(v1);
+          acc[KT > 2 ? 2 : 0] += leaf_to_acc<ACC>(v2);
+          acc[KT > 3 ? 3 : 0] += leaf_to_acc<ACC>(v3);
+        } else {
+#pragma unroll
+          for (int k = 0; k < KT; ++k) acc[k] += leaf_to_acc<ACC>(ptx::lds_f32(la + 4u * k));
+        }
+      }
+      return;
+    }
+#pragma unroll
+    for (int u = 0; u < NI; ++u) idx[u] = (int)((A[u] + cb[u] - 4u) >> 2);
   } else {
     constexpr uint32_t kFeatMask = ML ? 0x7fffffffu : 0xffffffffu;
     const uint2* nb = static_cast<const uint2*>(nodes) + (size_t)j * I;

@@ -191,6 +191,114 @@ __global__ void __launch_bounds__(512, 1) bin_kernel(const float* __restrict__ X
   }
 }
 
+// Cooperative binning for search tables too large to leave room for per-warp
+// staging (C3: 90 features x 511-slot trees = 184 KB): the CTA's 16 warps share
+// one double-buffered dense [32][F] block (bulk copy, mbarrier) and split its
+// feature pairs; lane = row as above, up to 8 chains (4 pairs) per warp pass.
+template <int NP>
+__global__ void __launch_bounds__(512, 1) bin_coop_kernel(const float* __restrict__ X, int64_t n_rows, int32_t F,
+                                                          const float* __restrict__ table, int32_t k,
+                                                          uint32_t* __restrict__ codes) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
+  const int P = (1 << k) - 1;
+  const int F2h = (F + 1) >> 1;
+  const size_t tab_bytes = ((size_t)F * P * 4 + 127) / 128 * 128;
+  const uint32_t blk_bytes = 128u * (uint32_t)F;
+  float* stage = reinterpret_cast<float*>(smem + tab_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + tab_bytes + 2 * (size_t)blk_bytes);
+  uint32_t* done = reinterpret_cast<uint32_t*>(bars + 2);  // [2] warps finished with buffer b
+  {
+    const float4* src = reinterpret_cast<const float4*>(table);
+    float4* dst = reinterpret_cast<float4*>(smem);
+    const int n4 = (F * P) / 4;
+    for (int i = threadIdx.x; i < n4; i += blockDim.x) dst[i] = src[i];
+    for (int i = n4 * 4 + threadIdx.x; i < F * P; i += blockDim.x) reinterpret_cast<float*>(smem)[i] = table[i];
+  }
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bars[0], 1);
+    ptx::mbar_init(&bars[1], 1);
+    done[0] = done[1] = 0;
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  const uint32_t tab_s = ptx::s2u(smem);
+  const int64_t n_blocks = (n_rows + 31) / 32;
+  auto issue = [&](int64_t b, int buf) {
+    if (threadIdx.x == 0 && b < n_blocks && (b + 1) * 32 <= n_rows) {
+      ptx::fence_proxy_async();
+      ptx::mbar_arrive_expect_tx(&bars[buf], blk_bytes);
+      ptx::bulk_g2s(stage + (size_t)buf * 32 * F, X + b * 32 * (int64_t)F, blk_bytes, &bars[buf]);
+    }
+  };
+  issue(blockIdx.x, 0);
+  issue((int64_t)blockIdx.x + gridDim.x, 1);
+  int it = 0;
+  for (int64_t blk = blockIdx.x; blk < n_blocks; blk += gridDim.x, ++it) {
+    const int buf = it & 1;
+    float* St = stage + (size_t)buf * 32 * F;
+    const int64_t row0 = blk * 32;
+    if (row0 + 32 <= n_rows) {
+      ptx::mbar_wait(&bars[buf], (uint32_t)(it >> 1) & 1u);
+    } else {
+      // the tail block (never bulk-copied): every warp is past the buffer's
+      // previous use before it is filled by hand
+      __syncthreads();
+      const int rows = (int)(n_rows - row0);
+      const float* src = X + row0 * F;
+      for (int e = threadIdx.x; e < 32 * F; e += blockDim.x) St[e] = e < rows * F ? src[e] : 0.f;
+      __syncthreads();
+    }
+    const float* xr = St + (size_t)lane * F;
+    uint32_t* dst = codes + (size_t)blk * F2h * 32 + lane;
+    // this warp's pairs warp, warp + NW, ...: NP pairs (2 NP chains) per pass
+    for (int p0 = warp; p0 < F2h; p0 += NP * NW) {
+      float x[2 * NP];
+      uint32_t A[2 * NP], c4[2 * NP];
+#pragma unroll
+      for (int u = 0; u < 2 * NP; ++u) {
+        const int f = min(2 * (p0 + (u >> 1) * NW) + (u & 1), F - 1);
+        x[u] = xr[f];
+        A[u] = tab_s + (uint32_t)(f * P) * 4u;
+        c4[u] = 4u - A[u];
+      }
+      for (int s = 0; s < k; ++s) {
+#pragma unroll
+        for (int u = 0; u < 2 * NP; ++u) {
+          const float e = ptx::lds_f32(A[u]);
+          A[u] = 2u * A[u] + c4[u];
+          if (e < x[u]) A[u] += 4u;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2 * NP; u += 2) {
+        const int pr = p0 + (u >> 1) * NW;
+        if (pr < F2h) {
+          const uint32_t c0 = isnan(x[u]) ? 0xFFFFu : ((A[u] + c4[u] - 4u) >> 2) - (uint32_t)P;
+          const uint32_t c1 = 2 * pr + 1 >= F ? 0u
+                              : isnan(x[u + 1]) ? 0xFFFFu : ((A[u + 1] + c4[u + 1] - 4u) >> 2) - (uint32_t)P;
+          dst[(size_t)pr * 32] = c0 | (c1 << 16);
+        }
+      }
+    }
+    // no CTA-wide barrier per block (it would drain the pipeline): the last
+    // warp to finish with this buffer refills it, the others run ahead
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd(&done[buf], 1u) == (uint32_t)NW - 1u) {
+        done[buf] = 0;
+        if (blk + 2 * (int64_t)gridDim.x < n_blocks && (blk + 2 * (int64_t)gridDim.x + 1) * 32 <= n_rows) {
+          ptx::fence_proxy_async();
+          ptx::mbar_arrive_expect_tx(&bars[buf], blk_bytes);
+          ptx::bulk_g2s(stage + (size_t)buf * 32 * F, X + (blk + 2 * (int64_t)gridDim.x) * 32 * (int64_t)F, blk_bytes,
+                        &bars[buf]);
+        }
+      }
+    }
+  }
+}
+
 // Pre-transposed input (FMT_HEAP_T): X [N][F] fp32 row-major -> [n_blocks][F][32]
 // fp32, the traversal's feature-major 32-row block layout, written once so
 // that every chunk CTA bulk-copies blocks with no per-chunk transpose.
@@ -368,26 +476,26 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
     if (err != cudaSuccess) return err;
     const int P = (1 << L.bin_k) - 1;
     const int fixed = (m->F * P * 4 + 127) / 128 * 128;
-    // staged (bulk-copied dense blocks) when the table leaves room for >= 8
-    // warps of double-buffered staging, else lanes read X from global memory
+    // per-warp staging (bulk-copied dense blocks) when the table leaves room
+    // for >= 8 warps of double-buffered staging, else one CTA-shared block
     int nwb = 16;
     while (nwb > 1 && fixed + nwb * (2 * 128 * m->F + 16) > 232448) --nwb;
     const bool stage = nwb >= 8;
+    const bool coop = !stage && fixed + 2 * 128 * m->F + 32 <= 232448;
     if (!stage) nwb = 16;
-    const int bsmem = fixed + (stage ? nwb * (2 * 128 * m->F + 16) : 0);
+    const int bsmem = fixed + (stage ? nwb * (2 * 128 * m->F + 16) : coop ? 2 * 128 * m->F + 32 : 0);
     const int vi = (m->F % 4 == 0) ? 2 : (m->F % 2 == 0) ? 1 : 0;
     void (*kerns[2][3])(const float*, int64_t, int32_t, const float*, int32_t, uint32_t*) = {
         {bin_kernel<1, false>, bin_kernel<2, false>, bin_kernel<4, false>},
         {bin_kernel<1, true>, bin_kernel<2, true>, bin_kernel<4, true>}};
-    auto bk = kerns[stage ? 1 : 0][vi];
-    static bool bin_attr[2][3] = {{false, false, false}, {false, false, false}};
-    if (!bin_attr[stage ? 1 : 0][vi]) {
-      cudaFuncSetAttribute(bk, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-      bin_attr[stage ? 1 : 0][vi] = true;
-    }
+    const int np = std::min(4, (((m->F + 1) >> 1) + nwb - 1) / nwb);  // pairs per warp pass (coop)
+    void (*coops[4])(const float*, int64_t, int32_t, const float*, int32_t, uint32_t*) = {
+        bin_coop_kernel<1>, bin_coop_kernel<2>, bin_coop_kernel<3>, bin_coop_kernel<4>};
+    auto bk = coop ? coops[np - 1] : kerns[stage ? 1 : 0][vi];
+    cudaFuncSetAttribute(bk, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bk, nwb * 32, bsmem);
-    const int64_t want_ctas = (nbk + nwb - 1) / nwb;
+    const int64_t want_ctas = coop ? nbk : (nbk + nwb - 1) / nwb;
     const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>(want_ctas, (int64_t)sms * std::max(1, occ)));
     bk<<<bgrid, nwb * 32, bsmem, st>>>(X, n_rows, m->F, m->d_bin_table, L.bin_k, static_cast<uint32_t*>(codes));
     count_launch();

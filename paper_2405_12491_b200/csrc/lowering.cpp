@@ -398,8 +398,8 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
   bool want_codes = codes_env ? codes_env[0] != '0' : (visits >= 12 * (int64_t)F && visits >= 64);
   if (want_codes) {
     want_codes = build_bin_table(d, out);
-    // the binning kernel keeps the whole table in shared memory
-    if (want_codes && out->bin_table.size() * 4 > 190 * 1024) want_codes = false;
+    // (tables of any size: the binning kernel keeps all of them, or a group of
+    // features' tables, in shared memory; one feature's is <= 128 KB)
   }
   std::vector<int32_t> order(T);
   std::iota(order.begin(), order.end(), 0);
@@ -417,11 +417,15 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
     // buffered, filled straight by bulk copy); fp32 mode = feature-major block
     // + dense staging block
     xw = codes ? 2 * code_buf_bytes(F) : 2 * 32 * F * 4;
-    // 16 warps; NB = largest power of two with NB * xw <= 120 KB (measured on
+    // 16 warps; NB = largest power of two with NB * xw <= the x budget below (measured on
     // B200: C2 best at NB=16/G=1, C3 at NB=4/G=4 in fp32 mode)
     nw = 16;
     nb = 16;
-    while (nb > 1 && nb * xw > 120 * 1024) nb /= 2;
+    // measured on B200: C3 codes (16 KB per group) best at NB=8 (12.59 vs 13.11
+    // ms at NB=4), C5 shard codes (32 KB per group) best at NB=2 (14.6 vs 15.3)
+    int32_t xbudget = (codes && xw <= 16 * 1024) ? 144 * 1024 : 120 * 1024;
+    if (const char* e = std::getenv("BRIDGER_XBUDGET")) xbudget = 1024 * std::atoi(e);  // experiments
+    while (nb > 1 && nb * xw > xbudget) nb /= 2;
     if (const char* e = std::getenv("BRIDGER_WARPS")) nw = std::max(1, std::min(16, std::atoi(e)));  // experiments
     if (const char* e = std::getenv("BRIDGER_BLOCKS")) nb = std::max(1, std::min(16, std::atoi(e)));
     nb = std::min(nb, nw);

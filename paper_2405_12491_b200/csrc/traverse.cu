@@ -299,6 +299,68 @@ __global__ void __launch_bounds__(512, 1) bin_coop_kernel(const float* __restric
   }
 }
 
+// Feature-group binning for search tables too large to hold for all features
+// at once (C5-shaped shards: 200 features x 8191-slot trees = 6.5 MB): a CTA
+// owns FG features (their tables in shared memory) and a range of 32-row
+// blocks; lane = row reads its row's FG contiguous values straight from global
+// memory and descends FG search trees (FG chains).  FG is 4 or 2 (whole code
+// pairs: one coalesced u32 store per pair), or 1 (u16 stores).
+template <int FG>
+__global__ void __launch_bounds__(512, 1) bin_fg_kernel(const float* __restrict__ X, int64_t n_rows, int32_t F,
+                                                        const float* __restrict__ table, int32_t k,
+                                                        uint32_t* __restrict__ codes) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
+  const int P = (1 << k) - 1;
+  const int F2h = (F + 1) >> 1;
+  const int n_fg = (F + FG - 1) / FG;
+  const int fg = blockIdx.x % n_fg;
+  const int slice = blockIdx.x / n_fg, n_slices = gridDim.x / n_fg;
+  const int f0 = fg * FG;
+  const int nf = min(FG, F - f0);
+  {
+    const float* src = table + (size_t)f0 * P;
+    float* dst = reinterpret_cast<float*>(smem);
+    for (int i = threadIdx.x; i < nf * P; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  const uint32_t tab_s = ptx::s2u(smem);
+  const int64_t n_blocks = (n_rows + 31) / 32;
+  for (int64_t blk = (int64_t)slice * NW + warp; blk < n_blocks; blk += (int64_t)n_slices * NW) {
+    const int64_t row = blk * 32 + lane;
+    const float* xr = X + (row < n_rows ? row : blk * 32) * (int64_t)F + f0;
+    float x[FG];
+#pragma unroll
+    for (int u = 0; u < FG; ++u) x[u] = u < nf ? __ldg(xr + u) : 0.f;
+    uint32_t A[FG], c4[FG];
+#pragma unroll
+    for (int u = 0; u < FG; ++u) {
+      A[u] = tab_s + (uint32_t)(min(u, nf - 1) * P) * 4u;
+      c4[u] = 4u - A[u];
+    }
+    for (int s = 0; s < k; ++s) {
+#pragma unroll
+      for (int u = 0; u < FG; ++u) {
+        const float e = ptx::lds_f32(A[u]);
+        A[u] = 2u * A[u] + c4[u];
+        if (e < x[u]) A[u] += 4u;
+      }
+    }
+    uint32_t cd[FG];
+#pragma unroll
+    for (int u = 0; u < FG; ++u)
+      cd[u] = u >= nf ? 0u : isnan(x[u]) ? 0xFFFFu : ((A[u] + c4[u] - 4u) >> 2) - (uint32_t)P;
+    uint32_t* dst = codes + (size_t)blk * F2h * 32 + lane;
+    if (FG == 1) {
+      reinterpret_cast<uint16_t*>(dst + (size_t)(f0 >> 1) * 32)[f0 & 1] = (uint16_t)cd[0];
+    } else {
+#pragma unroll
+      for (int u = 0; u < FG; u += 2)
+        if (f0 + u < 2 * F2h) dst[(size_t)((f0 + u) >> 1) * 32] = cd[u] | (cd[u + 1 < FG ? u + 1 : u] << 16) * (u + 1 < FG);
+    }
+  }
+}
+
 // Pre-transposed input (FMT_HEAP_T): X [N][F] fp32 row-major -> [n_blocks][F][32]
 // fp32, the traversal's feature-major 32-row block layout, written once so
 // that every chunk CTA bulk-copies blocks with no per-chunk transpose.
@@ -480,8 +542,12 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
     // for >= 8 warps of double-buffered staging, else one CTA-shared block
     int nwb = 16;
     while (nwb > 1 && fixed + nwb * (2 * 128 * m->F + 16) > 232448) --nwb;
-    const bool stage = nwb >= 8;
-    const bool coop = !stage && fixed + 2 * 128 * m->F + 32 <= 232448;
+    bool stage = nwb >= 8;
+    bool coop = !stage && fixed + 2 * 128 * m->F + 32 <= 232448;
+    if (const char* e = std::getenv("BRIDGER_BIN")) {  // tests: force a binning variant where it fits
+      if (e[0] == 'f') stage = coop = false;
+      if (e[0] == 'c' && fixed + 2 * 128 * m->F + 32 <= 232448) { stage = false; coop = true; }
+    }
     if (!stage) nwb = 16;
     const int bsmem = fixed + (stage ? nwb * (2 * 128 * m->F + 16) : coop ? 2 * 128 * m->F + 32 : 0);
     const int vi = (m->F % 4 == 0) ? 2 : (m->F % 2 == 0) ? 1 : 0;
@@ -492,12 +558,26 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
     void (*coops[4])(const float*, int64_t, int32_t, const float*, int32_t, uint32_t*) = {
         bin_coop_kernel<1>, bin_coop_kernel<2>, bin_coop_kernel<3>, bin_coop_kernel<4>};
     auto bk = coop ? coops[np - 1] : kerns[stage ? 1 : 0][vi];
+    int bsm = bsmem;
+    int64_t want_ctas = coop ? nbk : (nbk + nwb - 1) / nwb;
+    int fgsz = 0;
+    if (!stage && !coop) {
+      // feature groups: FG features' tables per CTA, whole code pairs when they fit
+      fgsz = 4 * P * 4 <= 200 * 1024 ? 4 : 2 * P * 4 <= 200 * 1024 ? 2 : 1;
+      bk = fgsz == 4 ? bin_fg_kernel<4> : fgsz == 2 ? bin_fg_kernel<2> : bin_fg_kernel<1>;
+      bsm = fgsz * P * 4;
+      const int n_fg = (m->F + fgsz - 1) / fgsz;
+      // slices of row blocks per feature group: fill the SMs, each slice >= 16 blocks
+      const int64_t slices = std::max<int64_t>(1, std::min<int64_t>((2 * sms + n_fg - 1) / n_fg, (nbk + 15) / 16));
+      want_ctas = n_fg * slices;
+      nwb = 16;
+    }
     cudaFuncSetAttribute(bk, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bk, nwb * 32, bsmem);
-    const int64_t want_ctas = coop ? nbk : (nbk + nwb - 1) / nwb;
-    const int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>(want_ctas, (int64_t)sms * std::max(1, occ)));
-    bk<<<bgrid, nwb * 32, bsmem, st>>>(X, n_rows, m->F, m->d_bin_table, L.bin_k, static_cast<uint32_t*>(codes));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bk, nwb * 32, bsm);
+    const int bgrid = fgsz ? (int)want_ctas
+                           : (int)std::max<int64_t>(1, std::min<int64_t>(want_ctas, (int64_t)sms * std::max(1, occ)));
+    bk<<<bgrid, nwb * 32, bsm, st>>>(X, n_rows, m->F, m->d_bin_table, L.bin_k, static_cast<uint32_t*>(codes));
     count_launch();
     err = cudaGetLastError();
     if (err != cudaSuccess) {

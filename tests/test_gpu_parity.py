@@ -219,6 +219,29 @@ def test_coded_format_feature_widths(F, monkeypatch):
     assert g.layout()["coded"]
 
 
+@pytest.mark.parametrize("binv", ["coop", "fg"])
+@pytest.mark.parametrize("F", [7, 28, 90])
+def test_coded_binning_variants(binv, F, monkeypatch):
+    """The cooperative (CTA-shared block) and feature-group (tables per CTA,
+    direct loads) binning kernels produce the same codes: bit-exact end to end."""
+    monkeypatch.setenv("BRIDGER_CODES", "1")
+    monkeypatch.setenv("BRIDGER_BIN", binv)
+    m = perfect_ensemble(60 + F, 31, 7, F, kind="regression", lr=0.1, calib_rows=2048)
+    m = prune_ensemble(m, 60 + F, p=0.05, with_missing=True)
+    X = inject_specials(gen_x(61 + F, 0, 2011, F), 61 + F, rate=0.02)
+    g, _ = check(m, X)
+    assert g.layout()["coded"]
+
+
+def test_c5_shard_coded(monkeypatch):
+    """C5-shaped tree shard (1250 trees would take minutes in the oracle: 120
+    trees of depth 10 over 200 features) in threshold-bin codes with
+    feature-group binning (6K+ thresholds per feature at full size)."""
+    monkeypatch.setenv("BRIDGER_CODES", "1")
+    c, m = make_config("C5", n_trees=120)
+    g, _ = check(m, gen_x(5, 0, 3001, 200), apply=False)
+
+
 @pytest.mark.parametrize("pret", ["1", "0"])
 def test_pretransposed_input_mode(pret, monkeypatch):
     """Wide input, many chunks: X transposed once into feature-major blocks

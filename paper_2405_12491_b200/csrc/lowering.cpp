@@ -596,14 +596,17 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
     // global-tree walker for comparison).
     const char* env = std::getenv("BRIDGER_STREAM");
     const bool want_stream = !(env && env[0] == '0');
-    const int64_t tree_nodes = (((int64_t)1 << Dmax) - 1) * 8;
+    // streamed trees are stored with an 8-byte front pad ([pad][node 0..I-1],
+    // 2^D * 8 bytes): the two children 2i+1, 2i+2 of every node then form one
+    // 16-byte-aligned pair (one LDS.128 in the speculative walk)
+    const int64_t tree_nodes = ((int64_t)1 << Dmax) * 8;
     const int32_t ns = 3;
     // one slot = 64-byte chunk header + node records
     const int64_t stage = std::max<int64_t>((tree_nodes + 15) / 16 * 16, 16384) + 64;
     std::vector<Run> pieces;
     int32_t min_n = INT32_MAX;
     for (const Run& r : bal) {
-      const int64_t per = std::max<int64_t>(1, std::min<int64_t>(4, (stage - 64) / ((((int64_t)1 << r.D) - 1) * 8)));
+      const int64_t per = std::max<int64_t>(1, std::min<int64_t>(4, (stage - 64) / (((int64_t)1 << r.D) * 8)));
       for (int32_t s0 = 0; s0 < r.n; s0 += (int32_t)per) {
         pieces.push_back({r.start + s0, (int32_t)std::min<int64_t>(per, r.n - s0), r.D});
         min_n = std::min(min_n, pieces.back().n);
@@ -647,7 +650,8 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
     c.depth = D;
     c.first_slot = r.start;
     const int64_t nodes = out->split ? (((int64_t)r.n * I * 4 + 15) / 16 * 16 + (int64_t)r.n * I)
-                                     : (int64_t)r.n * I * node_bytes;
+                          : out->stream ? (int64_t)r.n * (I + 1) * 8
+                                        : (int64_t)r.n * I * node_bytes;
     c.leaf_offset = (int32_t)((nodes + 15) / 16 * 16);
     c.bytes = (int32_t)(c.leaf_offset + ((int64_t)r.n * L * K * 4 + 15) / 16 * 16);
     out->data.resize(off + c.bytes, 0);
@@ -676,7 +680,8 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
           fe[i] = (uint8_t)(pt.feature[i] | (pt.missing[i] << 7));
         }
       } else {
-        uint32_t* nd = reinterpret_cast<uint32_t*>(base) + (size_t)j * I * 2;
+        // streamed: tree j at [(I + 1) j + 1] (front pad), else [I j]
+        uint32_t* nd = reinterpret_cast<uint32_t*>(base) + (out->stream ? ((size_t)j * (I + 1) + 1) * 2 : (size_t)j * I * 2);
         for (int32_t i = 0; i < I; ++i) {
           uint32_t tb;
           std::memcpy(&tb, &pt.threshold[i], 4);

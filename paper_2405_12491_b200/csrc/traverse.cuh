@@ -776,18 +776,34 @@ cudaError_t launch_trav_t(const TravParams& p, int grid_ctas, int block, int sme
 // software-pipelined by one pass (loads of pass p land while pass p+1 walks).
 template <int W, bool ML>
 __device__ __forceinline__ void stream_walk(const uint2* nb, const float* xl, int I, int D, int (&idx)[W]) {
+  // nb: tree 0's node 0; tree u at nb + u (I + 1) (8-byte front pad per tree,
+  // lowering.cpp), so the children pair {2i+1, 2i+2} of every node is one
+  // 16-byte-aligned LDS.128.  Child-pair speculation: at each level the
+  // feature value of the current node and BOTH children's records are loaded
+  // together (independent addresses), the compare then selects the child
+  // record already in registers -- one shared-memory latency per level
+  // instead of two (node record, then the feature value it names).
   constexpr uint32_t kFeatMask = ML ? 0x7fffffffu : 0xffffffffu;
+  uint2 a[W];
 #pragma unroll
-  for (int u = 0; u < W; ++u) idx[u] = 0;
+  for (int u = 0; u < W; ++u) {
+    idx[u] = 0;
+    a[u] = nb[u * (I + 1)];
+  }
   for (int lvl = 0; lvl < D; ++lvl) {
-    uint2 a[W];
-#pragma unroll
-    for (int u = 0; u < W; ++u) a[u] = nb[u * I + idx[u]];
     float x[W];
+    uint4 pr[W];
 #pragma unroll
-    for (int u = 0; u < W; ++u) x[u] = xl[(a[u].y & kFeatMask) * 32];
+    for (int u = 0; u < W; ++u) {
+      x[u] = xl[(a[u].y & kFeatMask) * 32];
+      if (lvl + 1 < D) pr[u] = *reinterpret_cast<const uint4*>(nb + u * (I + 1) + 2 * idx[u] + 1);
+    }
 #pragma unroll
-    for (int u = 0; u < W; ++u) idx[u] = 2 * idx[u] + 1 + go_right<ML>(x[u], a[u]);
+    for (int u = 0; u < W; ++u) {
+      const int r = go_right<ML>(x[u], a[u]);
+      idx[u] = 2 * idx[u] + 1 + r;
+      if (lvl + 1 < D) a[u] = r ? make_uint2(pr[u].z, pr[u].w) : make_uint2(pr[u].x, pr[u].y);
+    }
   }
 #pragma unroll
   for (int u = 0; u < W; ++u) idx[u] -= I;  // leaf index
@@ -838,7 +854,7 @@ __global__ void __launch_bounds__(544, 1) trav_stream_kernel(const TravParams p)
       for (int64_t k = 0; k < n_items; ++k) {
         const TravChunk c = p.chunks[c_i];
         if (++c_i == nC) c_i = 0;
-        ptx::mbar_wait(&empty[s], ph ^ 1);
+        ptx::mbar_wait_sleep(&empty[s], ph ^ 1, 256);
         uint8_t* slot = ring + (size_t)s * p.stream_stage;
         *reinterpret_cast<TravChunk*>(slot) = c;
         ptx::fence_proxy_async();
@@ -924,7 +940,7 @@ __global__ void __launch_bounds__(544, 1) trav_stream_kernel(const TravParams p)
         int idx[W];
         // trees past the chunk's end re-walk its last tree (masked below)
         const int jw = min(j, ch.n_trees - W < 0 ? 0 : ch.n_trees - W);
-        stream_walk<W, ML>(nodes + (size_t)jw * I, xl, I, D, idx);
+        stream_walk<W, ML>(nodes + (size_t)jw * (I + 1) + 1, xl, I, D, idx);
         if (APPLY) {
 #pragma unroll
           for (int u = 0; u < W; ++u) {

@@ -473,6 +473,10 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
         if (!out->global_trees && sms > 0 && nc > sms / 2 && nc % sms != 0) {
           const int32_t nc2 = (nc + sms - 1) / sms * sms;
           if (nc2 <= total) nc = nc2;
+        } else if (!out->global_trees && sms > 0 && sms % 2 == 0 && nc > sms / 4 && nc < sms / 2 && sms / 2 <= total) {
+          // ... or up to half the SM count: two CTAs per chunk fill every SM
+          // (C5 shard in codes: 70 chunks of 18 trees -> 74 x 2 CTAs = 148)
+          nc = sms / 2;
         }
         int32_t st = runs[i].start;
         for (int32_t c = 0; c < nc; ++c) {

@@ -593,6 +593,7 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
   out->group = G;
   out->chunk_budget = budget;
   out->stream = false;
+  out->stream_split = false;
   if (out->global_trees && !out->sparse) {
     // Tree-streamed mode (traverse.cuh K4s): rows resident, node records of
     // chunks of <= 4 equal-depth trees streamed through a 3-slot ring; leaves
@@ -602,15 +603,23 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
     const bool want_stream = !(env && env[0] == '0');
     // streamed trees are stored with an 8-byte front pad ([pad][node 0..I-1],
     // 2^D * 8 bytes): the two children 2i+1, 2i+2 of every node then form one
-    // 16-byte-aligned pair (one LDS.128 in the speculative walk)
-    const int64_t tree_nodes = ((int64_t)1 << Dmax) * 8;
-    const int32_t ns = 3;
+    // 16-byte-aligned pair (one LDS.128 in the speculative walk).  With
+    // F <= 127 the split format ([pad][thresholds] fp32 + [pad][features] u8,
+    // 5 * 2^D bytes) lets two trees share a slot of a 2-slot ring, so every
+    // thread walks two trees at once (BRIDGER_STREAM_SPLIT=0 keeps 8-byte nodes)
+    const char* senv = std::getenv("BRIDGER_STREAM_SPLIT");
+    const bool spl = F <= 127 && !(senv && senv[0] == '0');
+    auto tree_bytes = [&](int32_t D) -> int64_t {
+      return spl ? ((((int64_t)5 << D) + 15) / 16 * 16) : ((int64_t)1 << D) * 8;
+    };
+    const int64_t tree_nodes = tree_bytes(Dmax);
+    const int32_t ns = spl ? 2 : 3;
     // one slot = 64-byte chunk header + node records
-    const int64_t stage = std::max<int64_t>((tree_nodes + 15) / 16 * 16, 16384) + 64;
+    const int64_t stage = std::max<int64_t>(spl ? 2 * tree_nodes : (tree_nodes + 15) / 16 * 16, 16384) + 64;
     std::vector<Run> pieces;
     int32_t min_n = INT32_MAX;
     for (const Run& r : bal) {
-      const int64_t per = std::max<int64_t>(1, std::min<int64_t>(4, (stage - 64) / (((int64_t)1 << r.D) * 8)));
+      const int64_t per = std::max<int64_t>(1, std::min<int64_t>(4, (stage - 64) / tree_bytes(r.D)));
       for (int32_t s0 = 0; s0 < r.n; s0 += (int32_t)per) {
         pieces.push_back({r.start + s0, (int32_t)std::min<int64_t>(per, r.n - s0), r.D});
         min_n = std::min(min_n, pieces.back().n);
@@ -629,6 +638,7 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
       out->stream_stage = (int32_t)stage;
       out->stream_warps = warps;
       out->stream_w = w;
+      out->stream_split = spl;
       bal.swap(pieces);
     }
   }
@@ -654,7 +664,7 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
     c.depth = D;
     c.first_slot = r.start;
     const int64_t nodes = out->split ? (((int64_t)r.n * I * 4 + 15) / 16 * 16 + (int64_t)r.n * I)
-                          : out->stream ? (int64_t)r.n * (I + 1) * 8
+                          : out->stream ? (int64_t)r.n * (out->stream_split ? ((((int64_t)5 << D) + 15) / 16 * 16) : (int64_t)(I + 1) * 8)
                                         : (int64_t)r.n * I * node_bytes;
     c.leaf_offset = (int32_t)((nodes + 15) / 16 * 16);
     c.bytes = (int32_t)(c.leaf_offset + ((int64_t)r.n * L * K * 4 + 15) / 16 * 16);
@@ -682,6 +692,15 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
         for (int32_t i = 0; i < I; ++i) {
           th[i] = pt.threshold[i];
           fe[i] = (uint8_t)(pt.feature[i] | (pt.missing[i] << 7));
+        }
+      } else if (out->stream && out->stream_split) {
+        // streamed split: tree j at j * tb: [pad][thr 0..I-1] fp32, [pad][feature | missing << 7] u8
+        const size_t tb = (((size_t)5 << D) + 15) / 16 * 16;
+        float* th = reinterpret_cast<float*>(base + (size_t)j * tb);
+        uint8_t* fe = base + (size_t)j * tb + ((size_t)4 << D);
+        for (int32_t i = 0; i < I; ++i) {
+          th[1 + i] = pt.threshold[i];
+          fe[1 + i] = (uint8_t)(pt.feature[i] | (pt.missing[i] << 7));
         }
       } else {
         // streamed: tree j at [(I + 1) j + 1] (front pad), else [I j]

@@ -2,8 +2,8 @@
 #include "traverse.cuh"
 
 namespace bridger {
-BRIDGER_STREAM_INSTANTIATE(long long, false)
-BRIDGER_STREAM_INSTANTIATE(long long, true)
-BRIDGER_STREAM_INSTANTIATE(double, false)
-BRIDGER_STREAM_INSTANTIATE(double, true)
+BRIDGER_STREAM_INSTANTIATE(long long, false, false)
+BRIDGER_STREAM_INSTANTIATE(long long, true, false)
+BRIDGER_STREAM_INSTANTIATE(double, false, false)
+BRIDGER_STREAM_INSTANTIATE(double, true, false)
 }  // namespace bridger

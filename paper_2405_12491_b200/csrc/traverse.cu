@@ -43,22 +43,25 @@ BRIDGER_TRAV_EXTERN(long long, false, false, 5)
 BRIDGER_TRAV_EXTERN(long long, true, false, 5)
 BRIDGER_TRAV_EXTERN(double, false, false, 5)
 BRIDGER_TRAV_EXTERN(double, true, false, 5)
-#define BRIDGER_STREAM_EXTERN_W(ACC, ML, W)                                                                         \
-  extern template cudaError_t launch_stream_t<1, ACC, ML, W, false>(const TravParams&, int, int, int, cudaStream_t);  \
-  extern template cudaError_t launch_stream_t<2, ACC, ML, W, false>(const TravParams&, int, int, int, cudaStream_t);  \
-  extern template cudaError_t launch_stream_t<4, ACC, ML, W, false>(const TravParams&, int, int, int, cudaStream_t);  \
-  extern template cudaError_t launch_stream_t<8, ACC, ML, W, false>(const TravParams&, int, int, int, cudaStream_t);  \
-  extern template cudaError_t launch_stream_t<16, ACC, ML, W, false>(const TravParams&, int, int, int, cudaStream_t); \
-  extern template cudaError_t launch_stream_t<64, ACC, ML, W, false>(const TravParams&, int, int, int, cudaStream_t); \
-  extern template cudaError_t launch_stream_t<1, ACC, ML, W, true>(const TravParams&, int, int, int, cudaStream_t);
-BRIDGER_STREAM_EXTERN_W(long long, false, 1)
-BRIDGER_STREAM_EXTERN_W(long long, true, 1)
-BRIDGER_STREAM_EXTERN_W(double, false, 1)
-BRIDGER_STREAM_EXTERN_W(double, true, 1)
-BRIDGER_STREAM_EXTERN_W(long long, false, 2)
-BRIDGER_STREAM_EXTERN_W(long long, true, 2)
-BRIDGER_STREAM_EXTERN_W(double, false, 2)
-BRIDGER_STREAM_EXTERN_W(double, true, 2)
+#define BRIDGER_STREAM_EXTERN_W(ACC, ML, W, SPL)                                                                         \
+  extern template cudaError_t launch_stream_t<1, ACC, ML, W, false, SPL>(const TravParams&, int, int, int, cudaStream_t);  \
+  extern template cudaError_t launch_stream_t<2, ACC, ML, W, false, SPL>(const TravParams&, int, int, int, cudaStream_t);  \
+  extern template cudaError_t launch_stream_t<4, ACC, ML, W, false, SPL>(const TravParams&, int, int, int, cudaStream_t);  \
+  extern template cudaError_t launch_stream_t<8, ACC, ML, W, false, SPL>(const TravParams&, int, int, int, cudaStream_t);  \
+  extern template cudaError_t launch_stream_t<16, ACC, ML, W, false, SPL>(const TravParams&, int, int, int, cudaStream_t); \
+  extern template cudaError_t launch_stream_t<64, ACC, ML, W, false, SPL>(const TravParams&, int, int, int, cudaStream_t); \
+  extern template cudaError_t launch_stream_t<1, ACC, ML, W, true, SPL>(const TravParams&, int, int, int, cudaStream_t);
+#define BRIDGER_STREAM_EXTERN_S(SPL)                \
+  BRIDGER_STREAM_EXTERN_W(long long, false, 1, SPL) \
+  BRIDGER_STREAM_EXTERN_W(long long, true, 1, SPL)  \
+  BRIDGER_STREAM_EXTERN_W(double, false, 1, SPL)    \
+  BRIDGER_STREAM_EXTERN_W(double, true, 1, SPL)     \
+  BRIDGER_STREAM_EXTERN_W(long long, false, 2, SPL) \
+  BRIDGER_STREAM_EXTERN_W(long long, true, 2, SPL)  \
+  BRIDGER_STREAM_EXTERN_W(double, false, 2, SPL)    \
+  BRIDGER_STREAM_EXTERN_W(double, true, 2, SPL)
+BRIDGER_STREAM_EXTERN_S(false)
+BRIDGER_STREAM_EXTERN_S(true)
 BRIDGER_TRAV_EXTERN(long long, false, true, 2)
 BRIDGER_TRAV_EXTERN(long long, true, true, 2)
 BRIDGER_TRAV_EXTERN(double, false, true, 2)
@@ -475,20 +478,23 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
       const int block_s = (L.stream_warps + 1) * 32;
       const bool w2 = W == 2;
       const bool ml = L.has_missing;
+      const bool spl = L.stream_split;
+#define BRIDGER_STA(ML, W)                                                                         \
+  (spl ? launch_stream_t<1, long long, ML, W, true, true>(p, grid_s, block_s, smem_s, st)          \
+       : launch_stream_t<1, long long, ML, W, true, false>(p, grid_s, block_s, smem_s, st))
+#define BRIDGER_STW(ACC, ML, W)                                                                    \
+  (spl ? launch_stream_t<KT, ACC, ML, W, false, true>(p, grid_s, block_s, smem_s, st)              \
+       : launch_stream_t<KT, ACC, ML, W, false, false>(p, grid_s, block_s, smem_s, st))
       if (want == 3) {
-        err = ml ? (w2 ? launch_stream_t<1, long long, true, 2, true>(p, grid_s, block_s, smem_s, st)
-                       : launch_stream_t<1, long long, true, 1, true>(p, grid_s, block_s, smem_s, st))
-                 : (w2 ? launch_stream_t<1, long long, false, 2, true>(p, grid_s, block_s, smem_s, st)
-                       : launch_stream_t<1, long long, false, 1, true>(p, grid_s, block_s, smem_s, st));
+        err = ml ? (w2 ? BRIDGER_STA(true, 2) : BRIDGER_STA(true, 1)) : (w2 ? BRIDGER_STA(false, 2) : BRIDGER_STA(false, 1));
       } else {
-#define BRIDGER_ST(ACC)                                                                      \
-  (ml ? (w2 ? launch_stream_t<KT, ACC, true, 2, false>(p, grid_s, block_s, smem_s, st)      \
-            : launch_stream_t<KT, ACC, true, 1, false>(p, grid_s, block_s, smem_s, st))     \
-      : (w2 ? launch_stream_t<KT, ACC, false, 2, false>(p, grid_s, block_s, smem_s, st)     \
-            : launch_stream_t<KT, ACC, false, 1, false>(p, grid_s, block_s, smem_s, st)))
+#define BRIDGER_ST(ACC) \
+  (ml ? (w2 ? BRIDGER_STW(ACC, true, 2) : BRIDGER_STW(ACC, true, 1)) : (w2 ? BRIDGER_STW(ACC, false, 2) : BRIDGER_STW(ACC, false, 1)))
         BRIDGER_DISPATCH_KT(m->K, { err = m->acc_int ? BRIDGER_ST(long long) : BRIDGER_ST(double); });
 #undef BRIDGER_ST
       }
+#undef BRIDGER_STA
+#undef BRIDGER_STW
     }
     cudaFreeAsync(xt, st);
     return err;

@@ -809,11 +809,55 @@ __device__ __forceinline__ void stream_walk(const uint2* nb, const float* xl, in
   for (int u = 0; u < W; ++u) idx[u] -= I;  // leaf index
 }
 
+// Split node format for streamed trees (F <= 127): per tree [pad][thresholds
+// 0..I-1] fp32 then [pad][features 0..I-1] u8 (bit 7 = missing_left), 5 * 2^D
+// bytes (vs 8 * 2^D): two trees fit a ring slot where one 8-byte-node tree
+// did, so every thread walks two trees at once.  Same child-pair speculation:
+// the children's thresholds (8 B) and features (2 B) are loaded with the
+// current node's feature value.
+template <int W, bool ML>
+__device__ __forceinline__ void stream_walk_split(const uint8_t* t0, int tb, const float* xl, int I, int D,
+                                                  int (&idx)[W]) {
+  float at[W];
+  uint32_t af[W];
+#pragma unroll
+  for (int u = 0; u < W; ++u) {
+    idx[u] = 0;
+    at[u] = reinterpret_cast<const float*>(t0 + u * tb)[1];
+    af[u] = (t0 + u * tb + (4 << D))[1];
+  }
+#pragma unroll 4
+  for (int lvl = 0; lvl < D; ++lvl) {
+    float x[W];
+    float2 tp[W];
+    uint32_t fp[W];
+#pragma unroll
+    for (int u = 0; u < W; ++u) {
+      x[u] = xl[(af[u] & 0x7Fu) * 32];
+      // unconditional (no branch in the level loop): at the last level the
+      // "children" are read past the tree's arrays -- still inside the ring /
+      // landing region of shared memory -- and discarded
+      tp[u] = *reinterpret_cast<const float2*>(reinterpret_cast<const float*>(t0 + u * tb) + 2 * idx[u] + 2);
+      fp[u] = *reinterpret_cast<const uint16_t*>(t0 + u * tb + (4 << D) + 2 * idx[u] + 2);
+    }
+#pragma unroll
+    for (int u = 0; u < W; ++u) {
+      int r = !(x[u] <= at[u]);  // NaN -> right (reading c2 default)
+      if (ML) r &= !((af[u] >> 7) & isnan(x[u]));
+      idx[u] = 2 * idx[u] + 1 + r;
+      at[u] = r ? tp[u].y : tp[u].x;
+      af[u] = r ? (fp[u] >> 8) : (fp[u] & 0xFFu);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < W; ++u) idx[u] -= I;  // leaf index
+}
+
 // W: trees walked together per pass (= the chunk width chosen at lowering; a
 // chunk's last pass masks trees past its end).  The steady-state loop has no
 // divergent branch: ptxas drains every load scoreboard at one, which would
 // serialise the leaf-gather latency the pipelining hides.
-template <int KT, typename ACC, bool ML, int W, bool APPLY>
+template <int KT, typename ACC, bool ML, int W, bool APPLY, bool SPL = false>
 __global__ void __launch_bounds__(544, 1) trav_stream_kernel(const TravParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -940,7 +984,12 @@ __global__ void __launch_bounds__(544, 1) trav_stream_kernel(const TravParams p)
         int idx[W];
         // trees past the chunk's end re-walk its last tree (masked below)
         const int jw = min(j, ch.n_trees - W < 0 ? 0 : ch.n_trees - W);
-        stream_walk<W, ML>(nodes + (size_t)jw * (I + 1) + 1, xl, I, D, idx);
+        if (SPL) {
+          const int tb = ((5 << D) + 15) & ~15;
+          stream_walk_split<W, ML>(reinterpret_cast<const uint8_t*>(nodes) + (size_t)jw * tb, tb, xl, I, D, idx);
+        } else {
+          stream_walk<W, ML>(nodes + (size_t)jw * (I + 1) + 1, xl, I, D, idx);
+        }
         if (APPLY) {
 #pragma unroll
           for (int u = 0; u < W; ++u) {
@@ -995,9 +1044,9 @@ __global__ void __launch_bounds__(544, 1) trav_stream_kernel(const TravParams p)
   }
 }
 
-template <int KT, typename ACC, bool ML, int W, bool APPLY>
+template <int KT, typename ACC, bool ML, int W, bool APPLY, bool SPL>
 cudaError_t launch_stream_t(const TravParams& p, int grid, int block, int smem, cudaStream_t st) {
-  auto kern = trav_stream_kernel<KT, ACC, ML, W, APPLY>;
+  auto kern = trav_stream_kernel<KT, ACC, ML, W, APPLY, SPL>;
   static int configured = 0;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
@@ -1015,18 +1064,18 @@ cudaError_t launch_stream_t(const TravParams& p, int grid, int block, int smem, 
   return cudaGetLastError();
 }
 
-#define BRIDGER_STREAM_INSTANTIATE_W(ACC, ML, W)                                                                  \
-  template cudaError_t launch_stream_t<1, ACC, ML, W, false>(const TravParams&, int, int, int, cudaStream_t);  \
-  template cudaError_t launch_stream_t<2, ACC, ML, W, false>(const TravParams&, int, int, int, cudaStream_t);  \
-  template cudaError_t launch_stream_t<4, ACC, ML, W, false>(const TravParams&, int, int, int, cudaStream_t);  \
-  template cudaError_t launch_stream_t<8, ACC, ML, W, false>(const TravParams&, int, int, int, cudaStream_t);  \
-  template cudaError_t launch_stream_t<16, ACC, ML, W, false>(const TravParams&, int, int, int, cudaStream_t); \
-  template cudaError_t launch_stream_t<64, ACC, ML, W, false>(const TravParams&, int, int, int, cudaStream_t);
-#define BRIDGER_STREAM_INSTANTIATE(ACC, ML)                                                                   \
-  BRIDGER_STREAM_INSTANTIATE_W(ACC, ML, 1)                                                                    \
-  BRIDGER_STREAM_INSTANTIATE_W(ACC, ML, 2)                                                                    \
-  template cudaError_t launch_stream_t<1, ACC, ML, 1, true>(const TravParams&, int, int, int, cudaStream_t); \
-  template cudaError_t launch_stream_t<1, ACC, ML, 2, true>(const TravParams&, int, int, int, cudaStream_t);
+#define BRIDGER_STREAM_INSTANTIATE_W(ACC, ML, W, SPL)                                                                  \
+  template cudaError_t launch_stream_t<1, ACC, ML, W, false, SPL>(const TravParams&, int, int, int, cudaStream_t);  \
+  template cudaError_t launch_stream_t<2, ACC, ML, W, false, SPL>(const TravParams&, int, int, int, cudaStream_t);  \
+  template cudaError_t launch_stream_t<4, ACC, ML, W, false, SPL>(const TravParams&, int, int, int, cudaStream_t);  \
+  template cudaError_t launch_stream_t<8, ACC, ML, W, false, SPL>(const TravParams&, int, int, int, cudaStream_t);  \
+  template cudaError_t launch_stream_t<16, ACC, ML, W, false, SPL>(const TravParams&, int, int, int, cudaStream_t); \
+  template cudaError_t launch_stream_t<64, ACC, ML, W, false, SPL>(const TravParams&, int, int, int, cudaStream_t);
+#define BRIDGER_STREAM_INSTANTIATE(ACC, ML, SPL)                                                                   \
+  BRIDGER_STREAM_INSTANTIATE_W(ACC, ML, 1, SPL)                                                                    \
+  BRIDGER_STREAM_INSTANTIATE_W(ACC, ML, 2, SPL)                                                                    \
+  template cudaError_t launch_stream_t<1, ACC, ML, 1, true, SPL>(const TravParams&, int, int, int, cudaStream_t); \
+  template cudaError_t launch_stream_t<1, ACC, ML, 2, true, SPL>(const TravParams&, int, int, int, cudaStream_t);
 
 #define BRIDGER_TRAV_INSTANTIATE(ACC, ML, GT, FMT)                                                                  \
   template cudaError_t launch_trav_t<1, ACC, ML, GT, FMT>(const TravParams&, int, int, int, int, cudaStream_t);  \

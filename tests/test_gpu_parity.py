@@ -263,11 +263,15 @@ def test_split_node_format(monkeypatch):
     check(m2, gen_x(2, 0, 9001, 28), apply=False)
 
 
-@pytest.mark.parametrize("n_rows", [77, 513, 148 * 512 + 333])
-def test_tree_streamed_c4_shape(n_rows):
+@pytest.mark.parametrize("split", ["1", "0"])
+@pytest.mark.parametrize("n_rows,n_trees", [(77, 6), (513, 7), (148 * 512 + 333, 6)])
+def test_tree_streamed_c4_shape(n_rows, n_trees, split, monkeypatch):
     # C4-shaped trees (depth 12, 8 classes: 164 KB per tree) exceed shared
-    # memory: tree-streamed mode (row tiles resident, node records streamed)
-    c, m = make_config("C4", n_trees=6)
+    # memory: tree-streamed mode (row tiles resident, node records streamed),
+    # split (5-byte, two trees per ring slot; odd tree counts leave a one-tree
+    # slot) or 8-byte node records
+    monkeypatch.setenv("BRIDGER_STREAM_SPLIT", split)
+    c, m = make_config("C4", n_trees=n_trees)
     g = B.Model(m)
     assert g.layout()["format"] == "stream"
     check(m, gen_x(4, 0, n_rows, 64), apply=n_rows < 1000)
@@ -275,7 +279,7 @@ def test_tree_streamed_c4_shape(n_rows):
 
 @pytest.mark.parametrize("ml", [False, True])
 def test_tree_streamed_pruned_missing_mixed_depth(ml):
-    m = perfect_ensemble(95, 9, 12, 64, kind="classification", n_classes=8, calib_rows=2048)
+    m = perfect_ensemble(95, 10, 12, 64, kind="classification", n_classes=8, calib_rows=2048)
     m = prune_ensemble(m, 95, p=0.003, with_missing=ml)  # heavier pruning selects the sparse layout
     g = B.Model(m)
     assert g.layout()["format"] == "stream"

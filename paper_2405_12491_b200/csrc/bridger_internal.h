@@ -104,6 +104,7 @@ struct TravLayout {
   int32_t stream_warps = 0;     //   walking warps (rows per tile / 32)
   int32_t stream_w = 1;         //   trees walked together per pass
   bool stream_split = false;    //   split node records (fp32 thresholds + u8 features, 5 * 2^D B per tree)
+  int32_t stream_slack = 0;     //   bytes after the ring the split walk's last-level child loads may read
   std::vector<uint32_t> hyb_nodes;  // [records][2] deep levels of every tree (slot order)
   std::vector<float> hyb_leaves;    // [slots][L][K]
   std::vector<SparseTree> sparse_trees;

@@ -435,7 +435,7 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
     const int32_t base_budget = kSmemMax - misc - trav_x_region(codes, F, nb);
     auto chunk_bytes = [&](int32_t n, int32_t D) -> int64_t {
       const int64_t nodes = (int64_t)n * ((1 << D) - 1) * node_bytes + (node_bytes == 5 ? 16 : 0);
-      return (nodes + 15) / 16 * 16 + ((int64_t)n * (1 << D) * K * 4 + 15) / 16 * 16;
+      return (nodes + 31) / 32 * 32 + ((int64_t)n * (1 << D) * K * 4 + 15) / 16 * 16;
     };
     out->global_trees = false;
     int32_t n_prev = 1;
@@ -594,6 +594,7 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
   out->chunk_budget = budget;
   out->stream = false;
   out->stream_split = false;
+  out->stream_slack = 0;
   if (out->global_trees && !out->sparse) {
     // Tree-streamed mode (traverse.cuh K4s): rows resident, node records of
     // chunks of <= 4 equal-depth trees streamed through a 3-slot ring; leaves
@@ -628,7 +629,11 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
     const int32_t w = (min_n >= 2 && K <= 8) ? 2 : 1;  // trees per pass (every chunk holds >= w)
     // shared memory: X tile (32 rows per warp) + ring + per-thread leaf slots
     auto fits = [&](int32_t wp) {
-      return (int64_t)wp * 32 * F * 4 + ns * stage + (int64_t)wp * 32 * w * K * 4 + 1024 <= kSmemMax;
+      const int64_t landing = (int64_t)wp * 32 * w * K * 4;
+      // split walk: the discarded last-level child loads read <= 3*2^D bytes
+      // past a tree, i.e. into the landing slots after the ring; pad if short
+      const int64_t slack = spl ? std::max<int64_t>(0, ((int64_t)3 << Dmax) + 64 - landing) : 0;
+      return (int64_t)wp * 32 * F * 4 + ns * stage + landing + slack + 1024 <= kSmemMax;
     };
     int32_t warps = 16;
     while (warps > 4 && !fits(warps)) --warps;
@@ -639,6 +644,7 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
       out->stream_warps = warps;
       out->stream_w = w;
       out->stream_split = spl;
+      out->stream_slack = spl ? (int32_t)std::max<int64_t>(0, ((int64_t)3 << Dmax) + 64 - (int64_t)warps * 32 * w * K * 4) : 0;
       bal.swap(pieces);
     }
   }
@@ -666,7 +672,7 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
     const int64_t nodes = out->split ? (((int64_t)r.n * I * 4 + 15) / 16 * 16 + (int64_t)r.n * I)
                           : out->stream ? (int64_t)r.n * (out->stream_split ? ((((int64_t)5 << D) + 15) / 16 * 16) : (int64_t)(I + 1) * 8)
                                         : (int64_t)r.n * I * node_bytes;
-    c.leaf_offset = (int32_t)((nodes + 15) / 16 * 16);
+    c.leaf_offset = (int32_t)((nodes + 31) / 32 * 32);  // 32-byte aligned leaf vectors (256-bit gathers)
     c.bytes = (int32_t)(c.leaf_offset + ((int64_t)r.n * L * K * 4 + 15) / 16 * 16);
     out->data.resize(off + c.bytes, 0);
     uint8_t* base = out->data.data() + off;

@@ -472,7 +472,10 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
       p.stream_x_bytes = rb * m->F * 4;
       const int W = L.stream_w;
       p.stream_lbuf_bytes = (rb * W * m->K * 4 + 15) / 16 * 16;
-      const int smem_s = p.stream_x_bytes + L.stream_ns * L.stream_stage + p.stream_lbuf_bytes + (1 + 2 * L.stream_ns) * 8 + 16;
+      // ring | landing slots | [split: slack for the walk's discarded last-level child loads] | barriers
+      const int smem_s = p.stream_x_bytes + L.stream_ns * L.stream_stage + p.stream_lbuf_bytes + L.stream_slack +
+                         (1 + 2 * L.stream_ns) * 8 + 16;
+      p.stream_lbuf_bytes += L.stream_slack;  // barriers sit after the slack
       const int64_t n_tiles = (n_rows + rb - 1) / rb;
       const int grid_s = (int)std::max<int64_t>(1, std::min<int64_t>(n_tiles, sms));
       const int block_s = (L.stream_warps + 1) * 32;

@@ -257,9 +257,10 @@ def main():
     from synth import gen_x, gen_x_torch, make_config
 
     world, rank, local = dist_env()
-    if world > 1:
-        dist.init_process_group("nccl")
     torch.cuda.set_device(local)
+    if world > 1:
+        # bind the process group to this rank's GPU before the first collective
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     cfg, m = make_config(args.config, n_trees=args.trees)
     if args.rows or args.trees:

@@ -71,34 +71,13 @@ BRIDGER_TRAV_EXTERN(double, true, true, 2)
 // codes [n_blocks][F2/2][32][2] u16 (F2 = F rounded up to even; feature pairs
 // interleaved per lane so that the traversal's per-lane code loads hit bank
 // `lane` for ANY feature), code = #{u in U_f : u < x}, NaN -> 0xFFFF.
-// lane = row; for 8 features at a time (8 independent chains) each lane
-// descends the features' k-level Eytzinger search trees in shared memory:
-// i <- 2i + 1 + [E_f[i] < x] (all lanes of a warp search the same feature, so
-// the top levels are broadcasts); the leaf reached, i - (2^k - 1), is the code
-// (lowering.cpp).  STAGE: each warp bulk-copies its dense [32][F] blocks into
-// shared memory (double buffered); otherwise (tables too large to leave room
-// for staging) lanes read their row's 8 features straight from global memory,
-// one slice ahead.
-template <int V>
-__device__ __forceinline__ void load_slice(const float* xr, int f0, int F, float (&x)[8]) {
-  if (V == 4 && f0 + 8 <= F) {
-    const float4 a = *reinterpret_cast<const float4*>(xr + f0);
-    const float4 b = *reinterpret_cast<const float4*>(xr + f0 + 4);
-    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
-  } else if (V == 2 && f0 + 8 <= F) {
-#pragma unroll
-    for (int u = 0; u < 8; u += 2) {
-      const float2 a = *reinterpret_cast<const float2*>(xr + f0 + u);
-      x[u] = a.x;
-      x[u + 1] = a.y;
-    }
-  } else {
-#pragma unroll
-    for (int u = 0; u < 8; ++u) x[u] = f0 + u < F ? xr[f0 + u] : 0.f;
-  }
-}
-
-template <int V, bool STAGE>
+// lane = row; each warp bulk-copies dense [32][F] blocks (double buffered) and
+// descends, for NP feature pairs at a time (2 NP independent chains, passes
+// sized so no chain is wasted: C2's 14 pairs = 2 passes of 7), the features'
+// k-level Eytzinger search trees in shared memory: i <- 2i + 1 + [E_f[i] < x]
+// (all lanes of a warp search the same feature, so the top levels are
+// broadcasts).  The leaf reached, i - (2^k - 1), is the code (lowering.cpp).
+template <int NP, int V>
 __global__ void __launch_bounds__(512, 1) bin_kernel(const float* __restrict__ X, int64_t n_rows, int32_t F,
                                                      const float* __restrict__ table, int32_t k,
                                                      uint32_t* __restrict__ codes) {
@@ -109,7 +88,7 @@ __global__ void __launch_bounds__(512, 1) bin_kernel(const float* __restrict__ X
   const size_t tab_bytes = ((size_t)F * P * 4 + 127) / 128 * 128;
   const uint32_t blk_bytes = 128u * (uint32_t)F;  // dense [32][F] fp32
   float* stage = reinterpret_cast<float*>(smem + tab_bytes + (size_t)warp * 2 * blk_bytes);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + tab_bytes + (STAGE ? (size_t)NW * 2 * blk_bytes : 0)) + 2 * warp;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + tab_bytes + (size_t)NW * 2 * blk_bytes) + 2 * warp;
   {
     const float4* src = reinterpret_cast<const float4*>(table);
     float4* dst = reinterpret_cast<float4*>(smem);
@@ -117,7 +96,7 @@ __global__ void __launch_bounds__(512, 1) bin_kernel(const float* __restrict__ X
     for (int i = threadIdx.x; i < n4; i += blockDim.x) dst[i] = src[i];
     for (int i = n4 * 4 + threadIdx.x; i < F * P; i += blockDim.x) reinterpret_cast<float*>(smem)[i] = table[i];
   }
-  if (STAGE && lane == 0) {
+  if (lane == 0) {
     ptx::mbar_init(&bars[0], 1);
     ptx::mbar_init(&bars[1], 1);
     ptx::fence_barrier_init();
@@ -128,7 +107,7 @@ __global__ void __launch_bounds__(512, 1) bin_kernel(const float* __restrict__ X
   const int64_t gstride = (int64_t)gridDim.x * NW;
   int64_t blk = (int64_t)blockIdx.x * NW + warp;
   auto issue = [&](int64_t b, int buf) {
-    if (STAGE && lane == 0 && b < n_blocks && (b + 1) * 32 <= n_rows) {
+    if (lane == 0 && b < n_blocks && (b + 1) * 32 <= n_rows) {
       ptx::fence_proxy_async();
       ptx::mbar_arrive_expect_tx(&bars[buf], blk_bytes);
       ptx::bulk_g2s(stage + (size_t)buf * 32 * F, X + b * 32 * (int64_t)F, blk_bytes, &bars[buf]);
@@ -138,49 +117,50 @@ __global__ void __launch_bounds__(512, 1) bin_kernel(const float* __restrict__ X
   uint32_t phase = 0;  // bit b: parity of buffer b
   for (int it = 0; blk < n_blocks; blk += gstride, ++it) {
     const int buf = it & 1;
+    float* St = stage + (size_t)buf * 32 * F;
     const int64_t row0 = blk * 32;
-    const float* xr;
-    if (STAGE) {
-      float* St = stage + (size_t)buf * 32 * F;
-      if (row0 + 32 <= n_rows) {
-        ptx::mbar_wait(&bars[buf], (phase >> buf) & 1u);
-        phase ^= 1u << buf;
-      } else {
-        const int rows = (int)(n_rows - row0);
-        const float* src = X + row0 * F;
-        for (int e = lane; e < 32 * F; e += 32) St[e] = e < rows * F ? src[e] : 0.f;
-        __syncwarp();
-      }
-      issue(blk + gstride, buf ^ 1);  // the other buffer was drained by the previous block
-      xr = St + (size_t)lane * F;
+    if (row0 + 32 <= n_rows) {
+      ptx::mbar_wait(&bars[buf], (phase >> buf) & 1u);
+      phase ^= 1u << buf;
     } else {
-      xr = X + (row0 + lane < n_rows ? row0 + lane : row0) * (int64_t)F;
+      const int rows = (int)(n_rows - row0);
+      const float* src = X + row0 * F;
+      for (int e = lane; e < 32 * F; e += 32) St[e] = e < rows * F ? src[e] : 0.f;
+      __syncwarp();
     }
+    issue(blk + gstride, buf ^ 1);  // the other buffer was drained by the previous block
+    const float* xr = St + (size_t)lane * F;
     uint32_t* dst = codes + (size_t)blk * F2h * 32 + lane;
-    float xn[8];
-    load_slice<V>(xr, 0, F, xn);
-    for (int f0 = 0; f0 < 2 * F2h; f0 += 8) {
-      float x[8];
+    for (int f0 = 0; f0 < 2 * F2h; f0 += 2 * NP) {
+      float x[2 * NP];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) x[u] = xn[u];
-      if (f0 + 8 < 2 * F2h) load_slice<V>(xr, f0 + 8, F, xn);  // one slice ahead
-      // shared address A of the current search-tree node; A' = 2A + (E < x ? c8 : c4)
-      uint32_t A[8], c4[8], c8[8];
+      for (int u = 0; u < 2 * NP; u += 2) {
+        if (V == 2 && f0 + u + 1 < F) {
+          const float2 v = *reinterpret_cast<const float2*>(xr + f0 + u);  // F even: 8-byte aligned
+          x[u] = v.x;
+          x[u + 1] = v.y;
+        } else {
+          x[u] = f0 + u < F ? xr[f0 + u] : 0.f;
+          x[u + 1] = f0 + u + 1 < F ? xr[f0 + u + 1] : 0.f;
+        }
+      }
+      // shared address A of the current search-tree node; A' = 2A + c4 (+ 4 if E < x)
+      uint32_t A[2 * NP], c4[2 * NP];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < 2 * NP; ++u) {
         A[u] = tab_s + (uint32_t)(min(f0 + u, F - 1) * P) * 4u;
         c4[u] = 4u - A[u];
-        c8[u] = 8u - A[u];
       }
       for (int s = 0; s < k; ++s) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < 2 * NP; ++u) {
           const float e = ptx::lds_f32(A[u]);
-          A[u] = 2u * A[u] + (e < x[u] ? c8[u] : c4[u]);
+          A[u] = 2u * A[u] + c4[u];
+          if (e < x[u]) A[u] += 4u;
         }
       }
 #pragma unroll
-      for (int u = 0; u < 8; u += 2) {
+      for (int u = 0; u < 2 * NP; u += 2) {
         if (f0 + u < 2 * F2h) {
           // leaf byte offset A + c4 - 4 = 4 (2^k - 1 + code)
           const uint32_t c0 = isnan(x[u]) ? 0xFFFFu : ((A[u] + c4[u] - 4u) >> 2) - (uint32_t)P;
@@ -559,14 +539,19 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
     }
     if (!stage) nwb = 16;
     const int bsmem = fixed + (stage ? nwb * (2 * 128 * m->F + 16) : coop ? 2 * 128 * m->F + 32 : 0);
-    const int vi = (m->F % 4 == 0) ? 2 : (m->F % 2 == 0) ? 1 : 0;
-    void (*kerns[2][3])(const float*, int64_t, int32_t, const float*, int32_t, uint32_t*) = {
-        {bin_kernel<1, false>, bin_kernel<2, false>, bin_kernel<4, false>},
-        {bin_kernel<1, true>, bin_kernel<2, true>, bin_kernel<4, true>}};
-    const int np = std::min(4, (((m->F + 1) >> 1) + nwb - 1) / nwb);  // pairs per warp pass (coop)
-    void (*coops[4])(const float*, int64_t, int32_t, const float*, int32_t, uint32_t*) = {
-        bin_coop_kernel<1>, bin_coop_kernel<2>, bin_coop_kernel<3>, bin_coop_kernel<4>};
-    auto bk = coop ? coops[np - 1] : kerns[stage ? 1 : 0][vi];
+    // staged kernel: NP pairs per pass, passes sized so that no chain is wasted
+    const int f2h = (m->F + 1) >> 1;
+    const int npass = (f2h + 6) / 7;
+    const int nps = (f2h + npass - 1) / npass;  // 1..7
+    using BinK = void (*)(const float*, int64_t, int32_t, const float*, int32_t, uint32_t*);
+    const BinK kerns[2][7] = {
+        {bin_kernel<1, 1>, bin_kernel<2, 1>, bin_kernel<3, 1>, bin_kernel<4, 1>, bin_kernel<5, 1>, bin_kernel<6, 1>,
+         bin_kernel<7, 1>},
+        {bin_kernel<1, 2>, bin_kernel<2, 2>, bin_kernel<3, 2>, bin_kernel<4, 2>, bin_kernel<5, 2>, bin_kernel<6, 2>,
+         bin_kernel<7, 2>}};
+    const int np = std::min(4, (f2h + nwb - 1) / nwb);  // pairs per warp pass (coop)
+    const BinK coops[4] = {bin_coop_kernel<1>, bin_coop_kernel<2>, bin_coop_kernel<3>, bin_coop_kernel<4>};
+    auto bk = coop ? coops[np - 1] : kerns[m->F % 2 == 0 ? 1 : 0][nps - 1];
     int bsm = bsmem;
     int64_t want_ctas = coop ? nbk : (nbk + nwb - 1) / nwb;
     int fgsz = 0;

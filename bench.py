@@ -375,7 +375,9 @@ def main():
         roof = {"bound": "alu", "resource": "shared-memory (LSU) pipe bandwidth",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
                 "kernel": "trav_kernel", "kernel_ms": hot_avg,
-                "node_format": "threshold-bin codes (4 B nodes, u16 inputs; bin_kernel pass)" if coded else "fp32 (8 B nodes)",
+                "node_format": ("threshold-bin codes (4 B nodes, u16 inputs; bin_kernel pass)" if coded
+                                else "tree-streamed, fp32 thresholds" if model.layout().get("format") == "stream"
+                                else "fp32 (8 B nodes)"),
                 "visits_per_s": n * model.n_trees * cfg.depth / (hot_avg / 1e3),
                 "hbm_frac": (n * cfg.n_features * 4 + n * 4) / (hot_avg / 1e3) / 1e9 / peaks["hbm_gbs"],
                 "peak_source": psrc}

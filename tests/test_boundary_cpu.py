@@ -182,3 +182,28 @@ def test_exactness_tiers_match_definition():
     m = make_config("C1")[1]
     v = m.value.copy(); v[-1] = 1.4e-45                      # subnormal -> q = -149 -> M >= 2^63
     assert B.analyze_exactness(ModelDesc(**{**m.__dict__, "value": v}))[1] == "F64"
+
+
+def test_no_fallback_without_library(tmp_path):
+    """The product path fails loudly without its CUDA library: a copy of the
+    package with no libbridger.so refuses to import (no CPU fallback)."""
+    import shutil
+    import subprocess
+    import sys
+    pkg = os.path.dirname(B.__file__)
+    dst = tmp_path / "paper_2405_12491_b200"
+    shutil.copytree(pkg, dst, ignore=shutil.ignore_patterns("*.so", "build", "__pycache__", "csrc"))
+    r = subprocess.run([sys.executable, "-c", "import paper_2405_12491_b200"], cwd=tmp_path,
+                       capture_output=True, text=True)
+    assert r.returncode != 0
+    assert "libbridger" in (r.stderr + r.stdout)
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="checks the no-device error path")
+def test_no_device_is_a_cuda_error():
+    """Without a GPU, loading a model returns BRIDGER_E_CUDA (the oracle is
+    never consulted)."""
+    c, m = make_config("C1")
+    with pytest.raises(B.BridgerError) as ei:
+        B.Model(m, device=0)
+    assert ei.value.status == B.E_CUDA

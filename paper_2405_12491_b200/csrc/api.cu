@@ -84,17 +84,19 @@ static cudaError_t upload(T** dst, const T* src, size_t n) {
   return cudaMemcpy(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice);
 }
 
+constexpr int kHostStages = 3;
 struct HostCtx {
-  cudaStream_t st[2] = {nullptr, nullptr};
-  float* dX[2] = {nullptr, nullptr};
-  void* dO[2] = {nullptr, nullptr};
+  cudaStream_t st[kHostStages] = {};
+  float* dX[kHostStages] = {};
+  void* dO[kHostStages] = {};
+  int stages = 2;
   int64_t rows = 0;       // capacity in rows per stage
   size_t out_row = 0;     // capacity in output bytes per row
 };
 
 static void free_host_ctx(HostCtx* c) {
   if (!c) return;
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < kHostStages; ++i) {
     if (c->st[i]) cudaStreamSynchronize(c->st[i]);
     cudaFree(c->dX[i]);
     cudaFree(c->dO[i]);
@@ -462,20 +464,25 @@ bridger_status bridger_predict_host(const bridger_model* m, const float* X_host,
   else out_row_bytes = 4;
   // stages of ~32 MiB of X: each H2D is large, and compute of stage i overlaps
   // the copies of stage i+1 on the other stream
-  int64_t chunk = std::max<int64_t>(1024, ((int64_t)32 << 20) / (4 * (int64_t)m->F));
+  int64_t stage_mb = 32;
+  int stages = 2;
+  if (const char* ev = std::getenv("BRIDGER_H2D_MB")) stage_mb = std::max(1, std::atoi(ev));  // experiments
+  if (const char* ev = std::getenv("BRIDGER_H2D_STAGES")) stages = std::max(2, std::min(kHostStages, std::atoi(ev)));
+  int64_t chunk = std::max<int64_t>(1024, (stage_mb << 20) / (4 * (int64_t)m->F));
   chunk = (chunk + 31) / 32 * 32;
   if (chunk > n_rows) chunk = (n_rows + 31) / 32 * 32;
   bridger_model* mm = const_cast<bridger_model*>(m);
   std::lock_guard<std::mutex> lock(mm->host_mu);
   HostCtx* c = static_cast<HostCtx*>(mm->host_ctx);
   cudaError_t e = cudaSuccess;
-  if (!c || c->rows < chunk || c->out_row < out_row_bytes) {
+  if (!c || c->rows < chunk || c->out_row < out_row_bytes || c->stages != stages) {
     free_host_ctx(c);
     c = new HostCtx();
     mm->host_ctx = c;
     c->rows = std::max<int64_t>(chunk, c->rows);
     c->out_row = std::max<size_t>(out_row_bytes, 4 * (size_t)(m->K < 2 ? 2 : m->K));
-    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    c->stages = stages;
+    for (int i = 0; i < stages && e == cudaSuccess; ++i) {
       e = cudaStreamCreateWithFlags(&c->st[i], cudaStreamNonBlocking);
       if (e == cudaSuccess) e = cudaMalloc(&c->dX[i], (size_t)c->rows * m->F * 4);
       if (e == cudaSuccess) e = cudaMalloc(&c->dO[i], (size_t)c->rows * c->out_row);
@@ -489,7 +496,7 @@ bridger_status bridger_predict_host(const bridger_model* m, const float* X_host,
   bridger_status rs = BRIDGER_OK;
   for (int64_t r0 = 0, i = 0; e == cudaSuccess && r0 < n_rows; r0 += chunk, ++i) {
     const int64_t rows = std::min(chunk, n_rows - r0);
-    const int b = (int)(i & 1);
+    const int b = (int)(i % c->stages);
     e = cudaMemcpyAsync(c->dX[b], X_host + r0 * m->F, (size_t)rows * m->F * 4, cudaMemcpyHostToDevice, c->st[b]);
     if (e != cudaSuccess) break;
     rs = run(m, c->dX[b], rows, n_features, c->dO[b], want, c->st[b]);
@@ -497,7 +504,7 @@ bridger_status bridger_predict_host(const bridger_model* m, const float* X_host,
     e = cudaMemcpyAsync(static_cast<uint8_t*>(out_host) + r0 * out_row_bytes, c->dO[b], (size_t)rows * out_row_bytes,
                         cudaMemcpyDeviceToHost, c->st[b]);
   }
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < c->stages; ++i) {
     cudaError_t e2 = cudaStreamSynchronize(c->st[i]);
     if (e == cudaSuccess) e = e2;
   }

@@ -233,7 +233,7 @@ static constexpr int32_t kSmemMax = 232448;  // 227 KB opt-in per block (sm_100)
 // code(x) = #{u in U_f : u < x} (NaN -> 0xFFFF), and a node's threshold t =
 // U_f[j] becomes j.  For every non-NaN x:  x <= U_f[j]  <=>  code(x) <= j
 // (the thresholds below x are exactly U_f[0..code(x)-1]), so the comparison is
-// unchanged bit for bit.  Eligible when F <= 512 and every |U_f| <= 32767
+// unchanged bit for bit.  Eligible when F <= 512 and every |U_f| <= 65534
 // (codes and node indices fit 15 bits).  The device search structure is, per
 // feature, U_f laid out as a complete binary search tree in BFS (Eytzinger)
 // order with 2^k - 1 slots (k uniform over the features so every lane of a
@@ -266,7 +266,7 @@ static bool build_bin_table(const bridger_model_desc* d, TravLayout* out) {
     std::sort(v.begin(), v.end());
     // -0.0 and +0.0 compare equal: keep one
     v.erase(std::unique(v.begin(), v.end(), [](float a, float b) { return a == b; }), v.end());
-    if (v.size() > 32767) return false;
+    if (v.size() > 65534) return false;  // codes 0..|U_f| and NaN = 0xFFFF in 16 bits
     nmax = std::max(nmax, v.size());
   }
   int32_t k = 1;
@@ -680,9 +680,9 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
       const int32_t t = order[r.start + j];
       pad_tree(d, t, D, &pt);
       if (out->codes) {
-        // node word: code index j (bits 16..30) | missing (bit 15) | byte
-        // offset of the feature's code within a lane's view of a [F/2][32][2]
-        // u16 code block (bits 0..14: (f/2)*128 + (f%2)*2, F <= 512)
+        // node word: code index j (bits 16..31) | byte offset of the feature's
+        // code within a lane's view of a [F/2][32][2] u16 code block (bits
+        // 1..14: (f/2)*128 + (f%2)*2, always even, F <= 512) | missing (bit 0)
         uint32_t* nd = reinterpret_cast<uint32_t*>(base) + (size_t)j * I;
         for (int32_t i = 0; i < I; ++i) {
           // real nodes: t is in U_f, exact index; dummy nodes under replicated
@@ -690,7 +690,7 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
           const int32_t f = pt.feature[i];
           const uint32_t code = code_of_threshold(*out, f, pt.threshold[i]);
           const uint32_t foff = (uint32_t)(f >> 1) * 128u + (uint32_t)(f & 1) * 2u;
-          nd[i] = (code << 16) | ((uint32_t)pt.missing[i] << 15) | foff;
+          nd[i] = (code << 16) | foff | (uint32_t)pt.missing[i];
         }
       } else if (out->split) {
         float* th = reinterpret_cast<float*>(base) + (size_t)j * I;

@@ -284,17 +284,19 @@ __global__ void __launch_bounds__(512, 1) bin_coop_kernel(const float* __restric
 
 // Feature-group binning for search tables too large to hold for all features
 // at once (C5-shaped shards: 200 features x 8191-slot trees = 6.5 MB): a CTA
-// owns FG features (their tables in shared memory) and a range of 32-row
-// blocks; lane = row reads its row's FG contiguous values straight from global
-// memory and descends FG search trees (FG chains).  FG is 4 or 2 (whole code
-// pairs: one coalesced u32 store per pair), or 1 (u16 stores).
+// owns FG features and a range of 32-row blocks; lane = row reads its row's FG
+// contiguous values straight from global memory and descends FG search trees
+// (FG chains).  The top T levels of each tree -- the first 2^T - 1 slots of the
+// Eytzinger array -- sit in shared memory; deeper levels (T < k: tables of
+// 2^16 - 1 slots, 256 KB per feature) are read from global memory (L2).  FG is
+// 4 or 2 (whole code pairs: one coalesced u32 store per pair), or 1 (u16 stores).
 template <int FG>
 __global__ void __launch_bounds__(512, 1) bin_fg_kernel(const float* __restrict__ X, int64_t n_rows, int32_t F,
-                                                        const float* __restrict__ table, int32_t k,
+                                                        const float* __restrict__ table, int32_t k, int32_t T,
                                                         uint32_t* __restrict__ codes) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
-  const int P = (1 << k) - 1;
+  const int P = (1 << k) - 1, Pt = (1 << T) - 1;
   const int F2h = (F + 1) >> 1;
   const int n_fg = (F + FG - 1) / FG;
   const int fg = blockIdx.x % n_fg;
@@ -302,9 +304,8 @@ __global__ void __launch_bounds__(512, 1) bin_fg_kernel(const float* __restrict_
   const int f0 = fg * FG;
   const int nf = min(FG, F - f0);
   {
-    const float* src = table + (size_t)f0 * P;
     float* dst = reinterpret_cast<float*>(smem);
-    for (int i = threadIdx.x; i < nf * P; i += blockDim.x) dst[i] = src[i];
+    for (int i = threadIdx.x; i < nf * Pt; i += blockDim.x) dst[i] = table[(size_t)(f0 + i / Pt) * P + i % Pt];
   }
   __syncthreads();
   const uint32_t tab_s = ptx::s2u(smem);
@@ -318,10 +319,10 @@ __global__ void __launch_bounds__(512, 1) bin_fg_kernel(const float* __restrict_
     uint32_t A[FG], c4[FG];
 #pragma unroll
     for (int u = 0; u < FG; ++u) {
-      A[u] = tab_s + (uint32_t)(min(u, nf - 1) * P) * 4u;
+      A[u] = tab_s + (uint32_t)(min(u, nf - 1) * Pt) * 4u;
       c4[u] = 4u - A[u];
     }
-    for (int s = 0; s < k; ++s) {
+    for (int s = 0; s < T; ++s) {
 #pragma unroll
       for (int u = 0; u < FG; ++u) {
         const float e = ptx::lds_f32(A[u]);
@@ -329,10 +330,19 @@ __global__ void __launch_bounds__(512, 1) bin_fg_kernel(const float* __restrict_
         if (e < x[u]) A[u] += 4u;
       }
     }
+    uint32_t i[FG];  // Eytzinger index after T levels
+#pragma unroll
+    for (int u = 0; u < FG; ++u) i[u] = (A[u] + c4[u] - 4u) >> 2;
+    for (int s = T; s < k; ++s) {
+#pragma unroll
+      for (int u = 0; u < FG; ++u) {
+        const float e = __ldg(table + (size_t)(f0 + min(u, nf - 1)) * P + i[u]);
+        i[u] = 2u * i[u] + 1u + (e < x[u] ? 1u : 0u);
+      }
+    }
     uint32_t cd[FG];
 #pragma unroll
-    for (int u = 0; u < FG; ++u)
-      cd[u] = u >= nf ? 0u : isnan(x[u]) ? 0xFFFFu : ((A[u] + c4[u] - 4u) >> 2) - (uint32_t)P;
+    for (int u = 0; u < FG; ++u) cd[u] = u >= nf ? 0u : isnan(x[u]) ? 0xFFFFu : i[u] - (uint32_t)P;
     uint32_t* dst = codes + (size_t)blk * F2h * 32 + lane;
     if (FG == 1) {
       reinterpret_cast<uint16_t*>(dst + (size_t)(f0 >> 1) * 32)[f0 & 1] = (uint16_t)cd[0];
@@ -554,12 +564,14 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
     auto bk = coop ? coops[np - 1] : kerns[m->F % 2 == 0 ? 1 : 0][nps - 1];
     int bsm = bsmem;
     int64_t want_ctas = coop ? nbk : (nbk + nwb - 1) / nwb;
-    int fgsz = 0;
+    int fgsz = 0, fg_levels = 0;
     if (!stage && !coop) {
-      // feature groups: FG features' tables per CTA, whole code pairs when they fit
-      fgsz = 4 * P * 4 <= 200 * 1024 ? 4 : 2 * P * 4 <= 200 * 1024 ? 2 : 1;
-      bk = fgsz == 4 ? bin_fg_kernel<4> : fgsz == 2 ? bin_fg_kernel<2> : bin_fg_kernel<1>;
-      bsm = fgsz * P * 4;
+      // feature groups: FG features' tables per CTA, whole code pairs when they
+      // fit; 2^16-slot tables: pairs with their top 14 levels in shared memory
+      fgsz = 4 * P * 4 <= 200 * 1024 ? 4 : 2 * P * 4 <= 200 * 1024 ? 2 : P * 4 <= 200 * 1024 ? 1 : 2;
+      fg_levels = L.bin_k;
+      while (fgsz * ((1 << fg_levels) - 1) * 4 > 200 * 1024) --fg_levels;
+      bsm = fgsz * ((1 << fg_levels) - 1) * 4;
       const int n_fg = (m->F + fgsz - 1) / fgsz;
       // slices of row blocks per feature group: fill the SMs, each slice >= 16 blocks
       const int64_t slices = std::max<int64_t>(1, std::min<int64_t>((2 * sms + n_fg - 1) / n_fg, (nbk + 15) / 16));
@@ -571,7 +583,14 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bk, nwb * 32, bsm);
     const int bgrid = fgsz ? (int)want_ctas
                            : (int)std::max<int64_t>(1, std::min<int64_t>(want_ctas, (int64_t)sms * std::max(1, occ)));
-    bk<<<bgrid, nwb * 32, bsm, st>>>(X, n_rows, m->F, m->d_bin_table, L.bin_k, static_cast<uint32_t*>(codes));
+    if (fgsz) {
+      auto fk = fgsz == 4 ? bin_fg_kernel<4> : fgsz == 2 ? bin_fg_kernel<2> : bin_fg_kernel<1>;
+      cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+      fk<<<bgrid, nwb * 32, bsm, st>>>(X, n_rows, m->F, m->d_bin_table, L.bin_k, fg_levels,
+                                       static_cast<uint32_t*>(codes));
+    } else {
+      bk<<<bgrid, nwb * 32, bsm, st>>>(X, n_rows, m->F, m->d_bin_table, L.bin_k, static_cast<uint32_t*>(codes));
+    }
     count_launch();
     err = cudaGetLastError();
     if (err != cudaSuccess) {

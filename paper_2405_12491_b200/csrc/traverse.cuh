@@ -136,10 +136,10 @@ __device__ __forceinline__ void walk_trees(const TravParams& p, const TravChunk&
       }
     }
   } else if (CODES) {
-    // 4-byte node: code index j (30..16) | missing (15) | feature byte offset
-    // (14..0) within a lane's view of a [F/2][32][2] u16 code block.  xl is
-    // this lane's 4-byte column of a 2^b-aligned block buffer, so the code
-    // address is (xl | (a & (2^b - 1))): bank `lane` for any feature, one LOP3.
+    // 4-byte node: code index j (31..16) | feature byte offset (14..1, even)
+    // within a lane's view of a [F/2][32][2] u16 code block | missing (0).
+    // xl is this lane's 4-byte column of a 2^b-aligned block buffer, so the
+    // code address is (xl | (a & (2^b - 2))): bank `lane` for any feature, one LOP3.
     // code(x) > j  <=>  x * 2^16 > a  (the low half of a is < 2^16), so the
     // compare needs no field extraction.  Node addresses are shared-window byte
     // addresses: node idx of tree u at A = base_u + 4 idx, and
@@ -148,7 +148,7 @@ __device__ __forceinline__ void walk_trees(const TravParams& p, const TravChunk&
     // the FMA pipe; the LOP3 / compare / select use the ALU pipe.
     const uint32_t nb = ptx::s2u(nodes) + 4u * (uint32_t)(j * I);
     const uint32_t xb = ptx::s2u(xl);
-    const uint32_t mask = (uint32_t)p.code_buf - 1u;
+    const uint32_t mask = (uint32_t)p.code_buf - 2u;  // feature offset bits, not the missing bit
     const uint32_t k2 = p.k2, k16 = p.k16;
     uint32_t A[NI], cb[NI];  // cb = 4 - base_u:  A' = A * 2 + cb (+ 4 if right)
 #pragma unroll
@@ -166,7 +166,7 @@ __device__ __forceinline__ void walk_trees(const TravParams& p, const TravChunk&
 #pragma unroll
       for (int u = 0; u < NI; ++u) {
         bool r = x[u] * k16 > a[u];  // code(x) > j  <=>  !(x <= t);  NaN code 0xFFFF -> right
-        if (ML) r = r && !(((a[u] >> 15) & 1u) && x[u] == 0xFFFFu);
+        if (ML) r = r && !((a[u] & 1u) && x[u] == 0xFFFFu);
         A[u] = A[u] * k2 + cb[u];
         if (r) A[u] += 4u;
       }

@@ -233,6 +233,25 @@ def test_coded_binning_variants(binv, F, monkeypatch):
     assert g.layout()["coded"]
 
 
+def test_coded_wide_code_range(monkeypatch):
+    """Up to 65534 distinct thresholds per feature (16-bit code index, missing
+    flag in bit 0): ~41K random distinct thresholds on each of 4 features ->
+    2^16-slot search trees, binned with their top 14 levels in shared memory
+    and the rest from global memory; NaN / missing-left routing included."""
+    monkeypatch.setenv("BRIDGER_CODES", "1")
+    m = perfect_ensemble(80, 40, 12, 4, kind="regression", lr=0.1, calib_rows=512)
+    rng = np.random.default_rng(81)
+    th = m.threshold.copy()
+    internal = m.left != -1
+    th[internal] = rng.standard_normal(int(internal.sum())).astype(np.float32)
+    ml = (rng.random(len(th)) < 0.3).astype(np.uint8)
+    m = ModelDesc(**{**m.__dict__, "threshold": th, "missing_left": ml})
+    X = inject_specials(gen_x(82, 0, 3001, 4), 82, rate=0.02)
+    X[::53, 1] = th[internal][m.feature[internal] == 1][:57].repeat(1)[: len(X[::53])]
+    g, _ = check(m, X, apply=False)
+    assert g.layout()["coded"]
+
+
 def test_c5_shard_coded(monkeypatch):
     """C5-shaped tree shard (1250 trees would take minutes in the oracle: 120
     trees of depth 10 over 200 features) in threshold-bin codes with

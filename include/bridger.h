@@ -141,7 +141,8 @@ bridger_status bridger_model_set_variant(bridger_model* m, int32_t variant); /* 
  * node format (*coded: 0 heap fp32, 1 threshold-bin codes, 2 sparse pointer
  * layout for deep / unbalanced trees, 3 heap fp32 with the input transposed
  * once into feature-major blocks, 4 hybrid top-levels-resident, 6 tree-streamed:
- * row tiles resident, chunk node records streamed through shared memory), global-tree mode
+ * row tiles resident, chunk node records streamed through shared memory, 7 tree-streamed in
+ * threshold-bin codes), global-tree mode
  * (trees too large for shared memory), warps per CTA and warps per row block.
  * Any output pointer may be NULL. */
 bridger_status bridger_model_layout(const bridger_model* m, int32_t* n_chunks, int32_t* coded, int32_t* global_trees,

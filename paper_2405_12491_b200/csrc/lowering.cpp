@@ -396,6 +396,7 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
   int64_t visits = 0;
   for (int32_t t = 0; t < T; ++t) visits += std::max(1, depth[t]);
   bool want_codes = codes_env ? codes_env[0] != '0' : (visits >= 12 * (int64_t)F && visits >= 64);
+  const bool codes_requested = want_codes;
   if (want_codes) {
     want_codes = build_bin_table(d, out);
     // (tables of any size: the binning kernel keeps all of them, or a group of
@@ -608,15 +609,26 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
     // F <= 127 the split format ([pad][thresholds] fp32 + [pad][features] u8,
     // 5 * 2^D bytes) lets two trees share a slot of a 2-slot ring, so every
     // thread walks two trees at once (BRIDGER_STREAM_SPLIT=0 keeps 8-byte nodes)
+    // Threshold-bin codes for streamed trees (when the tables can be built:
+    // <= 65534 distinct thresholds per feature, F <= 512): 4-byte node words,
+    // u16 code blocks as the row tile (half the fp32 tile); BRIDGER_STREAM_CODES=0
+    // keeps the fp32 formats
+    const char* cenv = std::getenv("BRIDGER_STREAM_CODES");
+    const bool scodes = codes_requested && F <= 512 && !(cenv && cenv[0] == '0') && build_bin_table(d, out);
+    if (!scodes) {
+      out->bin_table.clear();
+      out->bin_sorted.clear();
+    }
     const char* senv = std::getenv("BRIDGER_STREAM_SPLIT");
-    const bool spl = F <= 127 && !(senv && senv[0] == '0');
+    const bool spl = !scodes && F <= 127 && !(senv && senv[0] == '0');
     auto tree_bytes = [&](int32_t D) -> int64_t {
-      return spl ? ((((int64_t)5 << D) + 15) / 16 * 16) : ((int64_t)1 << D) * 8;
+      return scodes ? (((((int64_t)1 << D) - 1) * 4 + 15) / 16 * 16)
+                    : spl ? ((((int64_t)5 << D) + 15) / 16 * 16) : ((int64_t)1 << D) * 8;
     };
     const int64_t tree_nodes = tree_bytes(Dmax);
     const int32_t ns = spl ? 2 : 3;
     // one slot = 64-byte chunk header + node records
-    const int64_t stage = std::max<int64_t>(spl ? 2 * tree_nodes : (tree_nodes + 15) / 16 * 16, 16384) + 64;
+    const int64_t stage = std::max<int64_t>((spl || scodes) ? 2 * tree_nodes : (tree_nodes + 15) / 16 * 16, 16384) + 64;
     std::vector<Run> pieces;
     int32_t min_n = INT32_MAX;
     for (const Run& r : bal) {
@@ -633,7 +645,8 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
       // split walk: the discarded last-level child loads read <= 3*2^D bytes
       // past a tree, i.e. into the landing slots after the ring; pad if short
       const int64_t slack = spl ? std::max<int64_t>(0, ((int64_t)3 << Dmax) + 64 - landing) : 0;
-      return (int64_t)wp * 32 * F * 4 + ns * stage + landing + slack + 1024 <= kSmemMax;
+      const int64_t xtile = scodes ? (int64_t)(wp + 1) * code_buf_bytes(F) : (int64_t)wp * 32 * F * 4;
+      return xtile + ns * stage + landing + slack + 1024 <= kSmemMax;
     };
     int32_t warps = 16;
     while (warps > 4 && !fits(warps)) --warps;
@@ -644,8 +657,12 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
       out->stream_warps = warps;
       out->stream_w = w;
       out->stream_split = spl;
+      out->codes = scodes;
       out->stream_slack = spl ? (int32_t)std::max<int64_t>(0, ((int64_t)3 << Dmax) + 64 - (int64_t)warps * 32 * w * K * 4) : 0;
       bal.swap(pieces);
+    } else if (scodes) {
+      out->bin_table.clear();
+      out->bin_sorted.clear();
     }
   }
   {
@@ -670,6 +687,7 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
     c.depth = D;
     c.first_slot = r.start;
     const int64_t nodes = out->split ? (((int64_t)r.n * I * 4 + 15) / 16 * 16 + (int64_t)r.n * I)
+                          : (out->stream && out->codes) ? (int64_t)r.n * I * 4
                           : out->stream ? (int64_t)r.n * (out->stream_split ? ((((int64_t)5 << D) + 15) / 16 * 16) : (int64_t)(I + 1) * 8)
                                         : (int64_t)r.n * I * node_bytes;
     c.leaf_offset = (int32_t)((nodes + 31) / 32 * 32);  // 32-byte aligned leaf vectors (256-bit gathers)

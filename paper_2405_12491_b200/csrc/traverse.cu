@@ -60,8 +60,9 @@ BRIDGER_TRAV_EXTERN(double, true, false, 5)
   BRIDGER_STREAM_EXTERN_W(long long, true, 2, SPL)  \
   BRIDGER_STREAM_EXTERN_W(double, false, 2, SPL)    \
   BRIDGER_STREAM_EXTERN_W(double, true, 2, SPL)
-BRIDGER_STREAM_EXTERN_S(false)
-BRIDGER_STREAM_EXTERN_S(true)
+BRIDGER_STREAM_EXTERN_S(0)
+BRIDGER_STREAM_EXTERN_S(1)
+BRIDGER_STREAM_EXTERN_S(2)
 BRIDGER_TRAV_EXTERN(long long, false, true, 2)
 BRIDGER_TRAV_EXTERN(long long, true, true, 2)
 BRIDGER_TRAV_EXTERN(double, false, true, 2)
@@ -394,6 +395,83 @@ static int num_sms(int dev) {
 }
 
 // Runs the traversal over all rows.  want: 0 predict, 1 proba, 2 raw, 3 apply.
+// Step a1 in coded form: bin the rows once into [n_blocks][F2/2][32][2] u16
+// code blocks (stream-ordered allocation, returned in *codes_out).
+static cudaError_t launch_binning(const bridger_model* m, const TravLayout& L, const float* X, int64_t n_rows, int sms,
+                                  cudaStream_t st, void** codes_out) {
+  void* codes = nullptr;
+  cudaError_t err = cudaSuccess;
+  // step a1 in coded form: bin the rows once (all chunks reuse the codes)
+  const int64_t nbk = (n_rows + 31) / 32;
+  const int F2 = (m->F + 1) & ~1;
+  err = cudaMallocAsync(&codes, (size_t)nbk * 32 * F2 * 2, st);
+  if (err != cudaSuccess) return err;
+  const int P = (1 << L.bin_k) - 1;
+  const int fixed = (m->F * P * 4 + 127) / 128 * 128;
+  // per-warp staging (bulk-copied dense blocks) when the table leaves room
+  // for >= 8 warps of double-buffered staging, else one CTA-shared block
+  int nwb = 16;
+  while (nwb > 1 && fixed + nwb * (2 * 128 * m->F + 16) > 232448) --nwb;
+  bool stage = nwb >= 8;
+  bool coop = !stage && fixed + 2 * 128 * m->F + 32 <= 232448;
+  if (const char* e = std::getenv("BRIDGER_BIN")) {  // tests: force a binning variant where it fits
+    if (e[0] == 'f') stage = coop = false;
+    if (e[0] == 'c' && fixed + 2 * 128 * m->F + 32 <= 232448) { stage = false; coop = true; }
+  }
+  if (!stage) nwb = 16;
+  const int bsmem = fixed + (stage ? nwb * (2 * 128 * m->F + 16) : coop ? 2 * 128 * m->F + 32 : 0);
+  // staged kernel: NP pairs per pass, passes sized so that no chain is wasted
+  const int f2h = (m->F + 1) >> 1;
+  const int npass = (f2h + 6) / 7;
+  const int nps = (f2h + npass - 1) / npass;  // 1..7
+  using BinK = void (*)(const float*, int64_t, int32_t, const float*, int32_t, uint32_t*);
+  const BinK kerns[2][7] = {
+      {bin_kernel<1, 1>, bin_kernel<2, 1>, bin_kernel<3, 1>, bin_kernel<4, 1>, bin_kernel<5, 1>, bin_kernel<6, 1>,
+       bin_kernel<7, 1>},
+      {bin_kernel<1, 2>, bin_kernel<2, 2>, bin_kernel<3, 2>, bin_kernel<4, 2>, bin_kernel<5, 2>, bin_kernel<6, 2>,
+       bin_kernel<7, 2>}};
+  const int np = std::min(4, (f2h + nwb - 1) / nwb);  // pairs per warp pass (coop)
+  const BinK coops[4] = {bin_coop_kernel<1>, bin_coop_kernel<2>, bin_coop_kernel<3>, bin_coop_kernel<4>};
+  auto bk = coop ? coops[np - 1] : kerns[m->F % 2 == 0 ? 1 : 0][nps - 1];
+  int bsm = bsmem;
+  int64_t want_ctas = coop ? nbk : (nbk + nwb - 1) / nwb;
+  int fgsz = 0, fg_levels = 0;
+  if (!stage && !coop) {
+    // feature groups: FG features' tables per CTA, whole code pairs when they
+    // fit; 2^16-slot tables: pairs with their top 14 levels in shared memory
+    fgsz = 4 * P * 4 <= 200 * 1024 ? 4 : 2 * P * 4 <= 200 * 1024 ? 2 : P * 4 <= 200 * 1024 ? 1 : 2;
+    fg_levels = L.bin_k;
+    while (fgsz * ((1 << fg_levels) - 1) * 4 > 200 * 1024) --fg_levels;
+    bsm = fgsz * ((1 << fg_levels) - 1) * 4;
+    const int n_fg = (m->F + fgsz - 1) / fgsz;
+    // slices of row blocks per feature group: fill the SMs, each slice >= 16 blocks
+    const int64_t slices = std::max<int64_t>(1, std::min<int64_t>((2 * sms + n_fg - 1) / n_fg, (nbk + 15) / 16));
+    want_ctas = n_fg * slices;
+    nwb = 16;
+  }
+  cudaFuncSetAttribute(bk, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bk, nwb * 32, bsm);
+  const int bgrid = fgsz ? (int)want_ctas
+                         : (int)std::max<int64_t>(1, std::min<int64_t>(want_ctas, (int64_t)sms * std::max(1, occ)));
+  if (fgsz) {
+    auto fk = fgsz == 4 ? bin_fg_kernel<4> : fgsz == 2 ? bin_fg_kernel<2> : bin_fg_kernel<1>;
+    cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    fk<<<bgrid, nwb * 32, bsm, st>>>(X, n_rows, m->F, m->d_bin_table, L.bin_k, fg_levels,
+                                     static_cast<uint32_t*>(codes));
+  } else {
+    bk<<<bgrid, nwb * 32, bsm, st>>>(X, n_rows, m->F, m->d_bin_table, L.bin_k, static_cast<uint32_t*>(codes));
+  }
+  count_launch();
+  err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    cudaFreeAsync(codes, st);
+    return err;
+  }
+  *codes_out = codes;
+  return cudaSuccess;
+}
+
 cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, void* out, int want,
                      int32_t total_trees, cudaStream_t st) {
   const TravLayout& L = m->trav;
@@ -432,26 +510,33 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
   fin.out = out;
   p.fin = fin;
   if (L.stream) {
-    // tree-streamed mode: X transposed once into feature-major 32-row blocks,
-    // then row tiles resident / chunk node records streamed (traverse.cuh K4s)
+    // tree-streamed mode: X transposed once into feature-major 32-row blocks
+    // (or binned into code blocks), then row tiles resident / chunk node
+    // records streamed (traverse.cuh K4s)
     const int64_t nbk = (n_rows + 31) / 32;
     void* xt = nullptr;
-    cudaError_t err = cudaMallocAsync(&xt, (size_t)nbk * 32 * m->F * 4, st);
-    if (err != cudaSuccess) return err;
-    int nwx = 16;
-    while (nwx > 1 && nwx * 32 * (m->F | 1) * 4 > 200 * 1024) --nwx;
-    const int xsmem = nwx * 32 * (m->F | 1) * 4;
-    static bool x_attr_s = false;
-    if (!x_attr_s) {
-      cudaFuncSetAttribute(xpose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-      x_attr_s = true;
+    cudaError_t err = cudaSuccess;
+    if (L.codes) {
+      err = launch_binning(m, L, X, n_rows, sms, st, &xt);
+      if (err != cudaSuccess) return err;
+    } else {
+      err = cudaMallocAsync(&xt, (size_t)nbk * 32 * m->F * 4, st);
+      if (err != cudaSuccess) return err;
+      int nwx = 16;
+      while (nwx > 1 && nwx * 32 * (m->F | 1) * 4 > 200 * 1024) --nwx;
+      const int xsmem = nwx * 32 * (m->F | 1) * 4;
+      static bool x_attr_s = false;
+      if (!x_attr_s) {
+        cudaFuncSetAttribute(xpose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+        x_attr_s = true;
+      }
+      int occ = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, xpose_kernel, nwx * 32, xsmem);
+      const int xgrid = (int)std::max<int64_t>(1, std::min<int64_t>((nbk + nwx - 1) / nwx, (int64_t)sms * std::max(1, occ)));
+      xpose_kernel<<<xgrid, nwx * 32, xsmem, st>>>(X, n_rows, m->F, static_cast<float*>(xt));
+      count_launch();
+      err = cudaGetLastError();
     }
-    int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, xpose_kernel, nwx * 32, xsmem);
-    const int xgrid = (int)std::max<int64_t>(1, std::min<int64_t>((nbk + nwx - 1) / nwx, (int64_t)sms * std::max(1, occ)));
-    xpose_kernel<<<xgrid, nwx * 32, xsmem, st>>>(X, n_rows, m->F, static_cast<float*>(xt));
-    count_launch();
-    err = cudaGetLastError();
     if (err == cudaSuccess) {
       p.X = static_cast<const float*>(xt);
       p.mode = want == 3 ? TRAV_APPLY : TRAV_FINAL;
@@ -459,7 +544,10 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
       p.stream_ns = L.stream_ns;
       p.stream_stage = L.stream_stage;
       const int rb = L.stream_warps * 32;
-      p.stream_x_bytes = rb * m->F * 4;
+      p.stream_x_bytes = L.codes ? (L.stream_warps + 1) * code_buf_bytes(m->F) : rb * m->F * 4;
+      p.code_buf = L.codes ? code_buf_bytes(m->F) : 0;
+      p.k2 = 2u;
+      p.k16 = 65536u;
       const int W = L.stream_w;
       p.stream_lbuf_bytes = (rb * W * m->K * 4 + 15) / 16 * 16;
       // ring | landing slots | [split: slack for the walk's discarded last-level child loads] | barriers
@@ -471,13 +559,15 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
       const int block_s = (L.stream_warps + 1) * 32;
       const bool w2 = W == 2;
       const bool ml = L.has_missing;
-      const bool spl = L.stream_split;
-#define BRIDGER_STA(ML, W)                                                                         \
-  (spl ? launch_stream_t<1, long long, ML, W, true, true>(p, grid_s, block_s, smem_s, st)          \
-       : launch_stream_t<1, long long, ML, W, true, false>(p, grid_s, block_s, smem_s, st))
-#define BRIDGER_STW(ACC, ML, W)                                                                    \
-  (spl ? launch_stream_t<KT, ACC, ML, W, false, true>(p, grid_s, block_s, smem_s, st)              \
-       : launch_stream_t<KT, ACC, ML, W, false, false>(p, grid_s, block_s, smem_s, st))
+      const int sf = L.codes ? 2 : L.stream_split ? 1 : 0;
+#define BRIDGER_STA(ML, W)                                                                             \
+  (sf == 2 ? launch_stream_t<1, long long, ML, W, true, 2>(p, grid_s, block_s, smem_s, st)             \
+   : sf == 1 ? launch_stream_t<1, long long, ML, W, true, 1>(p, grid_s, block_s, smem_s, st)           \
+             : launch_stream_t<1, long long, ML, W, true, 0>(p, grid_s, block_s, smem_s, st))
+#define BRIDGER_STW(ACC, ML, W)                                                                        \
+  (sf == 2 ? launch_stream_t<KT, ACC, ML, W, false, 2>(p, grid_s, block_s, smem_s, st)                 \
+   : sf == 1 ? launch_stream_t<KT, ACC, ML, W, false, 1>(p, grid_s, block_s, smem_s, st)               \
+             : launch_stream_t<KT, ACC, ML, W, false, 0>(p, grid_s, block_s, smem_s, st))
       if (want == 3) {
         err = ml ? (w2 ? BRIDGER_STA(true, 2) : BRIDGER_STA(true, 1)) : (w2 ? BRIDGER_STA(false, 2) : BRIDGER_STA(false, 1));
       } else {
@@ -530,73 +620,8 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
   cudaError_t err = cudaSuccess;
   void* codes = nullptr;
   if (L.codes) {
-    // step a1 in coded form: bin the rows once (all chunks reuse the codes)
-    const int64_t nbk = (n_rows + 31) / 32;
-    const int F2 = (m->F + 1) & ~1;
-    err = cudaMallocAsync(&codes, (size_t)nbk * 32 * F2 * 2, st);
+    err = launch_binning(m, L, X, n_rows, sms, st, &codes);
     if (err != cudaSuccess) return err;
-    const int P = (1 << L.bin_k) - 1;
-    const int fixed = (m->F * P * 4 + 127) / 128 * 128;
-    // per-warp staging (bulk-copied dense blocks) when the table leaves room
-    // for >= 8 warps of double-buffered staging, else one CTA-shared block
-    int nwb = 16;
-    while (nwb > 1 && fixed + nwb * (2 * 128 * m->F + 16) > 232448) --nwb;
-    bool stage = nwb >= 8;
-    bool coop = !stage && fixed + 2 * 128 * m->F + 32 <= 232448;
-    if (const char* e = std::getenv("BRIDGER_BIN")) {  // tests: force a binning variant where it fits
-      if (e[0] == 'f') stage = coop = false;
-      if (e[0] == 'c' && fixed + 2 * 128 * m->F + 32 <= 232448) { stage = false; coop = true; }
-    }
-    if (!stage) nwb = 16;
-    const int bsmem = fixed + (stage ? nwb * (2 * 128 * m->F + 16) : coop ? 2 * 128 * m->F + 32 : 0);
-    // staged kernel: NP pairs per pass, passes sized so that no chain is wasted
-    const int f2h = (m->F + 1) >> 1;
-    const int npass = (f2h + 6) / 7;
-    const int nps = (f2h + npass - 1) / npass;  // 1..7
-    using BinK = void (*)(const float*, int64_t, int32_t, const float*, int32_t, uint32_t*);
-    const BinK kerns[2][7] = {
-        {bin_kernel<1, 1>, bin_kernel<2, 1>, bin_kernel<3, 1>, bin_kernel<4, 1>, bin_kernel<5, 1>, bin_kernel<6, 1>,
-         bin_kernel<7, 1>},
-        {bin_kernel<1, 2>, bin_kernel<2, 2>, bin_kernel<3, 2>, bin_kernel<4, 2>, bin_kernel<5, 2>, bin_kernel<6, 2>,
-         bin_kernel<7, 2>}};
-    const int np = std::min(4, (f2h + nwb - 1) / nwb);  // pairs per warp pass (coop)
-    const BinK coops[4] = {bin_coop_kernel<1>, bin_coop_kernel<2>, bin_coop_kernel<3>, bin_coop_kernel<4>};
-    auto bk = coop ? coops[np - 1] : kerns[m->F % 2 == 0 ? 1 : 0][nps - 1];
-    int bsm = bsmem;
-    int64_t want_ctas = coop ? nbk : (nbk + nwb - 1) / nwb;
-    int fgsz = 0, fg_levels = 0;
-    if (!stage && !coop) {
-      // feature groups: FG features' tables per CTA, whole code pairs when they
-      // fit; 2^16-slot tables: pairs with their top 14 levels in shared memory
-      fgsz = 4 * P * 4 <= 200 * 1024 ? 4 : 2 * P * 4 <= 200 * 1024 ? 2 : P * 4 <= 200 * 1024 ? 1 : 2;
-      fg_levels = L.bin_k;
-      while (fgsz * ((1 << fg_levels) - 1) * 4 > 200 * 1024) --fg_levels;
-      bsm = fgsz * ((1 << fg_levels) - 1) * 4;
-      const int n_fg = (m->F + fgsz - 1) / fgsz;
-      // slices of row blocks per feature group: fill the SMs, each slice >= 16 blocks
-      const int64_t slices = std::max<int64_t>(1, std::min<int64_t>((2 * sms + n_fg - 1) / n_fg, (nbk + 15) / 16));
-      want_ctas = n_fg * slices;
-      nwb = 16;
-    }
-    cudaFuncSetAttribute(bk, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bk, nwb * 32, bsm);
-    const int bgrid = fgsz ? (int)want_ctas
-                           : (int)std::max<int64_t>(1, std::min<int64_t>(want_ctas, (int64_t)sms * std::max(1, occ)));
-    if (fgsz) {
-      auto fk = fgsz == 4 ? bin_fg_kernel<4> : fgsz == 2 ? bin_fg_kernel<2> : bin_fg_kernel<1>;
-      cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-      fk<<<bgrid, nwb * 32, bsm, st>>>(X, n_rows, m->F, m->d_bin_table, L.bin_k, fg_levels,
-                                       static_cast<uint32_t*>(codes));
-    } else {
-      bk<<<bgrid, nwb * 32, bsm, st>>>(X, n_rows, m->F, m->d_bin_table, L.bin_k, static_cast<uint32_t*>(codes));
-    }
-    count_launch();
-    err = cudaGetLastError();
-    if (err != cudaSuccess) {
-      cudaFreeAsync(codes, st);
-      return err;
-    }
     p.X = static_cast<const float*>(codes);
   } else if (L.hybrid || (L.pretransposed && want != 3)) {
     const int64_t nbk = (n_rows + 31) / 32;

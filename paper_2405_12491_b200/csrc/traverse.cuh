@@ -853,18 +853,58 @@ __device__ __forceinline__ void stream_walk_split(const uint8_t* t0, int tb, con
   for (int u = 0; u < W; ++u) idx[u] -= I;  // leaf index
 }
 
+// Threshold-bin codes for streamed trees: 4-byte node words (code index j <<
+// 16 | feature byte offset | missing) walked as in walk_trees' CODES branch;
+// xb = this lane's column of its warp's 2^b-aligned code block.
+template <int W, bool ML>
+__device__ __forceinline__ void stream_walk_codes(uint32_t nb, int tstride, uint32_t xb, uint32_t mask, uint32_t k2,
+                                                  uint32_t k16, int I, int D, int (&idx)[W]) {
+  uint32_t A[W], cb[W];
+#pragma unroll
+  for (int u = 0; u < W; ++u) {
+    A[u] = nb + (uint32_t)(u * tstride);
+    cb[u] = 4u - A[u];
+  }
+  for (int lvl = 0; lvl < D; ++lvl) {
+    uint32_t a[W], x[W];
+#pragma unroll
+    for (int u = 0; u < W; ++u) a[u] = ptx::lds_u32(A[u]);
+#pragma unroll
+    for (int u = 0; u < W; ++u) x[u] = ptx::lds_u16(xb | (a[u] & mask));
+#pragma unroll
+    for (int u = 0; u < W; ++u) {
+      bool r = x[u] * k16 > a[u];  // code(x) > j; NaN code 0xFFFF -> right
+      if (ML) r = r && !((a[u] & 1u) && x[u] == 0xFFFFu);
+      A[u] = A[u] * k2 + cb[u];
+      if (r) A[u] += 4u;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < W; ++u) idx[u] = (int)((A[u] + cb[u] - 4u) >> 2) - I;  // leaf index
+}
+
 // W: trees walked together per pass (= the chunk width chosen at lowering; a
 // chunk's last pass masks trees past its end).  The steady-state loop has no
 // divergent branch: ptxas drains every load scoreboard at one, which would
 // serialise the leaf-gather latency the pipelining hides.
-template <int KT, typename ACC, bool ML, int W, bool APPLY, bool SPL = false>
+// SF: streamed node format -- 0: 8-byte records, 1: split (fp32 thresholds +
+// u8 features), 2: threshold-bin codes (4-byte words, u16 input codes)
+template <int KT, typename ACC, bool ML, int W, bool APPLY, int SF = 0>
 __global__ void __launch_bounds__(544, 1) trav_stream_kernel(const TravParams p) {
+  constexpr bool SPL = SF == 1;
+  constexpr bool SCODES = SF == 2;
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int NWc = (blockDim.x >> 5) - 1;  // walking warps; the last warp is the loader
   const int RB = NWc * 32;                // rows per tile
   const int NS = p.stream_ns, F = p.F, K = p.K, nC = p.n_chunks;
   float* Xs = reinterpret_cast<float*>(smem);
+  // codes: per-warp code-block buffers aligned to their power-of-two size
+  uint8_t* xcodes = smem;
+  if (SCODES) {
+    const uint32_t a0 = ptx::s2u(smem);
+    xcodes = smem + (((a0 + (uint32_t)p.code_buf - 1u) & ~((uint32_t)p.code_buf - 1u)) - a0);
+  }
   uint8_t* ring = smem + p.stream_x_bytes;
   // per-thread landing slot of the previous pass's leaf values (cp.async)
   float* lbuf_all = reinterpret_cast<float*>(ring + (size_t)NS * p.stream_stage);
@@ -925,17 +965,27 @@ __global__ void __launch_bounds__(544, 1) trav_stream_kernel(const TravParams p)
     // every walking warp is done with the previous tile: reload X
     asm volatile("bar.sync 1, %0;" ::"r"(RB) : "memory");
     if (threadIdx.x == 0) {
-      const uint32_t bytes = (uint32_t)nblk * 32u * (uint32_t)F * 4u;
       ptx::fence_proxy_async();
-      ptx::mbar_arrive_expect_tx(xbar, bytes);
-      const uint8_t* src = reinterpret_cast<const uint8_t*>(p.X) + blk0 * 32 * (int64_t)F * 4;
-      for (uint32_t o = 0; o < bytes; o += 65536u)
-        ptx::bulk_g2s(reinterpret_cast<uint8_t*>(Xs) + o, src + o, min(65536u, bytes - o), xbar);
+      if (SCODES) {
+        // one code block (64 * F2 bytes) per walking warp, into its 2^b-aligned buffer
+        const uint32_t cbytes = 64u * (uint32_t)((F + 1) & ~1);
+        ptx::mbar_arrive_expect_tx(xbar, (uint32_t)nblk * cbytes);
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(p.X) + blk0 * (int64_t)cbytes;
+        for (int w = 0; w < nblk; ++w)
+          ptx::bulk_g2s(xcodes + (size_t)w * p.code_buf, src + (size_t)w * cbytes, cbytes, xbar);
+      } else {
+        const uint32_t bytes = (uint32_t)nblk * 32u * (uint32_t)F * 4u;
+        ptx::mbar_arrive_expect_tx(xbar, bytes);
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(p.X) + blk0 * 32 * (int64_t)F * 4;
+        for (uint32_t o = 0; o < bytes; o += 65536u)
+          ptx::bulk_g2s(reinterpret_cast<uint8_t*>(Xs) + o, src + o, min(65536u, bytes - o), xbar);
+      }
     }
     ptx::mbar_wait(xbar, xphase);
     xphase ^= 1;
     const int64_t row = tile * RB + warp * 32 + lane;
     const float* xl = Xs + (size_t)warp * F * 32 + lane;
+    const uint32_t xcl = SCODES ? ptx::s2u(xcodes + (size_t)warp * p.code_buf) + 4u * lane : 0u;
     ACC acc[KT];
 #pragma unroll
     for (int q = 0; q < KT; ++q) acc[q] = ACC(0);
@@ -984,7 +1034,10 @@ __global__ void __launch_bounds__(544, 1) trav_stream_kernel(const TravParams p)
         int idx[W];
         // trees past the chunk's end re-walk its last tree (masked below)
         const int jw = min(j, ch.n_trees - W < 0 ? 0 : ch.n_trees - W);
-        if (SPL) {
+        if (SCODES) {
+          stream_walk_codes<W, ML>(ptx::s2u(nodes) + 4u * (uint32_t)(jw * I), 4 * I, xcl, (uint32_t)p.code_buf - 2u,
+                                   p.k2, p.k16, I, D, idx);
+        } else if (SPL) {
           const int tb = ((5 << D) + 15) & ~15;
           stream_walk_split<W, ML>(reinterpret_cast<const uint8_t*>(nodes) + (size_t)jw * tb, tb, xl, I, D, idx);
         } else {
@@ -1044,7 +1097,7 @@ __global__ void __launch_bounds__(544, 1) trav_stream_kernel(const TravParams p)
   }
 }
 
-template <int KT, typename ACC, bool ML, int W, bool APPLY, bool SPL>
+template <int KT, typename ACC, bool ML, int W, bool APPLY, int SPL>
 cudaError_t launch_stream_t(const TravParams& p, int grid, int block, int smem, cudaStream_t st) {
   auto kern = trav_stream_kernel<KT, ACC, ML, W, APPLY, SPL>;
   static int configured = 0;

@@ -296,6 +296,23 @@ def test_tree_streamed_c4_shape(n_rows, n_trees, split, monkeypatch):
     check(m, gen_x(4, 0, n_rows, 64), apply=n_rows < 1000)
 
 
+@pytest.mark.parametrize("n_rows,n_trees,ml", [(77, 6, False), (513, 7, True), (148 * 512 + 333, 6, False)])
+def test_tree_streamed_codes(n_rows, n_trees, ml, monkeypatch):
+    """Tree-streamed mode in threshold-bin codes (C4-shaped: depth 12, 8
+    classes): u16 code blocks as the row tile, 4-byte node words streamed two
+    trees per slot; odd tree counts, tail tiles, specials and missing-left."""
+    monkeypatch.setenv("BRIDGER_CODES", "1")
+    c, m = make_config("C4", n_trees=n_trees)
+    if ml:
+        m = prune_ensemble(m, 97, p=0.0005, with_missing=True)
+    g = B.Model(m)
+    assert g.layout()["format"] == "stream_codes"
+    X = gen_x(4, 0, n_rows, 64)
+    if ml:
+        X = inject_specials(X, 98, rate=0.02)
+    check(m, X, apply=n_rows < 1000)
+
+
 @pytest.mark.parametrize("ml", [False, True])
 def test_tree_streamed_pruned_missing_mixed_depth(ml):
     m = perfect_ensemble(95, 10, 12, 64, kind="classification", n_classes=8, calib_rows=2048)

@@ -626,19 +626,37 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
                     : spl ? ((((int64_t)5 << D) + 15) / 16 * 16) : ((int64_t)1 << D) * 8;
     };
     const int64_t tree_nodes = tree_bytes(Dmax);
-    const int32_t ns = spl ? 2 : 3;
+    // codes: two trees per slot of a 3-slot ring; three per slot of a 2-slot
+    // ring (BRIDGER_STREAM_W=3) measured slower on C4 (16.1 vs 14.1 ms)
+    int32_t per_slot = (spl || scodes) ? 2 : 1;
+    if (scodes) {
+      if (const char* e = std::getenv("BRIDGER_STREAM_W")) per_slot = std::max(2, std::min(3, std::atoi(e)));
+    }
+    const int32_t ns = (spl || per_slot == 3) ? 2 : 3;
     // one slot = 64-byte chunk header + node records
-    const int64_t stage = std::max<int64_t>((spl || scodes) ? 2 * tree_nodes : (tree_nodes + 15) / 16 * 16, 16384) + 64;
+    const int64_t stage = std::max<int64_t>(per_slot > 1 ? per_slot * tree_nodes : (tree_nodes + 15) / 16 * 16, 16384) + 64;
     std::vector<Run> pieces;
     int32_t min_n = INT32_MAX;
     for (const Run& r : bal) {
       const int64_t per = std::max<int64_t>(1, std::min<int64_t>(4, (stage - 64) / tree_bytes(r.D)));
-      for (int32_t s0 = 0; s0 < r.n; s0 += (int32_t)per) {
-        pieces.push_back({r.start + s0, (int32_t)std::min<int64_t>(per, r.n - s0), r.D});
-        min_n = std::min(min_n, pieces.back().n);
+      // pieces of `per` trees; a remainder of 1 behind a full piece is
+      // rebalanced (3 + 1 -> 2 + 2) so that no chunk holds a single tree
+      std::vector<int32_t> sizes;
+      for (int32_t s0 = 0; s0 < r.n; s0 += (int32_t)per) sizes.push_back((int32_t)std::min<int64_t>(per, r.n - s0));
+      if (sizes.size() >= 2 && sizes.back() == 1 && sizes[sizes.size() - 2] >= 3) {
+        sizes[sizes.size() - 2] -= 1;
+        sizes.back() += 1;
+      }
+      int32_t s0 = 0;
+      for (int32_t sz : sizes) {
+        pieces.push_back({r.start + s0, sz, r.D});
+        min_n = std::min(min_n, sz);
+        s0 += sz;
       }
     }
-    const int32_t w = (min_n >= 2 && K <= 8) ? 2 : 1;  // trees per pass (every chunk holds >= w)
+    // trees per pass (every chunk holds >= w)
+    // (codes walk clamps chunks that hold fewer than w trees; the fp32 walks need >= w)
+    const int32_t w = scodes ? per_slot : (min_n >= 2 && K <= 8) ? 2 : 1;
     // shared memory: X tile (32 rows per warp) + ring + per-thread leaf slots
     auto fits = [&](int32_t wp) {
       const int64_t landing = (int64_t)wp * 32 * w * K * 4;

@@ -63,6 +63,10 @@ BRIDGER_TRAV_EXTERN(double, true, false, 5)
 BRIDGER_STREAM_EXTERN_S(0)
 BRIDGER_STREAM_EXTERN_S(1)
 BRIDGER_STREAM_EXTERN_S(2)
+BRIDGER_STREAM_EXTERN_W(long long, false, 3, 2)
+BRIDGER_STREAM_EXTERN_W(long long, true, 3, 2)
+BRIDGER_STREAM_EXTERN_W(double, false, 3, 2)
+BRIDGER_STREAM_EXTERN_W(double, true, 3, 2)
 BRIDGER_TRAV_EXTERN(long long, false, true, 2)
 BRIDGER_TRAV_EXTERN(long long, true, true, 2)
 BRIDGER_TRAV_EXTERN(double, false, true, 2)
@@ -568,7 +572,18 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
   (sf == 2 ? launch_stream_t<KT, ACC, ML, W, false, 2>(p, grid_s, block_s, smem_s, st)                 \
    : sf == 1 ? launch_stream_t<KT, ACC, ML, W, false, 1>(p, grid_s, block_s, smem_s, st)               \
              : launch_stream_t<KT, ACC, ML, W, false, 0>(p, grid_s, block_s, smem_s, st))
-      if (want == 3) {
+      if (W == 3) {  // codes only
+        if (want == 3) {
+          err = ml ? launch_stream_t<1, long long, true, 3, true, 2>(p, grid_s, block_s, smem_s, st)
+                   : launch_stream_t<1, long long, false, 3, true, 2>(p, grid_s, block_s, smem_s, st);
+        } else {
+#define BRIDGER_ST3(ACC)                                                                    \
+  (ml ? launch_stream_t<KT, ACC, true, 3, false, 2>(p, grid_s, block_s, smem_s, st)        \
+      : launch_stream_t<KT, ACC, false, 3, false, 2>(p, grid_s, block_s, smem_s, st))
+          BRIDGER_DISPATCH_KT(m->K, { err = m->acc_int ? BRIDGER_ST3(long long) : BRIDGER_ST3(double); });
+#undef BRIDGER_ST3
+        }
+      } else if (want == 3) {
         err = ml ? (w2 ? BRIDGER_STA(true, 2) : BRIDGER_STA(true, 1)) : (w2 ? BRIDGER_STA(false, 2) : BRIDGER_STA(false, 1));
       } else {
 #define BRIDGER_ST(ACC) \

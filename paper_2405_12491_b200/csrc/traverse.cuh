@@ -857,12 +857,12 @@ __device__ __forceinline__ void stream_walk_split(const uint8_t* t0, int tb, con
 // 16 | feature byte offset | missing) walked as in walk_trees' CODES branch;
 // xb = this lane's column of its warp's 2^b-aligned code block.
 template <int W, bool ML>
-__device__ __forceinline__ void stream_walk_codes(uint32_t nb, int tstride, uint32_t xb, uint32_t mask, uint32_t k2,
-                                                  uint32_t k16, int I, int D, int (&idx)[W]) {
+__device__ __forceinline__ void stream_walk_codes(uint32_t nb, int tstride, int umax, uint32_t xb, uint32_t mask,
+                                                  uint32_t k2, uint32_t k16, int I, int D, int (&idx)[W]) {
   uint32_t A[W], cb[W];
 #pragma unroll
   for (int u = 0; u < W; ++u) {
-    A[u] = nb + (uint32_t)(u * tstride);
+    A[u] = nb + (uint32_t)(min(u, umax) * tstride);  // chunks with < W trees re-walk their last tree
     cb[u] = 4u - A[u];
   }
   for (int lvl = 0; lvl < D; ++lvl) {
@@ -1035,8 +1035,8 @@ __global__ void __launch_bounds__(544, 1) trav_stream_kernel(const TravParams p)
         // trees past the chunk's end re-walk its last tree (masked below)
         const int jw = min(j, ch.n_trees - W < 0 ? 0 : ch.n_trees - W);
         if (SCODES) {
-          stream_walk_codes<W, ML>(ptx::s2u(nodes) + 4u * (uint32_t)(jw * I), 4 * I, xcl, (uint32_t)p.code_buf - 2u,
-                                   p.k2, p.k16, I, D, idx);
+          stream_walk_codes<W, ML>(ptx::s2u(nodes) + 4u * (uint32_t)(jw * I), 4 * I, ch.n_trees - 1 - jw, xcl,
+                                   (uint32_t)p.code_buf - 2u, p.k2, p.k16, I, D, idx);
         } else if (SPL) {
           const int tb = ((5 << D) + 15) & ~15;
           stream_walk_split<W, ML>(reinterpret_cast<const uint8_t*>(nodes) + (size_t)jw * tb, tb, xl, I, D, idx);
@@ -1064,7 +1064,7 @@ __global__ void __launch_bounds__(544, 1) trav_stream_kernel(const TravParams p)
           for (int u = 0; u < W; ++u) {
             const int t = jw + u;
             pmask[u] = (t >= j && t < ch.n_trees) ? 0xffffffffu : 0u;
-            const float* e = leaves + ((size_t)t * L + idx[u]) * K;
+            const float* e = leaves + ((size_t)min(t, ch.n_trees - 1) * L + idx[u]) * K;
             if (v4) {
 #pragma unroll
               for (int q = 0; q < KT; q += 4) {

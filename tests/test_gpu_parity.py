@@ -296,7 +296,7 @@ def test_tree_streamed_c4_shape(n_rows, n_trees, split, monkeypatch):
     check(m, gen_x(4, 0, n_rows, 64), apply=n_rows < 1000)
 
 
-@pytest.mark.parametrize("n_rows,n_trees,ml", [(77, 6, False), (513, 7, True), (148 * 512 + 333, 6, False)])
+@pytest.mark.parametrize("n_rows,n_trees,ml", [(77, 6, False), (513, 7, True), (300, 5, False), (148 * 512 + 333, 6, False)])
 def test_tree_streamed_codes(n_rows, n_trees, ml, monkeypatch):
     """Tree-streamed mode in threshold-bin codes (C4-shaped: depth 12, 8
     classes): u16 code blocks as the row tile, 4-byte node words streamed two

@@ -11,3 +11,4 @@ for f in c2 c1 c3 c4 c5s; do tail -1 gpurun_out/bench_$f.log | python -c "import
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-gemm --e2e-steps 0 > gpurun_out/ncu_launch.log 2>&1; echo launch=$?
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"bin_kernel|trav_kernel|trav_combine" -c 3 -o gpurun_out/r1_c2_full python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-gemm --e2e-steps 0 > gpurun_out/ncu_full.log 2>&1; echo ncufull=$?
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"bin_kernel|trav_kernel" -c 2 -o gpurun_out/r1_c3_full python bench.py --config C3 --steps 1 --warmup 3 --no-cpu-baseline --no-gemm --e2e-steps 0 > gpurun_out/ncu_full3.log 2>&1; echo ncufull3=$?
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"trav_stream|bin_fg" -c 2 -o gpurun_out/r1_c4_full python bench.py --config C4 --rows 1000000 --steps 1 --warmup 3 --no-cpu-baseline --no-gemm --e2e-steps 0 > gpurun_out/ncu_full4.log 2>&1; echo ncufull4=$?

@@ -114,7 +114,9 @@ def test_zero_rows_and_shape_errors():
         B.Model(r).predict_proba(torch.zeros((4, 90), device="cuda"))
 
 
-def test_predict_host_matches_device():
+@pytest.mark.parametrize("codes", ["0", "1"])
+def test_predict_host_matches_device(codes, monkeypatch):
+    monkeypatch.setenv("BRIDGER_CODES", codes)
     c, m = make_config("C2", n_trees=30)
     X = gen_x(2, 0, 70001, 28)
     g = B.Model(m)
@@ -311,6 +313,20 @@ def test_tree_streamed_codes(n_rows, n_trees, ml, monkeypatch):
     if ml:
         X = inject_specials(X, 98, rate=0.02)
     check(m, X, apply=n_rows < 1000)
+
+
+def test_tree_streamed_codes_f64_tier(monkeypatch):
+    """Streamed codes with fp64 accumulation (a subnormal leaf value forces the
+    F64 tier, reading c9): scores within the tolerance, labels exact."""
+    monkeypatch.setenv("BRIDGER_CODES", "1")
+    c, m = make_config("C4", n_trees=5)
+    v = m.value.copy()
+    v[np.nonzero(m.left == -1)[0][0] * m.n_outputs] = np.float32(1.4e-45)
+    m = ModelDesc(**{**m.__dict__, "value": v})
+    assert B.analyze_exactness(m)[1] == "F64"
+    g = B.Model(m)
+    assert g.layout()["format"] == "stream_codes"
+    check(m, gen_x(4, 0, 1200, 64), exact=False, apply=False)
 
 
 @pytest.mark.parametrize("ml", [False, True])

@@ -315,6 +315,16 @@ def test_tree_streamed_codes(n_rows, n_trees, ml, monkeypatch):
     check(m, X, apply=n_rows < 1000)
 
 
+def test_tree_streamed_codes_many_classes(monkeypatch):
+    """Streamed codes with K = 12 (leaf vectors gathered by 4-byte cp.async
+    into element-major landing slots, KT = 16 != K) and an odd feature count."""
+    monkeypatch.setenv("BRIDGER_CODES", "1")
+    m = perfect_ensemble(120, 5, 12, 21, kind="classification", n_classes=12, calib_rows=2048)
+    g = B.Model(m)
+    assert g.layout()["format"] == "stream_codes"
+    check(m, inject_specials(gen_x(121, 0, 1500, 21), 121, rate=0.01))
+
+
 def test_tree_streamed_codes_f64_tier(monkeypatch):
     """Streamed codes with fp64 accumulation (a subnormal leaf value forces the
     F64 tier, reading c9): scores within the tolerance, labels exact."""

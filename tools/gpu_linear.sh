@@ -1,0 +1,5 @@
+# linear-model bench lines + ncu full of the linear kernel (C2 shape and softmax shape)
+mkdir -p gpurun_out
+python tools/bench_linear.py > gpurun_out/bench_linear.log 2>&1; echo lin=$?; cat gpurun_out/bench_linear.log
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:linear_kernel -c 3 -o gpurun_out/r1_linear_full python tools/bench_linear.py --steps 1 --warmup 0 > gpurun_out/ncu_linear.log 2>&1; echo ncu=$?
+ncu -i gpurun_out/r1_linear_full.ncu-rep --page raw --csv --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,dram__throughput.avg.pct_of_peak_sustained_elapsed,sm__throughput.avg.pct_of_peak_sustained_elapsed,launch__grid_size,launch__block_size > gpurun_out/linear_raw.csv 2>&1; cat gpurun_out/linear_raw.csv | head -8

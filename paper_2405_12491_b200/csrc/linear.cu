@@ -8,8 +8,9 @@
 // B200 mapping: HBM-bound (4F bytes of input per row against K*F fp64 MACs).
 // Persistent CTAs of W warps; each warp streams 32-row blocks of X through a
 // double-buffered shared-memory staging block filled by cp.async (coalesced
-// 4-byte copies; odd row stride F|1 so that lane = row reads are conflict
-// free) while it computes the previous block; the weights sit in shared memory
+// 16-, 8- or 4-byte copies, the widest F and X's alignment allow; row stride
+// odd in copy vectors so that lane = row vector reads are conflict free)
+// while it computes the previous block; the weights sit in shared memory
 // and are read as warp-wide broadcasts.  fp64 arithmetic costs nothing here:
 // the kernel is bound by the X stream.
 #include <cuda_runtime.h>
@@ -27,7 +28,7 @@ struct bridger_linear {
   int device = 0;
   int32_t F = 0, K = 0, task = 0, post = 0;
   bool scaler = false;
-  double* d_w = nullptr;      // [K*F] coef, then [K] intercept
+  double* d_w = nullptr;      // [F][K] coef (feature-major), then [K] intercept
   float* d_scale = nullptr;   // [2F] fp32 mean, scale (reading c16: cast to the input dtype)
 };
 
@@ -41,20 +42,20 @@ struct LinParams {
   const float* X;
   int64_t n_rows;
   int32_t F, K, S;      // S = staging row stride (odd)
-  const double* w;      // [K*F] then [K]
+  const double* w;      // [F][K] coef (feature-major) then [K] intercept
   const float* sc;      // [2F] or nullptr
   int32_t want;         // 0 predict, 1 proba, 2 decision (fp64 scores)
   FinalizeArgs fin;     // task / post / K / out
 };
 
-template <int KT, bool SCALER>
+template <int KT, bool SCALER, int VW, bool FULL>  // FULL: K == KT
 __global__ void __launch_bounds__(512) linear_kernel(const LinParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
-  const int F = p.F, K = p.K, S = p.S;
-  double* W = reinterpret_cast<double*>(smem);                 // [K*F + K]
-  float* SC = reinterpret_cast<float*>(W + (size_t)K * F + K);  // [2F]
-  float* St = SC + 2 * F + ((2 * F) & 1);                       // [NW][2][32*S]
+  const int F = p.F, K = FULL ? KT : p.K, S = p.S;
+  double* W = reinterpret_cast<double*>(smem);                 // [F][K] + [K]
+  float* SC = reinterpret_cast<float*>(W + (((size_t)K * F + K + 1) & ~(size_t)1));  // [2F]
+  float* St = SC + ((2 * F + 3) & ~3);                          // [NW][2][32*S], 16-B aligned
   for (int i = threadIdx.x; i < K * F + K; i += blockDim.x) W[i] = p.w[i];
   if (SCALER)
     for (int i = threadIdx.x; i < 2 * F; i += blockDim.x) SC[i] = p.sc[i];
@@ -63,17 +64,34 @@ __global__ void __launch_bounds__(512) linear_kernel(const LinParams p) {
   const int64_t n_blocks = (p.n_rows + 31) / 32;
   const int64_t stride = (int64_t)gridDim.x * NW;
   int64_t blk = (int64_t)blockIdx.x * NW + warp;
-  // stage block b into buffer `buf`: element e of the contiguous [rows][F]
-  // block goes to row e / F, column e % F of the odd-stride staging block
+  // The contiguous [rows][F] block is copied in VW-float vectors (VW = 4, 2
+  // or 1: the largest that divides F and the alignment of X): vector e =
+  // lane + 32 j goes to row e / FV, vector column e % FV of the staging block,
+  // whose row stride S = VW * (FV | 1) is odd in vector units, so the lane =
+  // row reads below are conflict free.  (row, column) advance incrementally
+  // (32 = q FV + r): no division in the copy loop.
+  const int FV = F / VW, q = 32 / FV, r = 32 - q * FV;
+  const int rr0 = lane / FV, c0 = lane - rr0 * FV;
   auto stage = [&](int64_t b, int buf) {
     if (b < n_blocks) {
       const int rows = (int)(p.n_rows - b * 32 < 32 ? p.n_rows - b * 32 : 32);
       const float* src = p.X + b * 32 * (int64_t)F;
-      float* dst = st0 + (size_t)buf * 32 * S;
-      for (int e = lane; e < rows * F; e += 32) {
-        const int rr = e / F, f = e - rr * F;
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(ptx::s2u(dst + rr * S + f)), "l"(src + e)
-                     : "memory");
+      const uint32_t dst = ptx::s2u(st0 + (size_t)buf * 32 * S);
+      int rr = rr0, c = c0;
+      for (int e = lane; e < rows * FV; e += 32) {
+        const uint32_t d = dst + (uint32_t)(rr * S + c * VW) * 4u;
+        if constexpr (VW == 4)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + (size_t)e * 4) : "memory");
+        else if constexpr (VW == 2)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src + (size_t)e * 2) : "memory");
+        else
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src + e) : "memory");
+        rr += q;
+        c += r;
+        if (c >= FV) {
+          c -= FV;
+          ++rr;
+        }
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -87,13 +105,28 @@ __global__ void __launch_bounds__(512) linear_kernel(const LinParams p) {
     double acc[KT];
 #pragma unroll
     for (int k = 0; k < KT; ++k) acc[k] = k < K ? W[(size_t)K * F + k] : 0.0;  // intercept
-    for (int f = 0; f < F; ++f) {
-      float xv = xr[f];
-      if (SCALER) xv = __fdiv_rn(__fsub_rn(xv, SC[f]), SC[F + f]);  // fp32 ops (c16)
-      const double xd = (double)xv;
+    for (int f0 = 0; f0 < F; f0 += VW) {
+      float xs[4];
+      if constexpr (VW == 4) {
+        const float4 v = *reinterpret_cast<const float4*>(xr + f0);
+        xs[0] = v.x, xs[1] = v.y, xs[2] = v.z, xs[3] = v.w;
+      } else if constexpr (VW == 2) {
+        const float2 v = *reinterpret_cast<const float2*>(xr + f0);
+        xs[0] = v.x, xs[1] = v.y;
+      } else {
+        xs[0] = xr[f0];
+      }
 #pragma unroll
-      for (int k = 0; k < KT; ++k)
-        if (k < K) acc[k] = __dadd_rn(acc[k], __dmul_rn(W[(size_t)k * F + f], xd));  // no FMA
+      for (int u = 0; u < VW; ++u) {  // features in ascending order
+        const int f = f0 + u;
+        float xv = xs[u];
+        if (SCALER) xv = __fdiv_rn(__fsub_rn(xv, SC[f]), SC[F + f]);  // fp32 ops (c16)
+        const double xd = (double)xv;
+        const double* wf = W + f * K;  // the K weights of feature f: immediate offsets below
+#pragma unroll
+        for (int k = 0; k < KT; ++k)
+          if (FULL || k < K) acc[k] = __dadd_rn(acc[k], __dmul_rn(wf[k], xd));  // no FMA
+      }
     }
     const int64_t row = blk * 32 + lane;
     if (row < p.n_rows) {
@@ -148,7 +181,11 @@ static bridger_status linear_run(const bridger_linear* m, const float* X, int64_
   p.n_rows = n_rows;
   p.F = m->F;
   p.K = m->K;
-  p.S = m->F | 1;
+  // vector width of the staging copies: the largest of 4, 2, 1 dividing F and
+  // the alignment of X; staging row stride odd in vectors (conflict-free reads)
+  int vw = 4;
+  while (vw > 1 && (m->F % vw != 0 || reinterpret_cast<uintptr_t>(X) % (4u * vw) != 0)) vw >>= 1;
+  p.S = vw * ((m->F / vw) | 1);
   p.w = m->d_w;
   p.sc = m->d_scale;
   p.want = want;
@@ -165,7 +202,7 @@ static bridger_status linear_run(const bridger_linear* m, const float* X, int64_
   fin.base = nullptr;
   fin.out = out;
   p.fin = fin;
-  const size_t fixed = ((size_t)m->K * m->F + m->K) * 8 + (2 * (size_t)m->F + 2) * 4;
+  const size_t fixed = (((size_t)m->K * m->F + m->K + 1) & ~(size_t)1) * 8 + (size_t)((2 * m->F + 3) & ~3) * 4;
   const size_t per_warp = (size_t)2 * 32 * p.S * 4;
   int nw = 16;
   while (nw > 1 && fixed + nw * per_warp > 232448) --nw;
@@ -177,7 +214,14 @@ static bridger_status linear_run(const bridger_linear* m, const float* X, int64_
   // persistent: as many CTAs as fit (up to 4 per SM), never more than row blocks need
   cudaError_t e = cudaSuccess;
   BRIDGER_DISPATCH_KT(m->K, {
-    auto kern = m->scaler ? linear_kernel<KT, true> : linear_kernel<KT, false>;
+    const bool full = m->K == KT;
+    auto pick = [&](auto f_full, auto f_part) { return full ? f_full : f_part; };
+    auto kern = vw == 4 ? (m->scaler ? pick(linear_kernel<KT, true, 4, true>, linear_kernel<KT, true, 4, false>)
+                                     : pick(linear_kernel<KT, false, 4, true>, linear_kernel<KT, false, 4, false>))
+                : vw == 2 ? (m->scaler ? pick(linear_kernel<KT, true, 2, true>, linear_kernel<KT, true, 2, false>)
+                                       : pick(linear_kernel<KT, false, 2, true>, linear_kernel<KT, false, 2, false>))
+                          : (m->scaler ? pick(linear_kernel<KT, true, 1, true>, linear_kernel<KT, true, 1, false>)
+                                       : pick(linear_kernel<KT, false, 1, true>, linear_kernel<KT, false, 1, false>));
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     int occ = 1;
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nw * 32, smem);
@@ -222,7 +266,7 @@ bridger_status bridger_linear_load(const bridger_linear_desc* d, int cuda_device
   std::vector<double> w((size_t)K * F + K, 0.0);
   for (size_t i = 0; i < (size_t)K * F; ++i) {
     if (!std::isfinite(d->coef[i])) return fail(BRIDGER_E_INVALID_TREE, "non-finite coefficient");
-    w[i] = d->coef[i];
+    w[(i % F) * K + i / F] = d->coef[i];  // feature-major: the kernel reads W[f][0..K)
   }
   for (int32_t k = 0; k < K; ++k) {
     const double b = d->intercept ? d->intercept[k] : 0.0;

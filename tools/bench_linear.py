@@ -39,6 +39,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--only", default=None, help="run the workloads whose name contains this string")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -54,6 +55,8 @@ def main():
     st = torch.cuda.current_stream(dev)
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
     for name, n, F, K, task, post, scaler in WORKLOADS:
+        if args.only and args.only not in name:
+            continue
         rng = np.random.default_rng(7)
         m = SimpleNamespace(n_features=F, n_outputs=K, coef=rng.normal(size=(K, F)) * 0.3,
                             intercept=rng.normal(size=K) * 0.1,

@@ -74,6 +74,36 @@ def test_linear_specials_and_empty():
     assert g.predict(torch.empty((0, 11), device="cuda")).shape[0] == 0
 
 
+@pytest.mark.parametrize("F,offset", [(28, 0), (28, 1), (28, 2), (90, 0), (90, 1), (64, 3)])
+def test_linear_copy_widths_and_misaligned_input(F, offset):
+    """The staging copies are 16-, 8- or 4-byte vectors, the widest that divides
+    F and the alignment of X: a view starting `offset` floats into its buffer
+    forces the narrower copies (F = 28: 16 B aligned -> 8 B -> 4 B)."""
+    m = _rand_linear(F + offset, F, 3, 1, 2, scaler=offset % 2 == 1)
+    n = 4133
+    X = gen_x(F * 7 + offset, 0, n, F)
+    buf = torch.zeros(n * F + offset, dtype=torch.float32, device="cuda")
+    Xd = buf[offset:].view(n, F)
+    Xd.copy_(dev(X))
+    g = B.LinearModel(m)
+    o = oracle.run_linear(m, X)
+    np.testing.assert_array_equal(g.decision_function(Xd).cpu().numpy(), o["s"])
+    np.testing.assert_array_equal(g.predict(Xd).cpu().numpy(), o["label"])
+
+
+def test_linear_c3_shape_full_size_sampled():
+    """At the size tools/bench_linear.py times (10M x 90, K = 1 regression), in
+    its launch configuration: sampled rows against the oracle, bitwise."""
+    F, n = 90, 10_000_000
+    m = _rand_linear(99, F, 1, 0, 0)
+    from synth import gen_x_torch
+    Xd = gen_x_torch(11, 0, n, F, device="cuda")
+    out = B.LinearModel(m).predict(Xd).cpu().numpy()
+    rows = np.unique(np.concatenate([np.arange(64), np.random.default_rng(3).integers(0, n, 2000), np.arange(n - 64, n)]))
+    Xs = np.stack([gen_x(11, int(r), 1, F)[0] for r in rows])  # counter-based: any row on its own
+    np.testing.assert_array_equal(out[rows], oracle.run_linear(m, Xs)["pred"])
+
+
 sk = pytest.importorskip("sklearn")
 
 

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -28,6 +29,11 @@ struct bridger_linear {
   int device = 0;
   int32_t F = 0, K = 0, task = 0, post = 0;
   bool scaler = false;
+  int sms = 148;
+  // per staging width (vw = 4, 2, 1): occupancy of the kernel that width
+  // selects, measured on first use (0 = not yet); the launch then makes no
+  // attribute or occupancy queries
+  mutable std::atomic<int> occ[3] = {0, 0, 0};
   double* d_w = nullptr;      // [F][K] coef (feature-major), then [K] intercept
   float* d_scale = nullptr;   // [2F] fp32 mean, scale (reading c16: cast to the input dtype)
 };
@@ -208,8 +214,7 @@ static bridger_status linear_run(const bridger_linear* m, const float* X, int64_
   while (nw > 1 && fixed + nw * per_warp > 232448) --nw;
   if (fixed + per_warp > 232448) return fail(BRIDGER_E_UNSUPPORTED, "model too wide for the linear kernel");
   const int smem = (int)(fixed + nw * per_warp);
-  int dev_sms = 148;
-  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, m->device);
+  const int dev_sms = m->sms;
   const int64_t n_blocks = (n_rows + 31) / 32;
   // persistent: as many CTAs as fit (up to 4 per SM), never more than row blocks need
   cudaError_t e = cudaSuccess;
@@ -222,9 +227,13 @@ static bridger_status linear_run(const bridger_linear* m, const float* X, int64_
                                        : pick(linear_kernel<KT, false, 2, true>, linear_kernel<KT, false, 2, false>))
                           : (m->scaler ? pick(linear_kernel<KT, true, 1, true>, linear_kernel<KT, true, 1, false>)
                                        : pick(linear_kernel<KT, false, 1, true>, linear_kernel<KT, false, 1, false>));
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    int occ = 1;
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nw * 32, smem);
+    const int vi = vw == 4 ? 0 : vw == 2 ? 1 : 2;
+    int occ = m->occ[vi].load(std::memory_order_relaxed);
+    if (occ == 0) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+      if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nw * 32, smem);
+      if (e == cudaSuccess) m->occ[vi].store(std::max(1, occ), std::memory_order_relaxed);
+    }
     if (e == cudaSuccess) {
       const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n_blocks + nw - 1) / nw,
                                                                    (int64_t)dev_sms * std::max(1, std::min(occ, 4))));
@@ -295,6 +304,7 @@ bridger_status bridger_linear_load(const bridger_linear_desc* d, int cuda_device
   m->task = d->task;
   m->post = d->post;
   m->scaler = !sc.empty();
+  cudaDeviceGetAttribute(&m->sms, cudaDevAttrMultiProcessorCount, cuda_device);
   e = cudaMalloc(&m->d_w, w.size() * 8);
   if (e == cudaSuccess) e = cudaMemcpy(m->d_w, w.data(), w.size() * 8, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && m->scaler) {

@@ -51,6 +51,7 @@ struct LinParams {
   const double* w;      // [F][K] coef (feature-major) then [K] intercept
   const float* sc;      // [2F] or nullptr
   int32_t want;         // 0 predict, 1 proba, 2 decision (fp64 scores)
+  int32_t bulk;         // S == F and X 16-B aligned: whole blocks by one cp.async.bulk
   FinalizeArgs fin;     // task / post / K / out
 };
 
@@ -62,6 +63,12 @@ __global__ void __launch_bounds__(512) linear_kernel(const LinParams p) {
   double* W = reinterpret_cast<double*>(smem);                 // [F][K] + [K]
   float* SC = reinterpret_cast<float*>(W + (((size_t)K * F + K + 1) & ~(size_t)1));  // [2F]
   float* St = SC + ((2 * F + 3) & ~3);                          // [NW][2][32*S], 16-B aligned
+  uint64_t* bars = reinterpret_cast<uint64_t*>(St + (size_t)NW * 2 * 32 * S) + 2 * warp;  // [NW][2]
+  if (lane == 0) {
+    ptx::mbar_init(&bars[0], 1);
+    ptx::mbar_init(&bars[1], 1);
+    ptx::fence_barrier_init();
+  }
   for (int i = threadIdx.x; i < K * F + K; i += blockDim.x) W[i] = p.w[i];
   if (SCALER)
     for (int i = threadIdx.x; i < 2 * F; i += blockDim.x) SC[i] = p.sc[i];
@@ -75,7 +82,10 @@ __global__ void __launch_bounds__(512) linear_kernel(const LinParams p) {
   // lane + 32 j goes to row e / FV, vector column e % FV of the staging block,
   // whose row stride S = VW * (FV | 1) is odd in vector units, so the lane =
   // row reads below are conflict free.  (row, column) advance incrementally
-  // (32 = q FV + r): no division in the copy loop.
+  // (32 = q FV + r): no division in the copy loop.  When FV is odd already
+  // (S == F: F = 28, 90, ...) the staging block is the dense [32][F] block, so
+  // whole blocks are fetched by one bulk copy (TMA engine, mbarrier) issued by
+  // lane 0; the ragged tail block always takes the per-lane path.
   const int FV = F / VW, q = 32 / FV, r = 32 - q * FV;
   const int rr0 = lane / FV, c0 = lane - rr0 * FV;
   auto stage = [&](int64_t b, int buf) {
@@ -83,6 +93,13 @@ __global__ void __launch_bounds__(512) linear_kernel(const LinParams p) {
       const int rows = (int)(p.n_rows - b * 32 < 32 ? p.n_rows - b * 32 : 32);
       const float* src = p.X + b * 32 * (int64_t)F;
       const uint32_t dst = ptx::s2u(st0 + (size_t)buf * 32 * S);
+      if (p.bulk && rows == 32) {
+        if (lane == 0) {
+          ptx::fence_proxy_async();  // this warp's generic reads of the buffer precede the async write
+          ptx::mbar_arrive_expect_tx(&bars[buf], 128u * (uint32_t)F);
+          ptx::bulk_g2s(st0 + (size_t)buf * 32 * S, src, 128u * (uint32_t)F, &bars[buf]);
+        }
+      } else {
       int rr = rr0, c = c0;
       for (int e = lane; e < rows * FV; e += 32) {
         const uint32_t d = dst + (uint32_t)(rr * S + c * VW) * 4u;
@@ -99,13 +116,20 @@ __global__ void __launch_bounds__(512) linear_kernel(const LinParams p) {
           ++rr;
         }
       }
+      }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   stage(blk, 0);
+  uint32_t phase = 0;  // bit b: parity of buffer b's mbarrier
   for (int buf = 0; blk < n_blocks; blk += stride, buf ^= 1) {
     stage(blk + stride, buf ^ 1);                                // next block in flight
-    asm volatile("cp.async.wait_group 1;" ::: "memory");        // this block landed
+    if (p.bulk && blk * 32 + 32 <= p.n_rows) {
+      ptx::mbar_wait(&bars[buf], (phase >> buf) & 1u);
+      phase ^= 1u << buf;
+    } else {
+      asm volatile("cp.async.wait_group 1;" ::: "memory");      // this block landed
+    }
     __syncwarp();
     const float* xr = st0 + (size_t)buf * 32 * S + lane * S;
     double acc[KT];
@@ -195,6 +219,7 @@ static bridger_status linear_run(const bridger_linear* m, const float* X, int64_
   p.w = m->d_w;
   p.sc = m->d_scale;
   p.want = want;
+  p.bulk = p.S == m->F && reinterpret_cast<uintptr_t>(X) % 16 == 0;
   FinalizeArgs fin{};
   fin.task = m->task;
   fin.agg = BRIDGER_AGG_SUM;
@@ -209,7 +234,7 @@ static bridger_status linear_run(const bridger_linear* m, const float* X, int64_
   fin.out = out;
   p.fin = fin;
   const size_t fixed = (((size_t)m->K * m->F + m->K + 1) & ~(size_t)1) * 8 + (size_t)((2 * m->F + 3) & ~3) * 4;
-  const size_t per_warp = (size_t)2 * 32 * p.S * 4;
+  const size_t per_warp = (size_t)2 * 32 * p.S * 4 + 16;  // two staging blocks + two mbarriers
   int nw = 16;
   while (nw > 1 && fixed + nw * per_warp > 232448) --nw;
   if (fixed + per_warp > 232448) return fail(BRIDGER_E_UNSUPPORTED, "model too wide for the linear kernel");

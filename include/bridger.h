@@ -274,6 +274,14 @@ bridger_status bridger_hot_kernel_time(double* total_ms, int64_t* launches);
  * linear-model kernel), 1 = gather-compare K1, 2 = leaf gather / reduce K3,
  * 3 = fused GEMM-form K5. */
 bridger_status bridger_hot_kernel_time_by(int32_t kernel, double* total_ms, int64_t* launches);
+/* Roofline probe (bench.py, live on the measuring box): shared-memory (LSU)
+ * pipe bandwidth on `cuda_device` in GB/s -- one 512-thread CTA per SM issuing
+ * unrolled LDS.64 with lane-consecutive (conflict-free, the 128 B/clk/SM unit
+ * rate) and per-lane random addresses; best of 5 launches each.  Synchronises
+ * the device; runs ~0.2 s.  Errors: invalid device / launch -> BRIDGER_E_CUDA.
+ * Not part of the inference path (the traversal is bound by this pipe,
+ * SURVEY.md §8(d) "Which roofline bounds what"). */
+bridger_status bridger_probe_smem_bandwidth(int32_t cuda_device, double* conflict_free_gbps, double* random_gbps);
 
 #ifdef __cplusplus
 }

@@ -52,7 +52,7 @@ EXPORTS = [
     "bridger_analyze_exactness", "bridger_validate", "bridger_last_error", "bridger_status_string",
     "bridger_launch_count", "bridger_hot_kernel_timing", "bridger_hot_kernel_time", "bridger_model_layout",
     "bridger_hot_kernel_time_by", "bridger_linear_load", "bridger_linear_free", "bridger_linear_predict",
-    "bridger_linear_predict_proba", "bridger_linear_decision",
+    "bridger_linear_predict_proba", "bridger_linear_decision", "bridger_probe_smem_bandwidth",
 ]
 
 
@@ -92,6 +92,7 @@ def _load_lib():
         "bridger_linear_predict": ([vp, vp, i64, i32, vp, vp], i32),
         "bridger_linear_predict_proba": ([vp, vp, i64, i32, vp, vp], i32),
         "bridger_linear_decision": ([vp, vp, i64, i32, vp, vp], i32),
+        "bridger_probe_smem_bandwidth": ([i32, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -127,6 +128,13 @@ def hot_kernel_time(kernel: int = 0):
     ms, n = C.c_double(), C.c_int64()
     _check(_lib.bridger_hot_kernel_time_by(int(kernel), C.byref(ms), C.byref(n)))
     return ms.value, n.value
+
+
+def probe_smem_bandwidth(device: int = 0):
+    """(conflict-free, random) shared-memory LDS.64 GB/s measured now on `device`."""
+    a, b = C.c_double(), C.c_double()
+    _check(_lib.bridger_probe_smem_bandwidth(int(device), C.byref(a), C.byref(b)))
+    return a.value, b.value
 
 
 class _DescKeep:

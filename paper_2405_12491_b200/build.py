@@ -15,7 +15,7 @@ LIB = os.path.join(HERE, "libbridger.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["api.cu", "traverse.cu", "trav_inst_i64.cu", "trav_inst_i64_ml.cu", "trav_inst_f64.cu",
-           "trav_inst_gt_i64.cu", "trav_inst_gt_f64.cu", "trav_inst_sparse.cu", "trav_inst_hybrid.cu", "trav_inst_split.cu", "trav_inst_stream.cu", "trav_inst_stream_split.cu", "trav_inst_stream_codes.cu", "gemm_path.cu", "linear.cu", "lowering.cpp"]
+           "trav_inst_gt_i64.cu", "trav_inst_gt_f64.cu", "trav_inst_sparse.cu", "trav_inst_hybrid.cu", "trav_inst_split.cu", "trav_inst_stream.cu", "trav_inst_stream_split.cu", "trav_inst_stream_codes.cu", "gemm_path.cu", "linear.cu", "probe.cu", "lowering.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-ftz=false", "-prec-div=true", "-prec-sqrt=true",
           "-fmad=true", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
@@ -35,10 +35,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
+    # headers are shared by most units: a newer header rebuilds everything,
+    # otherwise only the units whose own source changed (incremental build)
+    hdr_t = max([os.path.getmtime(os.path.join(CSRC, f)) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))] +
+                [os.path.getmtime(os.path.join(HERE, "..", "include", f))
+                 for f in os.listdir(os.path.join(HERE, "..", "include"))] + [os.path.getmtime(__file__)])
     objs, cmds = [], []
     for s in SOURCES:
         src = os.path.join(CSRC, s)
         obj = os.path.join(objdir, s + ".o")
+        objs_ok = os.path.exists(obj) and os.path.getmtime(obj) >= max(hdr_t, os.path.getmtime(src))
+        if objs_ok and not force:
+            objs.append(obj)
+            continue
         cmd = [NVCC, *ARCH, *COMMON, "-c", src, "-o", obj]
         if s.endswith(".cu"):
             cmd += ["-Xptxas", "-v"] if verbose else []

@@ -3,6 +3,7 @@
 // include/bridger.h.
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <mutex>
 #include <string>
@@ -159,6 +160,25 @@ struct GemmClass {
   int32_t depth, i_pad, l_pad;
   int32_t first_tree, n_trees;   // trees of this depth class (in sorted order)
 };
+
+// ------------------------------------------------ launch configuration -----
+#ifdef __CUDACC__
+// Opt a kernel in to the full 227 KB of dynamic shared memory on the CURRENT
+// device.  The attribute belongs to one device's context, so the cache is a
+// per-device bitmask (one per kernel, passed by the caller as a function-local
+// static), updated atomically: safe when models on several GPUs launch from
+// several threads.  Devices >= 64 are simply configured on every launch.
+inline cudaError_t smem_opt_in(const void* kern, std::atomic<uint64_t>& dev_mask) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = dev < 64 ? (uint64_t)1 << dev : 0;
+  if (bit && (dev_mask.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+  if (e == cudaSuccess && bit) dev_mask.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
+#endif
 
 // ------------------------------------------------------------- finalize -----
 struct FinalizeArgs {

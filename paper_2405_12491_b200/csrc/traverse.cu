@@ -389,6 +389,8 @@ __global__ void __launch_bounds__(512) xpose_kernel(const float* __restrict__ X,
 }
 
 // ------------------------------------------------------------- launchers ----
+static std::atomic<uint64_t> g_xpose_smem{0};  // xpose_kernel's shared-memory opt-in, per device
+
 static int num_sms(int dev) {
   static int cached[64] = {0};
   if (dev >= 0 && dev < 64 && cached[dev]) return cached[dev];
@@ -529,11 +531,7 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
       int nwx = 16;
       while (nwx > 1 && nwx * 32 * (m->F | 1) * 4 > 200 * 1024) --nwx;
       const int xsmem = nwx * 32 * (m->F | 1) * 4;
-      static bool x_attr_s = false;
-      if (!x_attr_s) {
-        cudaFuncSetAttribute(xpose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-        x_attr_s = true;
-      }
+      smem_opt_in(reinterpret_cast<const void*>(xpose_kernel), g_xpose_smem);
       int occ = 1;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, xpose_kernel, nwx * 32, xsmem);
       const int xgrid = (int)std::max<int64_t>(1, std::min<int64_t>((nbk + nwx - 1) / nwx, (int64_t)sms * std::max(1, occ)));
@@ -645,11 +643,7 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
     int nwx = 16;
     while (nwx > 1 && nwx * 32 * (m->F | 1) * 4 > 200 * 1024) --nwx;
     const int xsmem = nwx * 32 * (m->F | 1) * 4;
-    static bool x_attr = false;
-    if (!x_attr) {
-      cudaFuncSetAttribute(xpose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-      x_attr = true;
-    }
+    smem_opt_in(reinterpret_cast<const void*>(xpose_kernel), g_xpose_smem);
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, xpose_kernel, nwx * 32, xsmem);
     const int64_t want_ctas = (nbk + nwx - 1) / nwx;

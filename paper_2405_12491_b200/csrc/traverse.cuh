@@ -712,13 +712,9 @@ template <int KT, typename ACC, bool ML, bool GT, int FMT>
 cudaError_t launch_trav_t(const TravParams& p, int grid_ctas, int block, int smem, int cluster,
                                  cudaStream_t st) {
   auto kern = trav_kernel<KT, ACC, ML, GT, FMT>;
-  static int configured_smem = 0;  // per instantiation
-  cudaError_t e;
-  if (configured_smem < smem) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    if (e != cudaSuccess) return e;
-    configured_smem = 232448;
-  }
+  static std::atomic<uint64_t> configured{0};  // per instantiation, per device
+  cudaError_t e = smem_opt_in(reinterpret_cast<const void*>(kern), configured);
+  if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
   cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = smem;
@@ -1100,12 +1096,9 @@ __global__ void __launch_bounds__(544, 1) trav_stream_kernel(const TravParams p)
 template <int KT, typename ACC, bool ML, int W, bool APPLY, int SPL>
 cudaError_t launch_stream_t(const TravParams& p, int grid, int block, int smem, cudaStream_t st) {
   auto kern = trav_stream_kernel<KT, ACC, ML, W, APPLY, SPL>;
-  static int configured = 0;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    if (e != cudaSuccess) return e;
-    configured = 1;
-  }
+  static std::atomic<uint64_t> configured{0};  // per instantiation, per device
+  cudaError_t e0 = smem_opt_in(reinterpret_cast<const void*>(kern), configured);
+  if (e0 != cudaSuccess) return e0;
   if (std::getenv("BRIDGER_DEBUG"))
     std::fprintf(stderr, "[bridger] trav_stream_kernel W=%d grid=%d block=%d smem=%d chunks=%d ns=%d stage=%d\n", W,
                  grid, block, smem, p.n_chunks, p.stream_ns, p.stream_stage);

@@ -35,38 +35,52 @@ def row_range(n_rows: int, world: int, rank: int) -> Tuple[int, int]:
 
 
 def tree_visits(desc) -> np.ndarray:
-    """Per-tree traversal cost (padded depth = node visits per row)."""
-    offs = np.asarray(desc.tree_offsets)
-    left = np.asarray(desc.left)
-    out = np.zeros(len(offs) - 1, np.int64)
-    for t in range(len(offs) - 1):
-        a, b = int(offs[t]), int(offs[t + 1])
-        l, r = left[a:b], np.asarray(desc.right)[a:b]
-        depth = np.zeros(b - a, np.int64)
-        stack = [0]
-        best = 0
-        while stack:
-            n = stack.pop()
-            if l[n] == -1:
-                best = max(best, depth[n])
-            else:
-                depth[l[n]] = depth[r[n]] = depth[n] + 1
-                stack += [int(l[n]), int(r[n])]
-        out[t] = max(best, 1)
-    return out
+    """Per-tree traversal cost: the longest root-to-leaf path (node visits per
+    row), at least 1.  Vectorised (pointer jumping over parent links), so a
+    10,000-tree depth-10 ensemble costs milliseconds, not a Python walk."""
+    offs = np.asarray(desc.tree_offsets, np.int64)
+    left = np.asarray(desc.left, np.int64)
+    right = np.asarray(desc.right, np.int64)
+    n = int(offs[-1])
+    T = len(offs) - 1
+    if T == 0:
+        return np.zeros(0, np.int64)
+    base = np.repeat(offs[:-1], np.diff(offs))          # tree offset of every node
+    parent = np.full(n, -1, np.int64)
+    inner = np.nonzero(left >= 0)[0]
+    parent[left[inner] + base[inner]] = inner
+    parent[right[inner] + base[inner]] = inner
+    # invariant: depth[v] = edges from v to jump[v] (jump[v] >= 0), else v's depth
+    depth = (parent >= 0).astype(np.int64)
+    jump = parent.copy()
+    while True:
+        live = np.nonzero(jump >= 0)[0]
+        if live.size == 0:
+            break
+        up = jump[live]
+        d_up, j_up = depth[up].copy(), jump[up].copy()   # simultaneous update
+        depth[live] += d_up
+        jump[live] = j_up
+    best = np.maximum.reduceat(depth, offs[:-1]) if n else np.zeros(T, np.int64)
+    return np.maximum(best, 1)
 
 
 def tree_partition(costs: Sequence[int], world: int) -> List[Tuple[int, int]]:
-    """Split trees [0, T) into `world` contiguous ranges of near-equal total cost."""
+    """Split trees [0, T) into `world` contiguous ranges of near-equal total
+    cost.  When T >= world every range holds at least one tree (bounds are
+    clamped to [previous + 1, T - (ranks left)]), so no rank is left without
+    work whatever the cost skew; T < world raises on every rank alike."""
     costs = np.asarray(costs, np.int64)
     T = len(costs)
+    if T < world:
+        raise ValueError(f"{world} ranks but only {T} trees: every tree shard needs >= 1 tree")
     cum = np.concatenate([[0], np.cumsum(costs)])
     total = cum[-1]
     bounds = [0]
     for r in range(1, world):
         target = total * r / world
         j = int(np.searchsorted(cum, target, side="left"))
-        j = max(bounds[-1], min(T, j))
+        j = max(bounds[-1] + 1, min(T - (world - r), j))
         bounds.append(j)
     bounds.append(T)
     return [(bounds[r], bounds[r + 1]) for r in range(world)]
@@ -76,11 +90,14 @@ def _reduce_scatter_sum(out, inp, group=None):
     import torch.distributed as dist
     if dist.get_backend(group) == "nccl":
         dist.reduce_scatter_tensor(out, inp, op=dist.ReduceOp.SUM, group=group)
-    else:  # gloo (CPU tests): all_reduce + own slice
-        buf = inp.clone()
+    else:
+        # gloo (CPU tests, and multi-rank tests sharing one GPU): host-side
+        # all_reduce + own slice.  The partials are staged through host memory
+        # so no collective ever runs on (or waits inside) the device.
+        buf = inp.detach().to("cpu", copy=True)
         dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
         r = dist.get_rank(group)
-        out.copy_(buf.view(dist.get_world_size(group), -1)[r].view_as(out))
+        out.copy_(buf.view(dist.get_world_size(group), -1)[r].view(out.shape))
     return out
 
 
@@ -96,61 +113,109 @@ def reduce_scatter_rows(raw, group=None):
     return _reduce_scatter_sum(out, raw.contiguous(), group)
 
 
-class RowShardedPredictor:
-    """Full model on every rank; each rank predicts its own contiguous rows."""
+def _pinned_host(x):
+    import torch
+    if isinstance(x, np.ndarray):
+        x = torch.from_numpy(np.ascontiguousarray(x, np.float32))
+    return x if x.is_pinned() else x.pin_memory()
 
-    def __init__(self, desc, device: int, variant=None):
+
+class RowShardedPredictor:
+    """Full model on every rank; each rank predicts its own contiguous rows
+    [row_range(N, world, rank)) -- no data-path collective."""
+
+    def __init__(self, desc, device: int, variant=None, group=None):
+        import torch.distributed as dist
+
         from . import Model
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.model = Model(desc, device=device, variant=variant)
+
+    def rows(self, n_rows: int) -> Tuple[int, int]:
+        return row_range(n_rows, self.world, self.rank)
 
     def predict(self, X_local, proba: bool = False):
         return self.model.predict_proba(X_local) if proba else self.model.predict(X_local)
+
+    def predict_host(self, X_host_local, proba: bool = False, out=None):
+        """End to end on this rank's host rows (pinned H2D, predict, D2H)."""
+        return self.model.predict_host(X_host_local, proba=proba, out=out)
 
 
 class TreeShardedPredictor:
     """Rank r holds trees [a_r, b_r); raw partials are reduce-scattered by row."""
 
-    def __init__(self, desc, device: int, group=None):
+    def __init__(self, desc, device: int, group=None, variant=None):
         import torch.distributed as dist
 
         from . import Model, analyze_exactness
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        self.device = int(device)
         q, tier, _ = analyze_exactness(desc)          # of the WHOLE ensemble
         self.total_trees = len(desc.tree_offsets) - 1
-        self.ranges = tree_partition(tree_visits(desc), self.world)
+        self.ranges = tree_partition(tree_visits(desc), self.world)   # raises alike on every rank
         a, b = self.ranges[self.rank]
-        if b <= a:
-            raise ValueError("more ranks than trees")
-        self.model = Model(_subset(desc, range(a, b)), device=device, force_fixed_point=(q, TIER_CODE[tier]))
+        self.model = Model(_subset(desc, range(a, b)), device=device, force_fixed_point=(q, TIER_CODE[tier]),
+                           variant=variant)
+        self._xbuf = None
+
+    def slice_of(self, n_rows: int) -> Tuple[int, int]:
+        """Rows [row0, row1) this rank owns after the reduce-scatter."""
+        n_pad = -(-n_rows // self.world) * self.world
+        row0 = self.rank * (n_pad // self.world)
+        return min(row0, n_rows), min(n_rows, row0 + n_pad // self.world)
+
+    def _reduce_finalize(self, raw, n, proba):
+        import torch
+        n_pad = -(-n // self.world) * self.world
+        if n_pad != n:
+            raw = torch.cat([raw, torch.zeros((n_pad - n, raw.shape[1]), dtype=raw.dtype, device=raw.device)])
+        mine = reduce_scatter_rows(raw, self.group)
+        row0, row1 = self.slice_of(n)
+        return row0, self.model.finalize(mine[: row1 - row0].contiguous(), total_trees=self.total_trees, proba=proba)
 
     def predict(self, X_all, proba: bool = False):
         """X_all: the same [N, F] rows on every rank.  Returns (row0, outputs of
         this rank's row slice [row0, row0 + N_pad/world) clipped to N)."""
+        return self._reduce_finalize(self.model.predict_raw(X_all), X_all.shape[0], proba)
+
+    def predict_host(self, X_host, proba: bool = False):
+        """End to end from HOST rows: pinned H2D of X on every rank, partial
+        sums, ONE reduce-scatter, finalize of the own slice, D2H of it.
+        Returns (row0, host outputs of this rank's slice)."""
         import torch
-        n = X_all.shape[0]
-        n_pad = -(-n // self.world) * self.world
-        raw = self.model.predict_raw(X_all)
-        if n_pad != n:
-            raw = torch.cat([raw, torch.zeros((n_pad - n, raw.shape[1]), dtype=raw.dtype, device=raw.device)])
-        mine = reduce_scatter_rows(raw, self.group)
-        row0 = self.rank * (n_pad // self.world)
-        keep = max(0, min(mine.shape[0], n - row0))
-        out = self.model.finalize(mine[:keep].contiguous(), total_trees=self.total_trees, proba=proba)
-        return row0, out
+        X_host = _pinned_host(X_host)
+        dev = torch.device("cuda", self.device)
+        if self._xbuf is None or self._xbuf.shape != X_host.shape:
+            self._xbuf = torch.empty(X_host.shape, dtype=torch.float32, device=dev)
+        self._xbuf.copy_(X_host, non_blocking=True)
+        row0, out = self.predict(self._xbuf, proba=proba)
+        host = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+        host.copy_(out, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        return row0, host
 
 
 def _subset(desc, trees):
-    """Model made of the listed trees (node arrays re-based); desc-agnostic."""
+    """Model made of the listed trees (node arrays re-based); desc-agnostic.
+    Honours per-tree scalar outputs (``tree_output``, reading c15): such models
+    store ONE value per node, otherwise K."""
     from types import SimpleNamespace
     trees = list(trees)
+    if not trees:
+        raise ValueError("empty tree subset")
     offs = np.asarray(desc.tree_offsets, np.int64)
     K = int(desc.n_outputs)
+    tout = getattr(desc, "tree_output", None)
+    vw = 1 if tout is not None else K
     idx = np.concatenate([np.arange(offs[t], offs[t + 1]) for t in trees])
     sizes = [int(offs[t + 1] - offs[t]) for t in trees]
     new_offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
-    val = np.asarray(desc.value, np.float32).reshape(-1, K)[idx].reshape(-1)
+    val = np.asarray(desc.value, np.float32).reshape(-1, vw)[idx].reshape(-1)
     ml = getattr(desc, "missing_left", None)
     return SimpleNamespace(
         n_features=desc.n_features, n_outputs=K, tree_offsets=new_offs,
@@ -158,7 +223,8 @@ def _subset(desc, trees):
         left=np.asarray(desc.left)[idx], right=np.asarray(desc.right)[idx], value=val,
         missing_left=None if ml is None else np.asarray(ml)[idx], task=getattr(desc, "task", 0),
         agg=getattr(desc, "agg", 0), post=getattr(desc, "post", 0), base_score=getattr(desc, "base_score", None),
-        leaf_scale=getattr(desc, "leaf_scale", 1.0))
+        leaf_scale=getattr(desc, "leaf_scale", 1.0),
+        tree_output=None if tout is None else np.asarray(tout, np.int32)[trees])
 
 
 # ------------------------------------------------------------- 2-D sharding --
@@ -194,7 +260,7 @@ class TwoDShardedPredictor:
         self.comms = make_row_group_comms(world, row_groups)
         q, tier, _ = analyze_exactness(desc)
         self.total_trees = len(desc.tree_offsets) - 1
-        a, b = tree_partition(tree_visits(desc), self.tg_n)[self.tg]
+        a, b = tree_partition(tree_visits(desc), self.tg_n)[self.tg]   # raises alike on every rank
         self.model = Model(_subset(desc, range(a, b)), device=device, force_fixed_point=(q, TIER_CODE[tier]))
 
     def predict(self, X_rows, proba: bool = False):

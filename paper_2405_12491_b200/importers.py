@@ -156,13 +156,21 @@ def from_xgboost_json(model: dict) -> Ensemble:
     if gb.get("name", "gbtree") not in ("gbtree", "dart"):
         raise ValueError(f"unsupported booster {gb.get('name')}")
     gm = gb["model"] if "model" in gb else gb["gbtree"]["model"]
+    # DART: at inference every tree's output is multiplied by its weight_drop
+    # (fp32 tree weights); folded into the leaf values (one fp32 rounding per
+    # leaf, as XGBoost's own weight * leaf product)
+    wdrop = None
+    if gb.get("name") == "dart":
+        wdrop = np.asarray(gb.get("weight_drop", []), np.float32)
+        if len(wdrop) != len(gm["trees"]):
+            raise ValueError(f"dart booster: {len(wdrop)} weight_drop entries for {len(gm['trees'])} trees")
     mp = lrn["learner_model_param"]
     F = int(mp["num_feature"])
     K = max(1, int(mp.get("num_class", "0")))
     objective = lrn.get("objective", {}).get("name", "reg:squarederror")
     base = _xgb_float(mp.get("base_score", "0.5"))
     trees = []
-    for tj in gm["trees"]:
+    for ti, tj in enumerate(gm["trees"]):
         lc = np.asarray(tj["left_children"], np.int64)
         rc = np.asarray(tj["right_children"], np.int64)
         if any(int(s) != 0 for s in tj.get("split_type", [])):
@@ -175,7 +183,8 @@ def from_xgboost_json(model: dict) -> Ensemble:
         trees.append(dict(feature=np.where(leaf, 0, np.asarray(tj["split_indices"], np.int64)).astype(np.int32),
                           threshold=np.where(leaf, np.float32(0), thr).astype(np.float32),
                           left=lc.astype(np.int32), right=rc.astype(np.int32),
-                          value=np.where(leaf, cond, np.float32(0)).astype(np.float32),
+                          value=np.where(leaf, cond if wdrop is None else (cond * wdrop[ti]).astype(np.float32),
+                                         np.float32(0)).astype(np.float32),
                           missing_left=np.asarray(tj["default_left"], np.uint8)))
     T = len(trees)
     if objective in ("binary:logistic", "reg:logistic", "binary:logitraw"):
@@ -248,11 +257,17 @@ def from_lightgbm_json(dump: dict) -> Ensemble:
     trees = [_lgb_tree(t["tree_structure"], flags) for t in dump["tree_info"]]
     agg = AGG_MEAN if dump.get("average_output", False) else AGG_SUM
     name = obj[0] if obj else "regression"
+    # objective flags with an output transform this path does not apply
+    if "sqrt" in obj[1:]:
+        raise ValueError("LightGBM 'regression sqrt' (sign(x) x^2 output transform) is not supported")
     if name == "binary":
         sig = 1.0
         for o in obj[1:]:
             if o.startswith("sigmoid:"):
                 sig = float(o.split(":")[1])
+        if agg == AGG_MEAN and sig != 1.0:
+            # MEAN finalisation is sum / T (reading c6): leaf_scale would be ignored
+            raise ValueError("average_output binary models with sigmoid:s != 1 are not supported")
         return _pack(trees, F, 1, task=TASK_CLASSIFICATION, agg=agg, post=POST_SIGMOID, leaf_scale=sig,
                      base_score=np.zeros(1))
     if name in ("multiclass", "softmax"):

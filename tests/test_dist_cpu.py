@@ -16,7 +16,8 @@ import oracle
 import paper_2405_12491_b200 as B
 from paper_2405_12491_b200.dist import (grid_2d, make_row_group_comms, reduce_scatter_rows, row_range,
                                         tree_partition, tree_visits)
-from synth import gen_x, make_config, perfect_ensemble, prune_ensemble
+from paper_2405_12491_b200.dist import _subset
+from synth import gen_x, make_config, multiclass_gbdt, perfect_ensemble, prune_ensemble
 
 
 def test_row_range_covers_exactly():
@@ -37,6 +38,37 @@ def test_tree_partition_balanced_contiguous():
         assert all(b == c for (_, b), (c, _) in zip(parts, parts[1:]))
         loads = [cost[a:b].sum() for a, b in parts]
         assert max(loads) - min(loads) <= 2 * cost.max()
+
+
+def test_tree_partition_nonempty_under_skew():
+    # costs [8, 8, 1, 1] on 4 ranks used to give an empty range
+    for costs, w in (([8, 8, 1, 1], 4), ([100, 1, 1, 1, 1], 5), ([1] * 7 + [50], 8), ([3, 3], 2)):
+        parts = tree_partition(costs, w)
+        assert all(b > a for a, b in parts), parts
+        assert parts[0][0] == 0 and parts[-1][1] == len(costs)
+        assert all(b == c for (_, b), (c, _) in zip(parts, parts[1:]))
+    with pytest.raises(ValueError):
+        tree_partition([1, 2, 3], 4)
+
+
+def test_subset_keeps_scalar_tree_outputs():
+    """Round-1 bug: ``_subset`` reshaped scalar leaves as K-vectors and dropped
+    tree_output (multiclass boosting, reading c15).  The shard must equal the
+    same trees taken by ModelDesc.subset, and the shards' oracle sums add up
+    to the whole ensemble's."""
+    m = multiclass_gbdt(81, 30, 6, 14, 5)
+    X = gen_x(82, 0, 97, 14)
+    full = oracle.run(m, X)["acc"]
+    tot = np.zeros_like(full)
+    for a, b in tree_partition(tree_visits(m), 3):
+        sub = _subset(m, range(a, b))
+        ref = m.subset(range(a, b))
+        assert len(sub.value) == len(ref.value) == int(ref.tree_offsets[-1])
+        np.testing.assert_array_equal(sub.tree_output, np.arange(a, b) % 5)
+        acc = oracle.run(sub, X)["acc"]
+        np.testing.assert_array_equal(acc, oracle.run(ref, X)["acc"])
+        tot += acc
+    np.testing.assert_allclose(tot, full, rtol=1e-12, atol=1e-12)
 
 
 def _free_port():

@@ -21,6 +21,39 @@ def test_xgboost_binary_logistic_strict_less_and_default_left():
     np.testing.assert_allclose(o["proba"][:, 1], g["expected"]["p1"], rtol=1e-6)
 
 
+def test_xgboost_dart_weight_drop():
+    """DART boosters scale each tree's output by weight_drop[i] at
+    inference.  Same two trees as xgboost_binary_logistic.json with weights
+    (0.5, 2.0); margins by hand: r0 0.5*0.4 + 2*0.25 = 0.7, r1 0.5*0.3 + 2*0.25
+    = 0.65, r2 0.5*(-0.2) + 2*0.25 = 0.4, r3 0.5*0.3 + 2*(-0.1) = -0.05."""
+    import copy
+    g = load_golden("xgboost_binary_logistic.json")
+    d = copy.deepcopy(g["model"])
+    gb = d["learner"]["gradient_booster"]
+    d["learner"]["gradient_booster"] = {"name": "dart", "gbtree": {"name": "gbtree", "model": gb["model"]},
+                                        "weight_drop": [0.5, 2.0]}
+    m = I.from_xgboost_json(d)
+    o = oracle.run(m, parse_x(g["X"]))
+    np.testing.assert_allclose(o["s"][:, 0], [0.7, 0.65, 0.4, -0.05], rtol=1e-6, atol=1e-7)
+    assert o["label"].tolist() == [1, 1, 1, 0]
+    d["learner"]["gradient_booster"]["weight_drop"] = [1.0]
+    with pytest.raises(ValueError):
+        I.from_xgboost_json(d)
+
+
+def test_lightgbm_unhandled_output_transforms_rejected():
+    import copy
+    g = load_golden("lightgbm_binary_dump.json")
+    d = copy.deepcopy(g["model"])
+    d["objective"] = "regression sqrt"
+    with pytest.raises(ValueError):
+        I.from_lightgbm_json(d)
+    d = copy.deepcopy(g["model"])
+    d["objective"], d["average_output"] = "binary sigmoid:2", True
+    with pytest.raises(ValueError):
+        I.from_lightgbm_json(d)
+
+
 def test_xgboost_multiclass_softprob():
     g = load_golden("xgboost_multiclass_softprob.json")
     m = I.from_xgboost_json(g["model"])

@@ -427,6 +427,10 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
     int32_t xbudget = (codes && xw <= 16 * 1024) ? 144 * 1024 : 120 * 1024;
     if (const char* e = std::getenv("BRIDGER_XBUDGET")) xbudget = 1024 * std::atoi(e);  // experiments
     while (nb > 1 && nb * xw > xbudget) nb /= 2;
+    // wide coded inputs (>= 16 KB code blocks, C5-shaped): 12 warps, measured
+    // on B200 with the K4d kernel (1250-tree shard, 1M rows: 7.94 ms vs 8.29 at
+    // 16 and 8.47 at 8 warps; profiles/r2_deep_sweep.jsonl)
+    if (codes && code_buf_bytes(F) >= 16 * 1024) nw = 12;
     if (const char* e = std::getenv("BRIDGER_WARPS")) nw = std::max(1, std::min(16, std::atoi(e)));  // experiments
     if (const char* e = std::getenv("BRIDGER_BLOCKS")) nb = std::max(1, std::min(16, std::atoi(e)));
     nb = std::min(nb, nw);
@@ -435,7 +439,9 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
     misc = 1024 + trav_bar_bytes(nb) + trav_red_bytes(nb, G, K);
     const int32_t base_budget = kSmemMax - misc - trav_x_region(codes, F, nb);
     auto chunk_bytes = [&](int32_t n, int32_t D) -> int64_t {
-      const int64_t nodes = (int64_t)n * ((1 << D) - 1) * node_bytes + (node_bytes == 5 ? 16 : 0);
+      // codes: [pad word][I node words] per tree (2^D words, see the packing below)
+      const int64_t nodes = codes ? (int64_t)n * (1 << D) * 4
+                                  : (int64_t)n * ((1 << D) - 1) * node_bytes + (node_bytes == 5 ? 16 : 0);
       return (nodes + 31) / 32 * 32 + ((int64_t)n * (1 << D) * K * 4 + 15) / 16 * 16;
     };
     out->global_trees = false;
@@ -706,6 +712,7 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
     c.first_slot = r.start;
     const int64_t nodes = out->split ? (((int64_t)r.n * I * 4 + 15) / 16 * 16 + (int64_t)r.n * I)
                           : (out->stream && out->codes) ? (int64_t)r.n * I * 4
+                          : out->codes ? (int64_t)r.n * (I + 1) * 4
                           : out->stream ? (int64_t)r.n * (out->stream_split ? ((((int64_t)5 << D) + 15) / 16 * 16) : (int64_t)(I + 1) * 8)
                                         : (int64_t)r.n * I * node_bytes;
     c.leaf_offset = (int32_t)((nodes + 31) / 32 * 32);  // 32-byte aligned leaf vectors (256-bit gathers)
@@ -718,8 +725,12 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
       if (out->codes) {
         // node word: code index j (bits 16..31) | byte offset of the feature's
         // code within a lane's view of a [F/2][32][2] u16 code block (bits
-        // 1..14: (f/2)*128 + (f%2)*2, always even, F <= 512) | missing (bit 0)
-        uint32_t* nd = reinterpret_cast<uint32_t*>(base) + (size_t)j * I;
+        // 1..14: (f/2)*128 + (f%2)*2, always even, F <= 512) | missing (bit 0).
+        // Resident chunks store tree j at words [j (I + 1), (j + 1)(I + 1)):
+        // a pad word, then nodes 0..I-1, so that the two children 2i+1, 2i+2
+        // of every node form one 8-byte-aligned pair (the speculative walk of
+        // trav_deep.cu loads both with one LDS.64); streamed chunks are dense.
+        uint32_t* nd = reinterpret_cast<uint32_t*>(base) + (out->stream ? (size_t)j * I : (size_t)j * (I + 1) + 1);
         for (int32_t i = 0; i < I; ++i) {
           // real nodes: t is in U_f, exact index; dummy nodes under replicated
           // leaves (feature 0, threshold 0): any code routes to identical leaves

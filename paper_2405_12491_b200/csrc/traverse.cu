@@ -12,6 +12,9 @@
 
 namespace bridger {
 
+cudaError_t launch_trav_deep(const TravParams& p, int K, bool ml, int grid, int block, int smem, cudaStream_t st);
+int trav_deep_smem(int chunk_cap, int code_buf, int nb);
+
 #define BRIDGER_TRAV_EXTERN(ACC, ML, GT, FMT)                                                                           \
   extern template cudaError_t launch_trav_t<1, ACC, ML, GT, FMT>(const TravParams&, int, int, int, int, cudaStream_t);  \
   extern template cudaError_t launch_trav_t<2, ACC, ML, GT, FMT>(const TravParams&, int, int, int, int, cudaStream_t);  \
@@ -606,6 +609,12 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
   int smem = p.slot_off;
   int cluster = 1;
   void* partial = nullptr;
+  // K4d (trav_deep.cu): coded chunks, several of them, exact int64 tiers ->
+  // per-warp red.global.add into one accumulator instead of per-chunk partials
+  // + combine (BRIDGER_DEEP=0 keeps K4's partials, for comparison)
+  const char* deep_env = std::getenv("BRIDGER_DEEP");
+  const bool deep = L.codes && !L.global_trees && want != 3 && m->acc_int && n_chunks >= 3 &&
+                    !(deep_env && deep_env[0] == '0');
   if (want == 3) {
     p.mode = TRAV_APPLY;
     p.out_leaf = static_cast<int32_t*>(out);
@@ -615,7 +624,7 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
     p.mode = TRAV_CLUSTER;
     cluster = n_chunks;
     smem += trav_slot_bytes(NB, n_chunks, m->K);
-  } else {
+  } else if (!deep) {
     p.mode = TRAV_PARTIAL;
     cudaError_t e = cudaMallocAsync(&partial, (size_t)n_chunks * n_rows * m->K * 8, st);
     if (e != cudaSuccess) return e;
@@ -656,6 +665,32 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
       return err;
     }
     p.X = static_cast<const float*>(codes);
+  }
+  if (deep) {
+    void* acc = want == 2 ? out : nullptr;
+    if (!acc) err = cudaMallocAsync(&acc, (size_t)n_rows * m->K * 8, st);
+    if (err == cudaSuccess) err = cudaMemsetAsync(acc, 0, (size_t)n_rows * m->K * 8, st);
+    if (err == cudaSuccess) {
+      p.mode = TRAV_PARTIAL;
+      p.partial = acc;
+      // child-pair speculation from this depth on (latency-bound deep chunks)
+      p.spec_min_d = 9;
+      if (const char* e = std::getenv("BRIDGER_SPEC_D")) p.spec_min_d = std::atoi(e);
+      const int dsmem = trav_deep_smem(p.chunk_cap, p.code_buf, NB);
+      err = launch_trav_deep(p, m->K, L.has_missing, grid, block, dsmem, st);
+    }
+    if (err == cudaSuccess && want != 2) {
+      const int tb = 256;
+      const int g = (int)((n_rows + tb - 1) / tb);
+      BRIDGER_DISPATCH_KT(m->K, {
+        trav_combine_kernel<KT, long long><<<g, tb, 0, st>>>(static_cast<const long long*>(acc), 1, n_rows, fin);
+      });
+      count_launch();
+      err = cudaGetLastError();
+    }
+    if (acc && want != 2) cudaFreeAsync(acc, st);
+    if (codes) cudaFreeAsync(codes, st);
+    return err;
   }
   BRIDGER_DISPATCH_KT(m->K, {
     auto launch = [&]() {

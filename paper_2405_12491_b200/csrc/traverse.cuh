@@ -79,6 +79,7 @@ struct TravParams {
   int32_t code_buf;   // codes: bytes (2^b) of one aligned code-block buffer
   uint32_t k2, k16;   // 2 and 65536, opaque to the compiler: keeps the walk's
                       // multiplies on the FMA pipe (IMAD) instead of the ALU pipe
+  int32_t spec_min_d; // trav_deep: chunks of depth >= this walk with child-pair speculation
   FinalizeArgs fin;   // (TRAV_FINAL, TRAV_CLUSTER)
 };
 
@@ -146,14 +147,16 @@ __device__ __forceinline__ void walk_trees(const TravParams& p, const TravChunk&
     // idx' = 2 idx + 1 + r  <=>  A' = 2 A + (r ? 8 : 4) - base_u.
     // The two multiplies use opaque constants (p.k2, p.k16) so they issue on
     // the FMA pipe; the LOP3 / compare / select use the ALU pipe.
-    const uint32_t nb = ptx::s2u(nodes) + 4u * (uint32_t)(j * I);
+    // tree u of the chunk at words [(j+u)(I+1), ...): a pad word, then nodes
+    // 0..I-1 (lowering.cpp), so node 0 of tree u sits at nb + 4 (u (I+1))
+    const uint32_t nb = ptx::s2u(nodes) + 4u * (uint32_t)(j * (I + 1)) + 4u;
     const uint32_t xb = ptx::s2u(xl);
     const uint32_t mask = (uint32_t)p.code_buf - 2u;  // feature offset bits, not the missing bit
     const uint32_t k2 = p.k2, k16 = p.k16;
     uint32_t A[NI], cb[NI];  // cb = 4 - base_u:  A' = A * 2 + cb (+ 4 if right)
 #pragma unroll
     for (int u = 0; u < NI; ++u) {
-      A[u] = nb + 4u * (uint32_t)(u * I);  // shared address of tree u's current node
+      A[u] = nb + 4u * (uint32_t)(u * (I + 1));  // shared address of tree u's current node
       cb[u] = 4u - A[u];
     }
     for (int lvl = 0; lvl < D; ++lvl) {

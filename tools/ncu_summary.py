@@ -19,7 +19,9 @@ KEYS = [
     "sm__throughput.avg.pct_of_peak_sustained_elapsed",
     "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
     "sm__pipe_tensor_subpipe_imma_cycles_active_realtime.avg", "lts__t_bytes.sum",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sectors_srcunit_tex_op_read.sum",
 ]
+STALL = "smsp__pcsamp_warps_issue_stalled_"
 
 
 def summarize_rep(rep):
@@ -35,6 +37,13 @@ def summarize_rep(rep):
                 if h == k or h.endswith("." + k):
                     out.append(f"  {h:90s} {d[h]:>16s} {units[hdr.index(h)]}")
                     break
+        # warp-stall sampling: share of all samples per reason (top 8)
+        st = {h[len(STALL):]: float(d[h] or 0) for h in hdr
+              if h.startswith(STALL) and not h.endswith("not_issued") and d[h] not in ("", "n/a")}
+        tot = sum(st.values())
+        if tot > 0:
+            top = sorted(st.items(), key=lambda kv: -kv[1])[:8]
+            out.append("  stall samples: " + ", ".join(f"{k} {100 * v / tot:.1f}%" for k, v in top))
     return "\n".join(out) + "\n"
 
 

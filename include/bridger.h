@@ -68,8 +68,12 @@ typedef enum {
   BRIDGER_VARIANT_GEMM = 2,     /* a1..a7 fused (K5): producer warps write the int8
                                    decisions straight into shared memory, int8 tcgen05 path contraction
                                    into TMEM, leaf select + gather + reduce in the epilogue warps */
-  BRIDGER_VARIANT_GEMM_STAGED = 3 /* the same operator form staged through HBM: K1 gather-compare ->
+  BRIDGER_VARIANT_GEMM_STAGED = 3, /* the same operator form staged through HBM: K1 gather-compare ->
                                    K2 tcgen05 contraction -> K3 leaf gather/reduce (step-level kernels) */
+  BRIDGER_VARIANT_GEMM_SPARSE = 4 /* staged, with K2 replaced by the 2:4-sparse path contraction
+                                   (tcgen05.mma.sp kind::i8, "sparse operator replacing" PAPER.md:502,
+                                   Table 2): S^T = C_sp^T . P^T with the level-regrouped
+                                   path matrix as the compressed sparse A operand, metadata in TMEM */
 } bridger_variant;
 
 /*
@@ -196,6 +200,13 @@ bridger_status bridger_step_path_scores(const bridger_model* m, int32_t depth, c
                                         int64_t rows, int32_t* out_S, void* stream);
 /* geometry of the GEMM lowering for a depth: I_pad (K), L_pad (N). */
 bridger_status bridger_gemm_geometry(int32_t depth, int32_t* i_pad, int32_t* l_pad);
+/* a3 on the 2:4-sparse form (K2s, variant GEMM_SPARSE): S[r][l] = sum_k P[r][k] *
+ * C_sp[k][l] for P given in the SPARSE K order of bridger_path_matrix_sparse
+ * (int8 0/1 [rows][k_sp], row-major; values at the pad positions are ignored
+ * because C_sp is zero there).  out_S int32 [rows][l_pad] (l_pad as in
+ * bridger_gemm_geometry).  Errors: depth not in the model -> BRIDGER_E_SHAPE. */
+bridger_status bridger_step_path_scores_sparse(const bridger_model* m, int32_t depth, const int8_t* P,
+                                               int64_t rows, int32_t* out_S, void* stream);
 
 /* --- host-only helpers (no device needed) ---------------------------------- */
 /* Universal path matrix of depth D (step a0): C[i*l_pad + l] = +1 if leaf l is
@@ -203,6 +214,16 @@ bridger_status bridger_gemm_geometry(int32_t depth, int32_t* i_pad, int32_t* l_p
  * (i < I_pad, rows >= I zero); Dv[l] = number of left turns on l's path
  * (D - popcount(l)), l < L.  C has i_pad*l_pad entries, Dv has 2^D. */
 bridger_status bridger_path_matrix(int32_t depth, int8_t* C, int32_t* Dv);
+/* The path matrix with its K dimension (internal nodes) regrouped for 2:4
+ * structured sparsity ("sparse operator replacing",
+ * PAPER.md:502): heap node i sits at K position pos(i) = i + [i >= 3] (one zero
+ * row after the two level-1 nodes, so levels 0+1 share the first group of four
+ * and every deeper level starts on a group boundary).  A leaf has exactly one
+ * ancestor per level, hence <= 2 non-zeros in the first group and <= 1 in every
+ * other group of 4 consecutive K positions.  C[k*m_sp + l] for k < k_sp =
+ * round_up(2^D, 64), l < m_sp = round_up(2^D, 128) (zero outside pos(i), l < L).
+ * C may be NULL (dimensions only).  depth in [1, 8] else BRIDGER_E_UNSUPPORTED. */
+bridger_status bridger_path_matrix_sparse(int32_t depth, int8_t* C, int32_t* k_sp, int32_t* m_sp);
 /* Padded perfect form of tree t (step a0): depth, then heap arrays feature[I],
  * threshold[I], missing_left[I], leaf_id[L] (original ids), leaf_value[L*K].
  * Call with all arrays NULL to query *depth first. */

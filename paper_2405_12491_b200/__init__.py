@@ -20,7 +20,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libbridger.so")
 
 OK, E_NULL_ARG, E_SHAPE, E_INVALID_TREE, E_UNSUPPORTED, E_CUDA, E_OOM = range(7)
-VARIANTS = {"auto": 0, "traverse": 1, "gemm": 2, "gemm_staged": 3}
+VARIANTS = {"auto": 0, "traverse": 1, "gemm": 2, "gemm_staged": 3, "gemm_sparse": 4}
 TIERS = {0: "E53", 1: "E63", 2: "F64"}
 
 
@@ -53,6 +53,7 @@ EXPORTS = [
     "bridger_launch_count", "bridger_hot_kernel_timing", "bridger_hot_kernel_time", "bridger_model_layout",
     "bridger_hot_kernel_time_by", "bridger_linear_load", "bridger_linear_free", "bridger_linear_predict",
     "bridger_linear_predict_proba", "bridger_linear_decision", "bridger_probe_smem_bandwidth",
+    "bridger_path_matrix_sparse", "bridger_step_path_scores_sparse",
 ]
 
 
@@ -93,6 +94,8 @@ def _load_lib():
         "bridger_linear_predict_proba": ([vp, vp, i64, i32, vp, vp], i32),
         "bridger_linear_decision": ([vp, vp, i64, i32, vp, vp], i32),
         "bridger_probe_smem_bandwidth": ([i32, vp, vp], i32),
+        "bridger_path_matrix_sparse": ([i32, vp, vp, vp], i32),
+        "bridger_step_path_scores_sparse": ([vp, i32, vp, i64, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -200,6 +203,16 @@ def path_matrix(depth: int):
     Dv = np.zeros(1 << depth, np.int32)
     _check(_lib.bridger_path_matrix(depth, Cm.ctypes.data, Dv.ctypes.data))
     return Cm, Dv
+
+
+def path_matrix_sparse(depth: int):
+    """(C_sp [k_sp, m_sp] int8) -- the path matrix with K regrouped for 2:4
+    sparsity (node i at K position i + [i >= 3]), as the library lowers it."""
+    ks, ms = C.c_int32(), C.c_int32()
+    _check(_lib.bridger_path_matrix_sparse(depth, None, C.byref(ks), C.byref(ms)))
+    Cm = np.zeros((ks.value, ms.value), np.int8)
+    _check(_lib.bridger_path_matrix_sparse(depth, Cm.ctypes.data, None, None))
+    return Cm
 
 
 def lower_tree(m, tree: int):
@@ -378,6 +391,17 @@ class Model:
                                            out.data_ptr(), _stream_ptr(X.device)))
         return out
 
+    def step_path_scores_sparse(self, depth: int, P):
+        """a3 on the 2:4-sparse tensor path (K2s): P [rows, k_sp] int8 in the
+        sparse K order -> S [rows, l_pad] int32."""
+        import torch
+        _, lp = gemm_geometry(depth)
+        rows = P.shape[0]
+        out = torch.empty((rows, lp), dtype=torch.int32, device=P.device)
+        _check(_lib.bridger_step_path_scores_sparse(self._h, depth, P.data_ptr(), rows, out.data_ptr(),
+                                                    _stream_ptr(P.device)))
+        return out
+
     def step_path_scores(self, depth: int, P):
         import torch
         ip, lp = gemm_geometry(depth)
@@ -388,7 +412,7 @@ class Model:
         return out
 
 
-__all__ = ["Model", "BridgerError", "validate", "analyze_exactness", "path_matrix", "lower_tree",
+__all__ = ["Model", "BridgerError", "validate", "analyze_exactness", "path_matrix", "path_matrix_sparse", "lower_tree",
            "gemm_geometry", "launch_count", "lib", "LIB_PATH", "EXPORTS"]
 
 

@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "bridger_internal.h"
+#include "variant_table.h"
 
 namespace bridger {
 
@@ -58,6 +59,10 @@ cudaError_t gemm_step_decisions(const bridger_model* m, const float* X, int64_t 
                                 int32_t n_trees, int8_t* out, cudaStream_t st, std::string* why);
 cudaError_t gemm_step_scores(const bridger_model* m, int32_t depth, const int8_t* P, int64_t rows,
                              int32_t* out, cudaStream_t st, std::string* why);
+cudaError_t gemm_step_scores_sparse(const bridger_model* m, int32_t depth, const int8_t* P, int64_t rows,
+                                    int32_t* out, cudaStream_t st, std::string* why);
+cudaError_t gemm_run_sparse(const bridger_model* m, const float* X, int64_t n_rows, void* out, int want,
+                            int32_t total_trees, cudaStream_t st);
 
 struct DeviceGuard {
   int prev = -1;
@@ -127,9 +132,18 @@ static void free_model(bridger_model* m) {
 
 static int32_t resolve_variant(const bridger_model* m, int32_t v) {
   if (v == BRIDGER_VARIANT_TRAVERSE) return m->trav_ok ? v : -1;
-  if (v == BRIDGER_VARIANT_GEMM || v == BRIDGER_VARIANT_GEMM_STAGED) return m->gemm_ok ? v : -1;
-  // AUTO: measured on B200: the traversal wins at
-  // every depth the GEMM form supports, so AUTO = traversal when available.
+  if (v == BRIDGER_VARIANT_GEMM || v == BRIDGER_VARIANT_GEMM_STAGED || v == BRIDGER_VARIANT_GEMM_SPARSE)
+    return m->gemm_ok ? v : -1;
+  // AUTO: the per-depth table measured on B200 (variant_table.h, generated
+  // from profiles/variant_table.json by tools/variant_table.py +
+  // tools/gen_variant_table.py; DESIGN.md §6 "Variant table"), indexed by the
+  // model's deepest padded tree; a variant the model cannot run falls back to
+  // the other form.
+  const int32_t d = m->max_depth < 0 ? 0 : m->max_depth > 15 ? 15 : m->max_depth;
+  const int32_t want = kVariantByDepth[d];
+  if ((want == BRIDGER_VARIANT_GEMM || want == BRIDGER_VARIANT_GEMM_STAGED || want == BRIDGER_VARIANT_GEMM_SPARSE) &&
+      m->gemm_ok)
+    return want;
   if (m->trav_ok) return BRIDGER_VARIANT_TRAVERSE;
   if (m->gemm_ok) return BRIDGER_VARIANT_GEMM;
   return -1;
@@ -164,6 +178,8 @@ static bridger_status run(const bridger_model* m, const float* X, int64_t n_rows
     e = gemm_run_fused(m, X, n_rows, out, want, m->T, st);
   else if (v == BRIDGER_VARIANT_GEMM_STAGED && want != 3)
     e = gemm_run(m, X, n_rows, out, want, m->T, st);
+  else if (v == BRIDGER_VARIANT_GEMM_SPARSE && want != 3)
+    e = gemm_run_sparse(m, X, n_rows, out, want, m->T, st);
   else if (m->trav_ok)
     e = trav_run(m, X, n_rows, out, want, m->T, st);
   else if (m->gemm_ok)
@@ -241,6 +257,14 @@ bridger_status bridger_path_matrix(int32_t depth, int8_t* C, int32_t* Dv) {
   if (depth < 1 || depth > 8) return fail(BRIDGER_E_UNSUPPORTED, "path matrix depth must be in [1,8]");
   if (!C) return fail(BRIDGER_E_NULL_ARG, "C is NULL");
   path_matrix(depth, gemm_i_pad(depth), gemm_l_pad(depth), C, Dv);
+  return BRIDGER_OK;
+}
+
+bridger_status bridger_path_matrix_sparse(int32_t depth, int8_t* C, int32_t* k_sp, int32_t* m_sp) {
+  if (depth < 1 || depth > 8) return fail(BRIDGER_E_UNSUPPORTED, "sparse path matrix depth must be in [1,8]");
+  if (k_sp) *k_sp = gemm_k_sp(depth);
+  if (m_sp) *m_sp = gemm_m_sp(depth);
+  if (C) path_matrix_sparse(depth, C);
   return BRIDGER_OK;
 }
 
@@ -365,6 +389,7 @@ bridger_status bridger_model_load(const bridger_model_desc* d_in, int cuda_devic
     if (!std::strcmp(env, "traverse")) v = BRIDGER_VARIANT_TRAVERSE;
     else if (!std::strcmp(env, "gemm")) v = BRIDGER_VARIANT_GEMM;
     else if (!std::strcmp(env, "gemm_staged")) v = BRIDGER_VARIANT_GEMM_STAGED;
+    else if (!std::strcmp(env, "gemm_sparse")) v = BRIDGER_VARIANT_GEMM_SPARSE;
   }
   m->variant = v;
   m->resolved_variant = resolve_variant(m, v);
@@ -390,7 +415,7 @@ bridger_status bridger_model_info(const bridger_model* m, int32_t* max_depth, in
 
 bridger_status bridger_model_set_variant(bridger_model* m, int32_t variant) {
   if (!m) return fail(BRIDGER_E_NULL_ARG, "model is NULL");
-  if (variant < 0 || variant > 3) return fail(BRIDGER_E_UNSUPPORTED, "unknown variant");
+  if (variant < 0 || variant > 4) return fail(BRIDGER_E_UNSUPPORTED, "unknown variant");
   const int32_t r = resolve_variant(m, variant);
   if (r < 0) return fail(BRIDGER_E_UNSUPPORTED, "variant not available for this model");
   m->variant = variant;
@@ -523,6 +548,21 @@ bridger_status bridger_step_decisions(const bridger_model* m, const float* X, in
   cudaError_t e = gemm_step_decisions(m, X, n_rows, tree0, n_trees, out_P, static_cast<cudaStream_t>(stream), &why);
   if (!why.empty()) return fail(BRIDGER_E_SHAPE, why);
   if (e != cudaSuccess) return cuda_fail(e, "step_decisions");
+  return BRIDGER_OK;
+}
+
+bridger_status bridger_step_path_scores_sparse(const bridger_model* m, int32_t depth, const int8_t* P, int64_t rows,
+                                               int32_t* out_S, void* stream) {
+  if (!m) return fail(BRIDGER_E_NULL_ARG, "model is NULL");
+  if (rows < 0) return fail(BRIDGER_E_SHAPE, "rows < 0");
+  if (rows == 0) return BRIDGER_OK;
+  if (!P || !out_S) return fail(BRIDGER_E_NULL_ARG, "P or out_S is NULL");
+  if (!m->gemm_ok) return fail(BRIDGER_E_UNSUPPORTED, "model has no GEMM lowering");
+  DeviceGuard g(m->device);
+  std::string why;
+  cudaError_t e = gemm_step_scores_sparse(m, depth, P, rows, out_S, static_cast<cudaStream_t>(stream), &why);
+  if (!why.empty()) return fail(BRIDGER_E_SHAPE, why);
+  if (e != cudaSuccess) return cuda_fail(e, "step_path_scores_sparse");
   return BRIDGER_OK;
 }
 

@@ -61,6 +61,13 @@ Exactness analyze_exactness(const bridger_model_desc* d);
 void path_matrix(int32_t D, int32_t i_pad, int32_t l_pad, int8_t* C, int32_t* Dv);
 inline int32_t gemm_i_pad(int32_t D) { int32_t I = (1 << D) - 1; return ((I + 31) / 32) * 32; }
 inline int32_t gemm_l_pad(int32_t D) { int32_t L = 1 << D; int32_t p = ((L + 15) / 16) * 16; return p < 16 ? 16 : p; }
+// 2:4-sparse form (include/bridger.h bridger_path_matrix_sparse): K position of
+// heap node i, K extent (multiple of the sparse MMA's 64), M extent (leaves,
+// multiple of the MMA's 128 rows)
+inline int32_t sparse_pos(int32_t i) { return i >= 3 ? i + 1 : i; }
+inline int32_t gemm_k_sp(int32_t D) { return ((1 << D) + 63) / 64 * 64; }
+inline int32_t gemm_m_sp(int32_t D) { return ((1 << D) + 127) / 128 * 128; }
+void path_matrix_sparse(int32_t D, int8_t* C);  // [gemm_k_sp(D)][gemm_m_sp(D)]
 
 // ----------------------------------------------- traversal (K4) layout -------
 // A chunk is a contiguous set of trees (same padded depth) resident in one

@@ -50,6 +50,13 @@ struct GemmClassDev {
   int32_t pad_;
   int64_t node_off;   // uint2 [n][i_pad] {feature | missing<<31, threshold} (K5; row I = constant-1 node)
   int64_t cmat2_off;  // int8 C'_D canonical K-major: C_D plus row I = popc(l) (K5, a4 folded in)
+  // 2:4-sparse form (K2s): K regrouped by level (sparse_pos), k_sp = round_up(2^D, 64),
+  // m_sp = round_up(2^D, 128) leaves as the MMA's M (the A operand is C_sp^T)
+  int32_t k_sp, m_sp;
+  int64_t feat_sp_off;  // int32 [n][k_sp]  nodes at sparse_pos(i), dummies elsewhere
+  int64_t thr_sp_off;   // float [n][k_sp]
+  int64_t asp_off;      // int8  [m_sp/128][k_sp/64][2][128][16]  compressed C_sp^T (2 of every 4 K values)
+  int64_t meta_off;     // u32   [m_sp/128][128][k_sp/64][2]     2:4 metadata per leaf row (TMEM layout)
 };
 
 struct GemmHost {
@@ -58,6 +65,7 @@ struct GemmHost {
   std::vector<int32_t> tree_slot;      // original tree -> slot
   std::vector<int32_t> tree_class;     // original tree -> class index
   int64_t max_p_per_row = 0;           // max over classes of n_trees * i_pad
+  int64_t max_psp_per_row = 0;         // ... of n_trees * k_sp (sparse form)
   int32_t max_trees = 0;
   bool has_missing = false;            // any real node with missing_left (K5 ML instantiation)
 };
@@ -331,6 +339,210 @@ __global__ void __launch_bounds__(kPcThreads, 1) pc_kernel(const PcParams p) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols) : "memory");
 }
 
+// ----------------------------------------------------------------- K2s -----
+// 2:4-sparse path contraction ("sparse operator replacing", PAPER.md:502,
+// Table 2).  The transposed product
+//     S^T[l][r] = sum_k C_sp^T[l][k] P[r][k]
+// puts the constant path matrix on the SPARSE operand: A = C_sp^T (M = leaves,
+// K = internal nodes regrouped by level so every group of 4 consecutive K
+// positions holds <= 2 ancestors of a leaf, bridger_path_matrix_sparse),
+// stored compressed (2 of every 4 K values, 32 B per row per 64-K step) in
+// shared memory once per CTA, its 2:4 metadata written once into TMEM (lane =
+// leaf, 2 columns per 64-K step; nibble g = positions p0 | p1 << 2 of group g,
+// pinned on B200 by tools/sparse_probe.cu); B = the decision tile P (N = 128
+// rows, K-major canonical, the same tiles K1 writes).  tcgen05.mma.sp
+// .cta_group::1.kind::i8 (M = 128, N = 128, K = 64): half the MACs of the
+// dense K2 per logical product.  Warp roles as in pc_kernel:
+//   warps 0-15 epilogue: thread = leaf (TMEM lane), a quarter of the tile's 128
+//              row columns: tcgen05.ld 2 x 16 columns, a4 (S == D_D[leaf]) ->
+//              this leaf is that row's leaf (unique), store it
+//   warp 16    producer: compressed A + metadata once, then decision tiles
+//   warp 17    MMA issuer: per (tile, M-tile) item k_sp/64 sparse MMAs into
+//              one of kSpSlots 128-column TMEM accumulators
+constexpr int kSpSlots = 3;
+struct PcsParams {
+  const int8_t* P;       // tiled decisions [n_trees][n_rt][k_sp/16][128][16]
+  const uint8_t* gbase;
+  GemmClassDev cls;
+  int32_t n_trees, n_rt, rows;
+  int32_t stages;        // B (decision tile) ring depth
+  int32_t mode;          // 0: int16 leaf index, 1: int32 S rows [n_trees][rows][l_pad]
+  int16_t* leaf;
+  int32_t* S;
+};
+
+__device__ __forceinline__ void mma_sp_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t tmem_e,
+                                          uint32_t idesc, uint32_t acc) {
+  const uint32_t z = 0u;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.sp.cta_group::1.kind::i8 [%0], %1, %2, [%3], %5, {%6, %6, %6, %6}, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(tmem_e), "r"(acc), "r"(idesc), "r"(z)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kPcThreads, 1) pcs_kernel(const PcsParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int D = p.cls.depth, L = 1 << D, lp = p.cls.l_pad;
+  const int ks_n = p.cls.k_sp / 64, mt_n = p.cls.m_sp / 128;
+  const int NS = p.stages;
+  const uint32_t a_bytes = (uint32_t)mt_n * ks_n * 4096u;  // compressed C_sp^T
+  const uint32_t b_bytes = 128u * (uint32_t)p.cls.k_sp;    // one decision tile
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + ((a_bytes + 1023) / 1024) * 1024;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + (size_t)NS * b_bytes);
+  uint64_t* afull = bars;                      // [1]
+  uint64_t* bfull = bars + 1;                  // [NS]
+  uint64_t* bempty = bars + 1 + NS;            // [NS]
+  uint64_t* tfull = bars + 1 + 2 * NS;         // [kSpSlots]
+  uint64_t* tempty = tfull + kSpSlots;         // [kSpSlots]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + kSpSlots);
+  constexpr uint32_t kMetaCol = kSpSlots * 128;  // metadata after the accumulator slots
+
+  if (tid == 0) {
+    ptx::mbar_init(afull, 1);
+    for (int i = 0; i < NS; ++i) {
+      ptx::mbar_init(&bfull[i], 1);
+      ptx::mbar_init(&bempty[i], 1);
+    }
+    for (int i = 0; i < kSpSlots; ++i) {
+      ptx::mbar_init(&tfull[i], 1);
+      ptx::mbar_init(&tempty[i], kPcEpiWarps * 32);
+    }
+    ptx::fence_barrier_init();
+    ptx::fence_proxy_async();
+  }
+  if (warp == kPcEpiWarps) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(ptx::s2u(tmem_holder))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = *tmem_holder;
+  // 2:4 metadata of every (M-tile, K-step) into TMEM: warp quadrant q writes lanes 32q..32q+31
+  if (warp < 4) {
+    const uint32_t* meta = reinterpret_cast<const uint32_t*>(p.gbase + p.cls.meta_off);
+    for (int mt = 0; mt < mt_n; ++mt)
+      for (int ks = 0; ks < ks_n; ++ks) {
+        const int r = warp * 32 + lane;
+        const uint32_t w0 = meta[((size_t)(mt * 128 + r) * ks_n + ks) * 2 + 0];
+        const uint32_t w1 = meta[((size_t)(mt * 128 + r) * ks_n + ks) * 2 + 1];
+        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + kMetaCol + (uint32_t)(mt * ks_n + ks) * 4u;
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "r"(w0), "r"(w1)
+                     : "memory");
+      }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const int n_tiles = p.n_trees * p.n_rt;
+  const int grid = gridDim.x;
+
+  if (warp == kPcEpiWarps) {
+    if (lane == 0) {
+      ptx::mbar_arrive_expect_tx(afull, a_bytes);
+      for (uint32_t o = 0; o < a_bytes; o += 32768u)
+        ptx::bulk_g2s(sA + o, p.gbase + p.cls.asp_off + o, min(32768u, a_bytes - o), afull);
+      int k = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += grid, ++k) {
+        const int s = k % NS;
+        ptx::mbar_wait(&bempty[s], ((k / NS) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&bfull[s], b_bytes);
+        ptx::bulk_g2s(sB + (size_t)s * b_bytes, p.P + (size_t)tile * b_bytes, b_bytes, &bfull[s]);
+      }
+    }
+  } else if (warp == kPcEpiWarps + 1) {
+    if (lane == 0) {
+      ptx::mbar_wait(afull, 0);
+      // idesc: sparse (bit 2), D s32, A s8, B s8, K-major both, N = 128, M = 128
+      const uint32_t idesc = (1u << 2) | (2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+      const uint32_t sA_u = ptx::s2u(sA), sB_u = ptx::s2u(sB);
+      int k = 0, item = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += grid, ++k) {
+        const int s = k % NS;
+        ptx::mbar_wait(&bfull[s], (k / NS) & 1);
+        const uint32_t b0 = sB_u + (uint32_t)s * b_bytes;
+        for (int mt = 0; mt < mt_n; ++mt, ++item) {
+          const int slot = item % kSpSlots;
+          ptx::mbar_wait(&tempty[slot], ((item / kSpSlots) & 1) ^ 1);  // epilogue drained the slot
+          umma::fence_after();
+          for (int ks = 0; ks < ks_n; ++ks) {
+            const uint64_t ad = umma::smem_desc(sA_u + (uint32_t)(mt * ks_n + ks) * 4096u, 2048u, 128u);
+            const uint64_t bd = umma::smem_desc(b0 + (uint32_t)ks * 4u * 2048u, 2048u, 128u);
+            mma_sp_i8(tmem + (uint32_t)slot * 128u, ad, bd, tmem + kMetaCol + (uint32_t)(mt * ks_n + ks) * 4u, idesc,
+                      ks > 0 ? 1u : 0u);
+          }
+          umma::commit(&tfull[slot]);
+        }
+        umma::commit(&bempty[s]);  // decision tile free once every M-tile's MMAs have read it
+      }
+    }
+  } else {
+    // epilogue: thread = leaf (TMEM lane) of the M-tile, 32 of the tile's 128 row columns
+    const int quad = warp & 3, part = warp >> 2;
+    const int32_t* dv = reinterpret_cast<const int32_t*>(p.gbase + p.cls.dv_off);
+    int32_t want_mt[2];  // D_D of this thread's leaf in each M-tile (padding leaves never match)
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int l = mt * 128 + quad * 32 + lane;
+      want_mt[mt] = (mt < mt_n && l < L) ? dv[l] : 0x7fffffff;
+    }
+    int item = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += grid) {
+      const int t = tile / p.n_rt, rt = tile % p.n_rt;
+      for (int mt = 0; mt < mt_n; ++mt, ++item) {
+        const int slot = item % kSpSlots;
+        ptx::mbar_wait(&tfull[slot], (item / kSpSlots) & 1);
+        umma::fence_after();
+        const int l = mt * 128 + quad * 32 + lane;
+        const int32_t want = mt ? want_mt[1] : want_mt[0];
+        const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)slot * 128u + (uint32_t)(part * 32);
+        uint32_t v[32];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(tbase));
+        umma::wait_ld();
+        umma::fence_before();
+        ptx::mbar_arrive(&tempty[slot]);
+        const int row0 = rt * 128 + part * 32;
+        if (p.mode == 0) {
+          // a4: S <= D_D[l] with equality iff the row reaches leaf l, so with
+          // w1 = D_D - 1, max(S, w1) = w1 + hit bit and (mod 2^32)
+          //   sum_j max(S_j, w1) << j = hit - w1
+          // -- two instructions per value (VIMNMX + IMAD); a few of the 32
+          // rows reach this leaf: store those
+          const int32_t w1 = want - 1;
+          uint32_t hit = (uint32_t)w1;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) hit += (uint32_t)max((int32_t)v[j], w1) << j;
+          while (hit) {
+            const int j = __ffs(hit) - 1;
+            hit &= hit - 1;
+            if (row0 + j < p.rows) p.leaf[(size_t)t * p.rows + row0 + j] = (int16_t)l;
+          }
+        } else if (l < lp) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (row0 + j < p.rows) p.S[((size_t)t * p.rows + row0 + j) * lp + l] = (int32_t)v[j];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  umma::fence_after();
+  if (warp == kPcEpiWarps)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
 // ------------------------------------------------------------------ K3 -----
 template <int KT, typename ACC>
 __global__ void __launch_bounds__(256) lg_kernel(const int16_t* __restrict__ leaf, int32_t rows, int32_t n_trees,
@@ -342,6 +554,7 @@ __global__ void __launch_bounds__(256) lg_kernel(const int16_t* __restrict__ lea
   ACC acc[KT];
 #pragma unroll
   for (int k = 0; k < KT; ++k) acc[k] = (first || k >= K) ? ACC(0) : accbuf[(size_t)r * K + k];
+#pragma unroll 4
   for (int t = 0; t < n_trees; ++t) {
     const int l = leaf[(size_t)t * rows + r];
     const float* e = E + ((size_t)t * L + l) * K;
@@ -805,6 +1018,74 @@ bool gemm_build(bridger_model* m, const bridger_model_desc* d, const std::vector
       float* lv = reinterpret_cast<float*>(buf.data() + c.leaf_off) + (size_t)j * L * K;
       for (int32_t l = 0; l < L * K; ++l) lv[l] = m->acc_int ? std::ldexp(pt.leaf_value[l], -m->ex.q) : pt.leaf_value[l];
     }
+    // ---- 2:4-sparse form: regrouped node arrays, compressed C_sp^T + metadata
+    c.k_sp = gemm_k_sp(D);
+    c.m_sp = gemm_m_sp(D);
+    {
+      const int32_t ks_n = c.k_sp / 64, mt_n = c.m_sp / 128;
+      std::vector<int8_t> Csp((size_t)c.k_sp * c.m_sp);
+      path_matrix_sparse(D, Csp.data());
+      align(1024);
+      c.asp_off = (int64_t)buf.size();
+      buf.resize(buf.size() + (size_t)mt_n * ks_n * 4096, 0);
+      align(16);
+      c.meta_off = (int64_t)buf.size();
+      buf.resize(buf.size() + (size_t)mt_n * 128 * ks_n * 2 * 4, 0);
+      int8_t* asp = reinterpret_cast<int8_t*>(buf.data() + c.asp_off);
+      uint32_t* meta = reinterpret_cast<uint32_t*>(buf.data() + c.meta_off);
+      for (int32_t mt = 0; mt < mt_n; ++mt)
+        for (int32_t r = 0; r < 128; ++r)
+          for (int32_t ks = 0; ks < ks_n; ++ks) {
+            const int32_t l = mt * 128 + r;
+            uint32_t w[2] = {0u, 0u};
+            for (int32_t g = 0; g < 16; ++g) {
+              const int32_t k0 = ks * 64 + 4 * g;
+              int8_t v[4];
+              int32_t nz[4], nnz = 0;
+              for (int32_t q = 0; q < 4; ++q) {
+                v[q] = Csp[(size_t)(k0 + q) * c.m_sp + l];
+                if (v[q]) nz[nnz++] = q;
+              }
+              if (nnz > 2) {
+                delete h;
+                if (why) *why = "internal: path matrix not 2:4 structured";
+                return false;
+              }
+              // two kept positions p0 < p1 (the non-zeros, padded with zeros)
+              int32_t p0 = 0, p1 = 1;
+              if (nnz == 2) { p0 = nz[0]; p1 = nz[1]; }
+              else if (nnz == 1) { p0 = nz[0] < 3 ? nz[0] : 2; p1 = p0 + 1; }
+              const int32_t j = 2 * g;  // compressed index within the K-step (0..31)
+              int8_t* a = asp + (size_t)(mt * ks_n + ks) * 4096;
+              a[(j >> 4) * 2048 + r * 16 + (j & 15)] = v[p0];
+              a[((j + 1) >> 4) * 2048 + r * 16 + ((j + 1) & 15)] = v[p1];
+              w[g >> 3] |= (uint32_t)(p0 | (p1 << 2)) << (4 * (g & 7));
+            }
+            meta[((size_t)(mt * 128 + r) * ks_n + ks) * 2 + 0] = w[0];
+            meta[((size_t)(mt * 128 + r) * ks_n + ks) * 2 + 1] = w[1];
+          }
+      align(16);
+      c.feat_sp_off = (int64_t)buf.size();
+      buf.resize(buf.size() + 4 * (size_t)n * c.k_sp, 0);
+      align(16);
+      c.thr_sp_off = (int64_t)buf.size();
+      buf.resize(buf.size() + 4 * (size_t)n * c.k_sp, 0);
+      const int32_t* fe_all = reinterpret_cast<const int32_t*>(buf.data() + c.feat_off);
+      const float* th_all = reinterpret_cast<const float*>(buf.data() + c.thr_off);
+      for (int32_t j = 0; j < n; ++j) {
+        int32_t* fe = reinterpret_cast<int32_t*>(buf.data() + c.feat_sp_off) + (size_t)j * c.k_sp;
+        float* th = reinterpret_cast<float*>(buf.data() + c.thr_sp_off) + (size_t)j * c.k_sp;
+        for (int32_t k = 0; k < c.k_sp; ++k) {
+          fe[k] = 0;
+          th[k] = std::numeric_limits<float>::quiet_NaN();  // dummy: decision 0 (C_sp is zero there anyway)
+        }
+        for (int32_t i = 0; i < I; ++i) {
+          fe[sparse_pos(i)] = fe_all[(size_t)j * c.i_pad + i];
+          th[sparse_pos(i)] = th_all[(size_t)j * c.i_pad + i];
+        }
+      }
+    }
+    h->max_psp_per_row = std::max<int64_t>(h->max_psp_per_row, (int64_t)n * c.k_sp);
     h->max_p_per_row = std::max<int64_t>(h->max_p_per_row, (int64_t)n * c.i_pad);
     h->max_trees = std::max(h->max_trees, n);
     h->classes.push_back(c);
@@ -896,18 +1177,55 @@ static cudaError_t launch_pc(const int8_t* P, const uint8_t* gbase, const GemmCl
   return cudaGetLastError();
 }
 
-cudaError_t gemm_run(const bridger_model* m, const float* X, int64_t n_rows, void* out, int want, int32_t total_trees,
-                     cudaStream_t st) {
+static cudaError_t launch_pcs(const int8_t* P, const uint8_t* gbase, const GemmClassDev& c, int32_t n_trees,
+                              int32_t rows, int mode, int16_t* leaf, int32_t* S, int dev, cudaStream_t st) {
+  PcsParams p{};
+  p.P = P;
+  p.gbase = gbase;
+  p.cls = c;
+  p.n_trees = n_trees;
+  p.n_rt = (rows + 127) / 128;
+  p.rows = rows;
+  p.mode = mode;
+  p.leaf = leaf;
+  p.S = S;
+  const int a_al = ((c.m_sp / 128) * (c.k_sp / 64) * 4096 + 1023) / 1024 * 1024;
+  const int b_bytes = 128 * c.k_sp;
+  const int bar_bytes = (1 + 2 * 8 + 2 * kSpSlots) * 8 + 16;
+  int stages = 6;
+  while (stages > 2 && a_al + stages * b_bytes + bar_bytes > kSmemMax) --stages;
+  p.stages = stages;
+  // one CTA per SM: the kernel allocates all 512 TMEM columns
+  const int smem = std::max(a_al + stages * b_bytes + bar_bytes, kSmemMax / 2 + 1024);
+  static std::atomic<uint64_t> configured{0};
+  cudaError_t e = smem_opt_in(reinterpret_cast<const void*>(pcs_kernel), configured);
+  if (e != cudaSuccess) return e;
+  const int n_tiles = n_trees * p.n_rt;
+  const int grid = std::max(1, std::min(n_tiles, dev_sms(dev)));
+  cudaEvent_t ev;
+  hot_begin(st, &ev);
+  pcs_kernel<<<grid, kPcThreads, smem, st>>>(p);
+  hot_end(st, ev);
+  count_launch();
+  return cudaGetLastError();
+}
+
+static cudaError_t gemm_run_impl(const bridger_model* m, const float* X, int64_t n_rows, void* out, int want,
+                                 int32_t total_trees, cudaStream_t st, bool sparse) {
   const GemmHost* h = static_cast<const GemmHost*>(m->gemm_host);
   const uint8_t* gbase = static_cast<const uint8_t*>(m->d_gemm);
-  // row blocks: decision scratch <= 256 MB
-  int64_t rb = ((int64_t)256 << 20) / std::max<int64_t>(1, h->max_p_per_row);
+  // row blocks: decision scratch <= 1 GB (large blocks keep every kernel's grid
+  // full); BRIDGER_GEMM_SCRATCH_MB sets it (e.g. L2-resident blocks)
+  const int64_t per_row = sparse ? h->max_psp_per_row : h->max_p_per_row;
+  int64_t scratch = (int64_t)1 << 30;
+  if (const char* ev = std::getenv("BRIDGER_GEMM_SCRATCH_MB")) scratch = (int64_t)std::max(1, std::atoi(ev)) << 20;
+  int64_t rb = scratch / std::max<int64_t>(1, per_row);
   rb = std::max<int64_t>(128, rb / 128 * 128);
   rb = std::min<int64_t>(rb, (n_rows + 127) / 128 * 128);
   int8_t* P = nullptr;
   int16_t* leaf = nullptr;
   void* accbuf = nullptr;
-  cudaError_t e = cudaMallocAsync(&P, (size_t)rb * h->max_p_per_row, st);
+  cudaError_t e = cudaMallocAsync(&P, (size_t)rb * per_row, st);
   if (e == cudaSuccess) e = cudaMallocAsync(&leaf, (size_t)rb * h->max_trees * 2, st);
   if (e == cudaSuccess) e = cudaMallocAsync(&accbuf, (size_t)rb * m->K * 8, st);
   FinalizeArgs fin{};
@@ -927,8 +1245,18 @@ cudaError_t gemm_run(const bridger_model* m, const float* X, int64_t n_rows, voi
     const int32_t rows = (int32_t)std::min<int64_t>(rb, n_rows - r0);
     for (int ci = 0; ci < nc && e == cudaSuccess; ++ci) {
       const GemmClassDev& c = h->classes[ci];
-      e = launch_gc(X, r0, rows, m->F, gbase, c, 0, c.n_trees, P, false, st);
-      if (e == cudaSuccess) e = launch_pc(P, gbase, c, c.n_trees, rows, 0, leaf, nullptr, m->device, st);
+      if (sparse) {
+        // K1 on the level-regrouped node arrays (K = k_sp), then the 2:4-sparse K2s
+        GemmClassDev csp = c;
+        csp.i_pad = c.k_sp;
+        csp.feat_off = c.feat_sp_off;
+        csp.thr_off = c.thr_sp_off;
+        e = launch_gc(X, r0, rows, m->F, gbase, csp, 0, c.n_trees, P, false, st);
+        if (e == cudaSuccess) e = launch_pcs(P, gbase, c, c.n_trees, rows, 0, leaf, nullptr, m->device, st);
+      } else {
+        e = launch_gc(X, r0, rows, m->F, gbase, c, 0, c.n_trees, P, false, st);
+        if (e == cudaSuccess) e = launch_pc(P, gbase, c, c.n_trees, rows, 0, leaf, nullptr, m->device, st);
+      }
       if (e != cudaSuccess) break;
       const int tb = 256, g = (rows + tb - 1) / tb;
       const float* E = reinterpret_cast<const float*>(gbase + c.leaf_off);
@@ -951,6 +1279,16 @@ cudaError_t gemm_run(const bridger_model* m, const float* X, int64_t n_rows, voi
   cudaFreeAsync(leaf, st);
   cudaFreeAsync(accbuf, st);
   return e;
+}
+
+cudaError_t gemm_run(const bridger_model* m, const float* X, int64_t n_rows, void* out, int want, int32_t total_trees,
+                     cudaStream_t st) {
+  return gemm_run_impl(m, X, n_rows, out, want, total_trees, st, false);
+}
+
+cudaError_t gemm_run_sparse(const bridger_model* m, const float* X, int64_t n_rows, void* out, int want,
+                            int32_t total_trees, cudaStream_t st) {
+  return gemm_run_impl(m, X, n_rows, out, want, total_trees, st, true);
 }
 
 // Shared-memory carve-up of K5: C'_D | X tile | A ring | node ring | partials | barriers.
@@ -1103,6 +1441,33 @@ cudaError_t gemm_step_scores(const bridger_model* m, int32_t depth, const int8_t
   e = cudaGetLastError();
   if (e == cudaSuccess)
     e = launch_pc(tiled, static_cast<const uint8_t*>(m->d_gemm), *c, 1, (int32_t)rows, 1, nullptr, out, m->device, st);
+  cudaFreeAsync(tiled, st);
+  return e;
+}
+
+cudaError_t gemm_step_scores_sparse(const bridger_model* m, int32_t depth, const int8_t* P, int64_t rows, int32_t* out,
+                                    cudaStream_t st, std::string* why) {
+  const GemmHost* h = static_cast<const GemmHost*>(m->gemm_host);
+  const GemmClassDev* c = nullptr;
+  for (auto& cc : h->classes)
+    if (cc.depth == depth) c = &cc;
+  if (!c) {
+    *why = "model has no trees of that depth";
+    return cudaErrorInvalidValue;
+  }
+  if (rows > INT32_MAX) {
+    *why = "too many rows";
+    return cudaErrorInvalidValue;
+  }
+  const int64_t n_rt = (rows + 127) / 128;
+  int8_t* tiled = nullptr;
+  cudaError_t e = cudaMallocAsync(&tiled, (size_t)n_rt * 128 * c->k_sp, st);
+  if (e != cudaSuccess) return e;
+  tile_kernel<<<256, 256, 0, st>>>(P, rows, c->k_sp, tiled);
+  count_launch();
+  e = cudaGetLastError();
+  if (e == cudaSuccess)
+    e = launch_pcs(tiled, static_cast<const uint8_t*>(m->d_gemm), *c, 1, (int32_t)rows, 1, nullptr, out, m->device, st);
   cudaFreeAsync(tiled, st);
   return e;
 }

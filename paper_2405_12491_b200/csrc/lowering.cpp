@@ -225,6 +225,16 @@ void path_matrix(int32_t D, int32_t i_pad, int32_t l_pad, int8_t* C, int32_t* Dv
   }
 }
 
+// 2:4-sparse regrouping of C_D's K dimension (bridger.h bridger_path_matrix_sparse)
+void path_matrix_sparse(int32_t D, int8_t* C) {
+  const int32_t I = (1 << D) - 1, ks = gemm_k_sp(D), ms = gemm_m_sp(D);
+  std::vector<int8_t> dense((size_t)std::max(I, 1) * ms);
+  path_matrix(D, std::max(I, 1), ms, dense.data(), nullptr);
+  std::memset(C, 0, (size_t)ks * ms);
+  for (int32_t i = 0; i < I; ++i)
+    std::memcpy(C + (size_t)sparse_pos(i) * ms, dense.data() + (size_t)i * ms, (size_t)ms);
+}
+
 // ------------------------------------------------------ traversal layout ----
 static constexpr int32_t kSmemMax = 232448;  // 227 KB opt-in per block (sm_100)
 

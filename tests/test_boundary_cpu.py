@@ -207,3 +207,42 @@ def test_no_device_is_a_cuda_error():
     with pytest.raises(B.BridgerError) as ei:
         B.Model(m, device=0)
     assert ei.value.status == B.E_CUDA
+
+
+def test_variant_table_header_matches_measurement():
+    """AUTO's per-depth table (csrc/variant_table.h) is the one generated from
+    the committed measurement profiles/variant_table.json (best variant per
+    depth of a 1M-row x 100-tree forest on B200)."""
+    import json
+    import os
+    import re
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    d = json.load(open(os.path.join(root, "profiles", "variant_table.json")))
+    hdr = open(os.path.join(root, "paper_2405_12491_b200", "csrc", "variant_table.h")).read()
+    vals = [int(v) for v in re.search(r"kVariantByDepth\[16\] = \{([^}]*)\}", hdr).group(1).split(",")]
+    code = {"traverse": 1, "gemm": 2, "gemm_staged": 3}
+    for r in d["rows"]:
+        assert vals[r["depth"]] == code[r["best"]]
+        ms = {k: r[k + "_ms"] for k in code if k + "_ms" in r}
+        assert r["best"] == min(ms, key=ms.get)
+
+
+def test_sparse_path_matrix_regrouping_is_2_4_structured():
+    """bridger_path_matrix_sparse: the dense C_D (pinned by exhaustive
+    enumeration above) with heap node i moved to K position i + [i >= 3]; every
+    group of 4 consecutive K positions holds <= 2 non-zeros of any leaf column
+    (2:4 structured sparsity, the operand form of tcgen05.mma.sp), zero rows
+    at the pads, and every leaf keeps exactly its D ancestors."""
+    for D in range(1, 9):
+        Cs = B.path_matrix_sparse(D)
+        Cd, _ = B.path_matrix(D)
+        I, L = (1 << D) - 1, 1 << D
+        assert Cs.shape == ((((1 << D) + 63) // 64) * 64, (((1 << D) + 127) // 128) * 128)
+        pos = [i + (1 if i >= 3 else 0) for i in range(I)]
+        np.testing.assert_array_equal(Cs[pos, :L], Cd[:I, :L])
+        mask = np.ones(Cs.shape[0], bool)
+        mask[pos] = False
+        assert not Cs[mask].any() and not Cs[:, L:].any()
+        nz = (Cs != 0).reshape(Cs.shape[0] // 4, 4, Cs.shape[1]).sum(axis=1)
+        assert nz.max() <= 2
+        assert ((Cs != 0).sum(axis=0)[:L] == D).all()

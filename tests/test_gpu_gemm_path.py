@@ -68,7 +68,25 @@ def test_k2_path_contraction_is_int_matmul(D):
     np.testing.assert_array_equal(S, ref)
 
 
-@pytest.mark.parametrize("variant", ["gemm", "gemm_staged"])
+@pytest.mark.parametrize("D", [3, 6, 7, 8])
+def test_k2_sparse_path_contraction_is_int_matmul(D):
+    """K2s (tcgen05.mma.sp kind::i8, 2:4-sparse C_sp^T as operand A) equals a
+    CPU int32 matmul with the regrouped path matrix, bitwise, on random 0/1
+    decisions in the sparse K order (pad positions random too: C_sp is zero
+    there), 7 full 128-row tiles + a ragged tail."""
+    m = perfect_ensemble(23, 4, D, 5, kind="regression")
+    g = B.Model(m)
+    _, lp = B.gemm_geometry(D)
+    Csp = B.path_matrix_sparse(D)
+    rows = 1000
+    rng = np.random.default_rng(100 + D)
+    P = (rng.random((rows, Csp.shape[0])) < 0.5).astype(np.int8)
+    S = g.step_path_scores_sparse(D, dev(P)).cpu().numpy()
+    ref = P.astype(np.int32) @ Csp[:, :lp].astype(np.int32)
+    np.testing.assert_array_equal(S, ref)
+
+
+@pytest.mark.parametrize("variant", ["gemm", "gemm_staged", "gemm_sparse"])
 @pytest.mark.parametrize("name,rows", [("C1", None), ("C2", 9001), ("C3", 5001)])
 def test_gemm_variant_end_to_end(name, rows, variant):
     c, m = make_config(name, n_trees=None if name != "C3" else 120)
@@ -81,7 +99,7 @@ def test_gemm_variant_end_to_end(name, rows, variant):
     assert g.info()["variant"] == variant
 
 
-@pytest.mark.parametrize("variant", ["gemm", "gemm_staged"])
+@pytest.mark.parametrize("variant", ["gemm", "gemm_staged", "gemm_sparse"])
 def test_gemm_variant_pruned_missing_mixed_depth(variant):
     m = perfect_ensemble(25, 40, 7, 13, kind="classification", n_classes=4, calib_rows=1024)
     m = prune_ensemble(m, 25, p=0.2, with_missing=True)
@@ -95,6 +113,22 @@ def test_fused_every_depth(D):
     m = perfect_ensemble(40 + D, 9, D, 11, kind="classification", n_classes=3, calib_rows=512)
     X = inject_specials(gen_x(60 + D, 0, 777, 11), 60 + D, rate=0.01)
     check(m, X, variant="gemm", apply=False)
+
+
+@pytest.mark.parametrize("D", [1, 2, 4, 5, 7, 8])
+def test_sparse_variant_every_depth(D):
+    # every K2s geometry (k_sp 64..256, one or two 128-leaf M-tiles), ragged last tile
+    m = perfect_ensemble(80 + D, 7, D, 11, kind="classification", n_classes=3, calib_rows=512)
+    X = inject_specials(gen_x(90 + D, 0, 1777, 11), 90 + D, rate=0.01)
+    check(m, X, variant="gemm_sparse", apply=False)
+
+
+def test_sparse_matches_dense_staged_bitwise():
+    c, m = make_config("C2")
+    X = dev(gen_x(2, 0, 30000, 28))
+    a = B.Model(m, variant="gemm_sparse").predict_raw(X).cpu().numpy()
+    b = B.Model(m, variant="gemm_staged").predict_raw(X).cpu().numpy()
+    np.testing.assert_array_equal(a, b)
 
 
 def test_fused_many_tiles_per_cta_regression():

@@ -204,6 +204,10 @@ __global__ void __launch_bounds__(512, 1) trav_deep_kernel(const TravParams p) {
       const int sz = sz0 + (q < nbig ? 1 : 0);
       if (spec)
         walk_spec_tail<KT, ML, SPEC_NI>(sz, p, nodes_s, leaves_s, ptx::s2u(xl), j, I, L, D, acc);
+      else if (!ML && KT <= 8 && D == 6)
+        walk_tail<KT, long long, ML, true, NI_MAX, false, 6>(sz, p, c, smem, leaves, xl, j, I, L, D, K, row, acc);
+      else if (!ML && KT <= 8 && D == 8)
+        walk_tail<KT, long long, ML, true, NI_MAX, false, 8>(sz, p, c, smem, leaves, xl, j, I, L, D, K, row, acc);
       else
         walk_tail<KT, long long, ML, true, NI_MAX>(sz, p, c, smem, leaves, xl, j, I, L, D, K, row, acc);
       j += sz;

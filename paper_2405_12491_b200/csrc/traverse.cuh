@@ -104,7 +104,10 @@ __device__ __forceinline__ int go_right(float x, uint2 nd) {
 
 // Walk NI trees [j, j+NI) of the chunk for this thread's row (NI independent
 // dependency chains for ILP), then gather and accumulate their leaf values.
-template <int NI, int KT, typename ACC, bool ML, bool CODES, bool SPLIT = false>
+// DT > 0: the depth is a compile-time constant (coded walks of the common
+// depths: the level loop unrolls fully -- no loop counter / branch / register
+// shuffling per level); DT == 0: runtime depth D.
+template <int NI, int KT, typename ACC, bool ML, bool CODES, bool SPLIT = false, int DT = 0>
 __device__ __forceinline__ void walk_trees(const TravParams& p, const TravChunk& c, const void* nodes,
                                            const float* leaves, const void* xl, int j, int I, int L, int D,
                                            int K, int64_t row, ACC (&acc)[KT]) {
@@ -159,7 +162,9 @@ __device__ __forceinline__ void walk_trees(const TravParams& p, const TravChunk&
       A[u] = nb + 4u * (uint32_t)(u * (I + 1));  // shared address of tree u's current node
       cb[u] = 4u - A[u];
     }
-    for (int lvl = 0; lvl < D; ++lvl) {
+    const int DD = DT > 0 ? DT : D;
+#pragma unroll (DT > 0 ? DT : 1)
+    for (int lvl = 0; lvl < DD; ++lvl) {
       uint32_t a[NI];
 #pragma unroll
       for (int u = 0; u < NI; ++u) a[u] = ptx::lds_u32(A[u]);
@@ -258,13 +263,13 @@ __device__ __forceinline__ void walk_trees(const TravParams& p, const TravChunk&
 }
 
 // one pass over r (<= 12) trees with ILP = r
-template <int KT, typename ACC, bool ML, bool CODES, int MAXNI, bool SPLIT = false>
+template <int KT, typename ACC, bool ML, bool CODES, int MAXNI, bool SPLIT = false, int DT = 0>
 __device__ __forceinline__ void walk_tail(int r, const TravParams& p, const TravChunk& c, const void* nodes,
                                           const float* leaves, const void* xl, int j, int I, int L, int D, int K,
                                           int64_t row, ACC (&acc)[KT]) {
   switch (r) {
 #define BRIDGER_TAIL(N) \
-  case N: if (N <= MAXNI) walk_trees<(N <= MAXNI ? N : 1), KT, ACC, ML, CODES, SPLIT>(p, c, nodes, leaves, xl, j, I, L, D, K, row, acc); break;
+  case N: if (N <= MAXNI) walk_trees<(N <= MAXNI ? N : 1), KT, ACC, ML, CODES, SPLIT, DT>(p, c, nodes, leaves, xl, j, I, L, D, K, row, acc); break;
     BRIDGER_TAIL(1) BRIDGER_TAIL(2) BRIDGER_TAIL(3) BRIDGER_TAIL(4) BRIDGER_TAIL(5) BRIDGER_TAIL(6)
     BRIDGER_TAIL(7) BRIDGER_TAIL(8) BRIDGER_TAIL(9) BRIDGER_TAIL(10) BRIDGER_TAIL(11) BRIDGER_TAIL(12)
 #undef BRIDGER_TAIL
@@ -594,7 +599,13 @@ __global__ void __launch_bounds__(512, 1) trav_kernel(const TravParams p) {
       int j = t0;
       for (int q = 0; q < n_pass; ++q) {
         const int sz = nt / n_pass + (q < nt % n_pass ? 1 : 0);
-        walk_tail<KT, ACC, ML, CODES, NI_MAX, FMT == FMT_SPLIT>(sz, p, cc, nodes, leaves, xptr, j, I, L, D, K, row, acc);
+        constexpr bool kFixedD = CODES && !ML && KT <= 8 && std::is_same<ACC, long long>::value;
+        if (kFixedD && D == 8)
+          walk_tail<KT, ACC, ML, CODES, NI_MAX, false, 8>(sz, p, cc, nodes, leaves, xptr, j, I, L, D, K, row, acc);
+        else if (kFixedD && D == 6)
+          walk_tail<KT, ACC, ML, CODES, NI_MAX, false, 6>(sz, p, cc, nodes, leaves, xptr, j, I, L, D, K, row, acc);
+        else
+          walk_tail<KT, ACC, ML, CODES, NI_MAX, FMT == FMT_SPLIT>(sz, p, cc, nodes, leaves, xptr, j, I, L, D, K, row, acc);
         j += sz;
       }
     };

@@ -220,7 +220,7 @@ def test_variant_table_header_matches_measurement():
     d = json.load(open(os.path.join(root, "profiles", "variant_table.json")))
     hdr = open(os.path.join(root, "paper_2405_12491_b200", "csrc", "variant_table.h")).read()
     vals = [int(v) for v in re.search(r"kVariantByDepth\[16\] = \{([^}]*)\}", hdr).group(1).split(",")]
-    code = {"traverse": 1, "gemm": 2, "gemm_staged": 3}
+    code = {"traverse": 1, "gemm": 2, "gemm_staged": 3, "gemm_sparse": 4}
     for r in d["rows"]:
         assert vals[r["depth"]] == code[r["best"]]
         ms = {k: r[k + "_ms"] for k in code if k + "_ms" in r}

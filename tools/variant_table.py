@@ -29,7 +29,7 @@ rows = []
 for D in range(1, 13):
     m = perfect_ensemble(100 + D, T, D, F, kind="classification", n_classes=2, calib_rows=2048)
     rec = {"depth": D, "n_trees": T, "rows": N, "features": F}
-    for v in ("traverse", "gemm", "gemm_staged"):
+    for v in ("traverse", "gemm", "gemm_staged", "gemm_sparse"):
         if v != "traverse" and D > 8:
             continue
         g = B.Model(m, device=0, variant=v)

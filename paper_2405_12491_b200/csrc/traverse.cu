@@ -224,6 +224,20 @@ __global__ void __launch_bounds__(512, 1) bin_coop_kernel(const float* __restric
   };
   issue(blockIdx.x, 0);
   issue((int64_t)blockIdx.x + gridDim.x, 1);
+  // this warp's pairs when one pass covers them all (F2h <= NP * NW): block-
+  // independent chain constants hoisted out of the block loop
+  const bool single = F2h <= NP * NW;
+  const int npairs = warp < F2h ? min(NP, (F2h - 1 - warp) / NW + 1) : 0;
+  uint32_t xoff[2 * NP], A0[2 * NP], c4[2 * NP], hi_mask[NP];
+#pragma unroll
+  for (int u = 0; u < 2 * NP; ++u) {
+    const int f = min(2 * (warp + (u >> 1) * NW) + (u & 1), F - 1);
+    xoff[u] = 4u * (uint32_t)f;
+    A0[u] = tab_s + (uint32_t)(f * P) * 4u;
+    c4[u] = 4u - A0[u];
+  }
+#pragma unroll
+  for (int q = 0; q < NP; ++q) hi_mask[q] = 2 * (warp + q * NW) + 1 >= F ? 0u : 0xFFFFFFFFu;
   int it = 0;
   for (int64_t blk = blockIdx.x; blk < n_blocks; blk += gridDim.x, ++it) {
     const int buf = it & 1;
@@ -240,18 +254,17 @@ __global__ void __launch_bounds__(512, 1) bin_coop_kernel(const float* __restric
       for (int e = threadIdx.x; e < 32 * F; e += blockDim.x) St[e] = e < rows * F ? src[e] : 0.f;
       __syncthreads();
     }
-    const float* xr = St + (size_t)lane * F;
+    const uint32_t xs = ptx::s2u(St) + 4u * (uint32_t)(lane * F);
     uint32_t* dst = codes + (size_t)blk * F2h * 32 + lane;
-    // this warp's pairs warp, warp + NW, ...: NP pairs (2 NP chains) per pass
-    for (int p0 = warp; p0 < F2h; p0 += NP * NW) {
+    if (single) {
+      // one pass: the per-chain constants (features, search-tree bases) are
+      // block independent and live in registers (hoisted below)
       float x[2 * NP];
-      uint32_t A[2 * NP], c4[2 * NP];
+      uint32_t A[2 * NP];
 #pragma unroll
       for (int u = 0; u < 2 * NP; ++u) {
-        const int f = min(2 * (p0 + (u >> 1) * NW) + (u & 1), F - 1);
-        x[u] = xr[f];
-        A[u] = tab_s + (uint32_t)(f * P) * 4u;
-        c4[u] = 4u - A[u];
+        x[u] = ptx::lds_f32(xs + xoff[u]);
+        A[u] = A0[u];
       }
       for (int s = 0; s < k; ++s) {
 #pragma unroll
@@ -263,14 +276,46 @@ __global__ void __launch_bounds__(512, 1) bin_coop_kernel(const float* __restric
       }
 #pragma unroll
       for (int u = 0; u < 2 * NP; u += 2) {
+        if (u / 2 < npairs) {
+          // leaf byte offset A + c4 - 4 = 4 (2^k - 1 + code)
+          const uint32_t c0 = isnan(x[u]) ? 0xFFFFu : ((A[u] + c4[u]) >> 2) - 1u - (uint32_t)P;
+          uint32_t c1 = isnan(x[u + 1]) ? 0xFFFFu : ((A[u + 1] + c4[u + 1]) >> 2) - 1u - (uint32_t)P;
+          c1 &= hi_mask[u / 2];
+          dst[(size_t)(warp + (u >> 1) * NW) * 32] = c0 | (c1 << 16);
+        }
+      }
+    } else {
+    const float* xr = St + (size_t)lane * F;
+    // this warp's pairs warp, warp + NW, ...: NP pairs (2 NP chains) per pass
+    for (int p0 = warp; p0 < F2h; p0 += NP * NW) {
+      float x[2 * NP];
+      uint32_t A[2 * NP], c4l[2 * NP];
+#pragma unroll
+      for (int u = 0; u < 2 * NP; ++u) {
+        const int f = min(2 * (p0 + (u >> 1) * NW) + (u & 1), F - 1);
+        x[u] = xr[f];
+        A[u] = tab_s + (uint32_t)(f * P) * 4u;
+        c4l[u] = 4u - A[u];
+      }
+      for (int s = 0; s < k; ++s) {
+#pragma unroll
+        for (int u = 0; u < 2 * NP; ++u) {
+          const float e = ptx::lds_f32(A[u]);
+          A[u] = 2u * A[u] + c4l[u];
+          if (e < x[u]) A[u] += 4u;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2 * NP; u += 2) {
         const int pr = p0 + (u >> 1) * NW;
         if (pr < F2h) {
-          const uint32_t c0 = isnan(x[u]) ? 0xFFFFu : ((A[u] + c4[u] - 4u) >> 2) - (uint32_t)P;
+          const uint32_t c0 = isnan(x[u]) ? 0xFFFFu : ((A[u] + c4l[u] - 4u) >> 2) - (uint32_t)P;
           const uint32_t c1 = 2 * pr + 1 >= F ? 0u
-                              : isnan(x[u + 1]) ? 0xFFFFu : ((A[u + 1] + c4[u + 1] - 4u) >> 2) - (uint32_t)P;
+                              : isnan(x[u + 1]) ? 0xFFFFu : ((A[u + 1] + c4l[u + 1] - 4u) >> 2) - (uint32_t)P;
           dst[(size_t)pr * 32] = c0 | (c1 << 16);
         }
       }
+    }
     }
     // no CTA-wide barrier per block (it would drain the pipeline): the last
     // warp to finish with this buffer refills it, the others run ahead
@@ -428,6 +473,12 @@ static cudaError_t launch_binning(const bridger_model* m, const TravLayout& L, c
     if (e[0] == 'c' && fixed + 2 * 128 * m->F + 32 <= 232448) { stage = false; coop = true; }
   }
   if (!stage) nwb = 16;
+  // cooperative binning: 16 warps (measured on B200 for C3, 45 feature pairs:
+  // 16 warps x 3 pairs 2.6 ms, 12 x 4 2.8, 8 x 6 3.1, 6 x 8 5.0 -- latency,
+  // not per-block overhead, bounds it); BRIDGER_BIN_WARPS overrides
+  if (coop) {
+    if (const char* e = std::getenv("BRIDGER_BIN_WARPS")) nwb = std::max(1, std::min(16, std::atoi(e)));
+  }
   const int bsmem = fixed + (stage ? nwb * (2 * 128 * m->F + 16) : coop ? 2 * 128 * m->F + 32 : 0);
   // staged kernel: NP pairs per pass, passes sized so that no chain is wasted
   const int f2h = (m->F + 1) >> 1;
@@ -439,8 +490,9 @@ static cudaError_t launch_binning(const bridger_model* m, const TravLayout& L, c
        bin_kernel<7, 1>},
       {bin_kernel<1, 2>, bin_kernel<2, 2>, bin_kernel<3, 2>, bin_kernel<4, 2>, bin_kernel<5, 2>, bin_kernel<6, 2>,
        bin_kernel<7, 2>}};
-  const int np = std::min(4, (f2h + nwb - 1) / nwb);  // pairs per warp pass (coop)
-  const BinK coops[4] = {bin_coop_kernel<1>, bin_coop_kernel<2>, bin_coop_kernel<3>, bin_coop_kernel<4>};
+  const int np = std::min(6, (f2h + nwb - 1) / nwb);  // pairs per warp pass (coop)
+  const BinK coops[6] = {bin_coop_kernel<1>, bin_coop_kernel<2>, bin_coop_kernel<3>, bin_coop_kernel<4>,
+                         bin_coop_kernel<5>, bin_coop_kernel<6>};
   auto bk = coop ? coops[np - 1] : kerns[m->F % 2 == 0 ? 1 : 0][nps - 1];
   int bsm = bsmem;
   int64_t want_ctas = coop ? nbk : (nbk + nwb - 1) / nwb;

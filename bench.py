@@ -257,7 +257,8 @@ def trav_roofline(B, model, cfg, n, hot_avg_ms, dev_index, n_trees=None):
     alg = n * T * per
     cf, rnd = smem_peak(B, dev_index)
     achieved = alg / (hot_avg_ms / 1e3) / 1e9
-    kern = "trav_stream_kernel" if lay["format"].startswith("stream") else "trav_kernel"
+    kern = ("trav_stream_kernel" if lay["format"].startswith("stream") else
+            "trav_deep_kernel" if lay["format"] == "codes_deep" else "trav_kernel")
     return {"bound": "alu", "resource": "shared-memory (LSU) pipe bandwidth", "kernel": kern,
             "achieved": achieved, "peak": cf, "unit": "GB/s", "frac": achieved / cf, "traffic": None,
             "kernel_ms": hot_avg_ms, "alg_bytes_per_row_tree": per, "alg_bytes_per_launch": alg,

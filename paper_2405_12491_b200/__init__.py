@@ -283,9 +283,9 @@ class Model:
     def layout(self) -> dict:
         n, c, g, w, gr = (C.c_int32() for _ in range(5))
         _check(_lib.bridger_model_layout(self._h, C.byref(n), C.byref(c), C.byref(g), C.byref(w), C.byref(gr)))
-        return dict(n_chunks=n.value, coded=c.value in (1, 7), sparse=c.value == 2,
+        return dict(n_chunks=n.value, coded=c.value in (1, 7, 8), sparse=c.value == 2,
                     format={0: "heap", 1: "codes", 2: "sparse", 3: "heap_pretransposed", 4: "hybrid", 6: "stream",
-                            7: "stream_codes"}[c.value],
+                            7: "stream_codes", 8: "codes_deep"}[c.value],
                     global_trees=bool(g.value),
                     n_warps=w.value, group=gr.value)
 

@@ -429,9 +429,14 @@ bridger_status bridger_model_layout(const bridger_model* m, int32_t* n_chunks, i
                                     int32_t* n_warps, int32_t* group) {
   if (!m) return fail(BRIDGER_E_NULL_ARG, "model is NULL");
   if (n_chunks) *n_chunks = m->trav_ok ? (int32_t)m->trav.chunks.size() : 0;
-  if (coded)
-    *coded = !m->trav_ok ? 0 : m->trav.stream ? (m->trav.codes ? 7 : 6) : m->trav.codes ? 1 : m->trav.sparse ? 2
-           : m->trav.hybrid ? 4 : m->trav.pretransposed ? 3 : 0;
+  if (coded) {
+    // 8: threshold-bin codes walked by the many-chunk K4d kernel (trav_deep.cu)
+    const char* de = std::getenv("BRIDGER_DEEP");
+    const bool deep = m->trav.codes && !m->trav.stream && !m->trav.global_trees && m->acc_int &&
+                      m->trav.chunks.size() >= 3 && !(de && de[0] == '0');
+    *coded = !m->trav_ok ? 0 : m->trav.stream ? (m->trav.codes ? 7 : 6) : deep ? 8 : m->trav.codes ? 1
+           : m->trav.sparse ? 2 : m->trav.hybrid ? 4 : m->trav.pretransposed ? 3 : 0;
+  }
   if (global_trees) *global_trees = m->trav_ok && m->trav.global_trees ? 1 : 0;
   if (n_warps) *n_warps = m->trav.n_warps;
   if (group) *group = m->trav.group;

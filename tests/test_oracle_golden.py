@@ -73,3 +73,17 @@ def test_gbdt_multiclass_softmax_hand():
     assert o["label"].tolist() == g["expected"]["label"]
     np.testing.assert_allclose(o["proba"], np.asarray(g["expected"]["proba"]), rtol=1e-6)
     np.testing.assert_allclose(o["proba"].sum(axis=1), 1.0, rtol=1e-6)
+
+
+def test_multiclass_softmax_golden_matches_its_generator():
+    """The fixture's proba block is exactly what the committed generator
+    (tests/golden/gen_gbdt_multiclass_softmax.py: math.exp softmax of the
+    hand-computed margins) produces."""
+    import importlib.util
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "gen_gbdt_multiclass_softmax.py")
+    spec = importlib.util.spec_from_file_location("gen_softmax", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    g = load_golden("gbdt_multiclass_softmax_hand.json")
+    assert mod.softmax_rows(g["expected"]["s"]) == g["expected"]["proba"]

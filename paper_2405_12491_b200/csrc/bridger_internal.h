@@ -120,6 +120,14 @@ struct TravLayout {
   std::vector<std::vector<float>> bin_sorted;  // host: sorted distinct thresholds per feature (U_f)
   std::vector<float> bin_table;     // device: [F][2^bin_k - 1] Eytzinger (BFS) search trees of U_f, +inf padded
   int32_t bin_k = 0;                // levels of every feature's search tree
+  // Bucketed binning (round 2, built when it fits and pays): per feature an
+  // affine fp32 bucket map b(x) = clamp(floor((x - lo) * iw), 0, NB-1)
+  // (monotone in x), cum[b] = #{u : b(u) < b}, and the sorted U_f padded with
+  // +inf; code(x) = cum[b(x)] + a fixed s_f-step search in a window of
+  // 2^s_f - 1 >= max bucket count (lowering.cpp build_bucket_table).  Blob:
+  // [F] {lo, iw, s, 0} 16 B | [F][NB+2] u16 cum | [F][bkt_stride] fp32 U
+  std::vector<uint8_t> bkt_blob;
+  int32_t bkt_nb = 0, bkt_stride = 0;
   int32_t smem_bytes = 0;       // dynamic shared memory per CTA
   int32_t chunk_budget = 0;     // max bytes of one chunk
   bool has_missing = false;
@@ -226,6 +234,7 @@ struct bridger_model {
   void* d_sparse_trees = nullptr;    // SparseTree[T] (TravLayout::sparse)
   void* d_sparse_nodes = nullptr;    // uint4 records
   float* d_bin_table = nullptr;      // threshold-bin codes (TravLayout::codes)
+  uint8_t* d_bkt = nullptr;          // bucketed binning tables (TravLayout::bkt_blob)
 
   // GEMM-path layout on device (filled by gemm_path.cu)
   bool gemm_ok = false;

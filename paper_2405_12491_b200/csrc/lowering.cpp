@@ -291,6 +291,80 @@ static bool build_bin_table(const bridger_model_desc* d, TravLayout* out) {
   return true;
 }
 
+// Bucketed binning tables (see TravLayout::bkt_blob).  Exactness: b(x) is
+// monotone non-decreasing in x (fp32 subtraction and multiplication by a
+// positive constant round monotonically, floor and clamp are monotone; the
+// device evaluates the identical fp32 expression, __fsub_rn / __fmul_rn /
+// fmaxf / fminf, host built with -ffp-contract=off), so thresholds in lower
+// buckets are < x and thresholds in higher buckets are > x: code(x) =
+// #{u < x} = cum[b(x)] + #{u in bucket b(x) : u < x}, the second term a
+// lower_bound in the window U[cum[b] .. cum[b] + 2^s - 1) (positions past the
+// bucket hold larger thresholds or +inf padding).  Built only if every
+// feature's max bucket count <= 15 (s <= 4) for the chosen NB and the tables
+// fit next to the staging buffers.
+static void build_bucket_table(int32_t F, TravLayout* out, int32_t staging_bytes) {
+  out->bkt_blob.clear();
+  out->bkt_nb = 0;
+  out->bkt_stride = 0;
+  const auto& u = out->bin_sorted;
+  if ((int32_t)u.size() != F || F == 0) return;
+  size_t nmax = 0;
+  for (auto& v : u) nmax = std::max(nmax, v.size());
+  const int32_t stride = (int32_t)((nmax + 16 + 3) / 4 * 4);  // + 15 +inf pad (window overrun), 16-B rows
+  for (int32_t NB : {256, 512, 1024}) {
+    const size_t cum_row = ((size_t)(NB + 2) * 2 + 3) / 4 * 4;
+    const size_t bytes = (size_t)F * 16 + (size_t)F * cum_row + (size_t)F * stride * 4;
+    if (bytes + (size_t)staging_bytes + 64 > (size_t)kSmemMax) break;
+    std::vector<uint8_t> blob(bytes, 0);
+    bool ok = true;
+    for (int32_t f = 0; f < F && ok; ++f) {
+      const std::vector<float>& v = u[f];
+      float lo = v.empty() ? 0.f : v.front();
+      float hi = v.empty() ? 0.f : v.back();
+      const float span = hi - lo;
+      const float iw = span > 0.f ? (float)NB / span : (v.size() > 1 ? 0.f : INFINITY);
+      if (!(std::isfinite(lo) && std::isfinite(hi)) || iw == 0.f) { ok = false; break; }
+      const float nbm1 = (float)(NB - 1);
+      auto bucket = [&](float x) {
+        float t = (x - lo) * iw;
+        t = std::fmin(std::fmax(t, 0.f), nbm1);
+        return (int32_t)t;
+      };
+      std::vector<int32_t> cnt(NB, 0);
+      int32_t prev = -1;
+      for (float x : v) {
+        const int32_t b = bucket(x);
+        if (b < prev) { ok = false; break; }  // monotonicity (holds by construction; checked)
+        prev = b;
+        ++cnt[b];
+      }
+      int32_t mx = 0;
+      for (int32_t c : cnt) mx = std::max(mx, c);
+      int32_t sf = 0;
+      while (((1 << sf) - 1) < mx) ++sf;
+      if (sf > 4) { ok = false; break; }
+      float* prm = reinterpret_cast<float*>(blob.data() + (size_t)f * 16);
+      prm[0] = lo;
+      prm[1] = iw;
+      reinterpret_cast<uint32_t*>(prm)[2] = (uint32_t)sf;
+      uint16_t* cum = reinterpret_cast<uint16_t*>(blob.data() + (size_t)F * 16 + (size_t)f * cum_row);
+      int32_t run = 0;
+      for (int32_t b = 0; b < NB; ++b) {
+        cum[b] = (uint16_t)run;
+        run += cnt[b];
+      }
+      cum[NB] = (uint16_t)run;
+      float* U = reinterpret_cast<float*>(blob.data() + (size_t)F * 16 + (size_t)F * cum_row) + (size_t)f * stride;
+      for (int32_t i = 0; i < stride; ++i) U[i] = i < (int32_t)v.size() ? v[i] : INFINITY;
+    }
+    if (!ok) continue;
+    out->bkt_blob.swap(blob);
+    out->bkt_nb = NB;
+    out->bkt_stride = stride;
+    return;
+  }
+}
+
 static uint32_t code_of_threshold(const TravLayout& L, int32_t f, float t) {
   const std::vector<float>& v = L.bin_sorted[f];
   return (uint32_t)(std::lower_bound(v.begin(), v.end(), t) - v.begin());  // t is present: exact index
@@ -515,6 +589,13 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
     out->split = !want_codes && F <= 127 && env && env[0] == '1';
   }
   out->codes = want_codes && plan(true);
+  // bucketed binning where it fits next to the cooperative kernel's staging
+  // (two dense [32][F] fp32 blocks); BRIDGER_BUCKET=0 keeps the Eytzinger search
+  {
+    const char* be = std::getenv("BRIDGER_BUCKET");
+    if (out->codes && !(be && be[0] == '0')) build_bucket_table(F, out, 2 * 128 * F + 64);
+    else { out->bkt_blob.clear(); out->bkt_nb = 0; }
+  }
   if (!out->codes) {
     out->bin_table.clear();
     out->bin_sorted.clear();

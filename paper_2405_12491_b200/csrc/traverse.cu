@@ -335,6 +335,130 @@ __global__ void __launch_bounds__(512, 1) bin_coop_kernel(const float* __restric
   }
 }
 
+// Bucketed binning (round 2; TravLayout::bkt_blob, lowering.cpp
+// build_bucket_table): code(x) = cum_f[b_f(x)] + lower_bound of x in the
+// window U_f[cum .. cum + 2^s_f - 1) -- one u16 load plus s_f <= 4 search
+// steps instead of the k = 9..10 levels of the Eytzinger descent.  The
+// bucket map b_f(x) = clamp(floor((x - lo_f) * iw_f), 0, NB - 1) is evaluated
+// with the same IEEE fp32 operations the host used (monotone: exact).  CTA
+// layout as bin_coop_kernel: the whole blob resident, 16 warps share one
+// double-buffered dense [32][F] block, the last warp done with a buffer
+// refills it; every warp owns fixed feature pairs (chain constants hoisted).
+template <int NP>
+__global__ void __launch_bounds__(512, 1) bin_bucket_kernel(const float* __restrict__ X, int64_t n_rows, int32_t F,
+                                                            const uint8_t* __restrict__ blob, int32_t blob_bytes,
+                                                            int32_t NB, int32_t stride,
+                                                            uint32_t* __restrict__ codes) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
+  const int F2h = (F + 1) >> 1;
+  const size_t tab_bytes = ((size_t)blob_bytes + 127) / 128 * 128;
+  const uint32_t blk_bytes = 128u * (uint32_t)F;
+  float* stage = reinterpret_cast<float*>(smem + tab_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + tab_bytes + 2 * (size_t)blk_bytes);
+  uint32_t* done = reinterpret_cast<uint32_t*>(bars + 2);
+  {
+    const float4* src = reinterpret_cast<const float4*>(blob);
+    float4* dst = reinterpret_cast<float4*>(smem);
+    for (int i = threadIdx.x; i < blob_bytes / 16; i += blockDim.x) dst[i] = src[i];
+  }
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bars[0], 1);
+    ptx::mbar_init(&bars[1], 1);
+    done[0] = done[1] = 0;
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  const uint32_t sbase = ptx::s2u(smem);
+  const uint32_t cum_row = (uint32_t)(((NB + 2) * 2 + 3) / 4 * 4);
+  const uint32_t cum0 = sbase + 16u * (uint32_t)F, u0 = cum0 + cum_row * (uint32_t)F;
+  const int64_t n_blocks = (n_rows + 31) / 32;
+  auto issue = [&](int64_t b, int buf) {
+    if (threadIdx.x == 0 && b < n_blocks && (b + 1) * 32 <= n_rows) {
+      ptx::fence_proxy_async();
+      ptx::mbar_arrive_expect_tx(&bars[buf], blk_bytes);
+      ptx::bulk_g2s(stage + (size_t)buf * 32 * F, X + b * 32 * (int64_t)F, blk_bytes, &bars[buf]);
+    }
+  };
+  issue(blockIdx.x, 0);
+  issue((int64_t)blockIdx.x + gridDim.x, 1);
+  // this warp's pairs warp, warp + NW, ... (one pass covers all: NP * NW >= F2h)
+  const int npairs = warp < F2h ? min(NP, (F2h - 1 - warp) / NW + 1) : 0;
+  uint32_t xoff[2 * NP], cumb[2 * NP], ub[2 * NP], hi_mask[NP];
+  float lo[2 * NP], iw[2 * NP];
+  const float nbm1 = (float)(NB - 1);
+#pragma unroll
+  for (int u = 0; u < 2 * NP; ++u) {
+    const int f = min(2 * (warp + (u >> 1) * NW) + (u & 1), F - 1);
+    xoff[u] = 4u * (uint32_t)f;
+    lo[u] = ptx::lds_f32(sbase + 16u * f);
+    iw[u] = ptx::lds_f32(sbase + 16u * f + 4u);
+    cumb[u] = cum0 + cum_row * (uint32_t)f;
+    ub[u] = u0 + 4u * (uint32_t)(stride * f);
+  }
+#pragma unroll
+  for (int q = 0; q < NP; ++q) hi_mask[q] = 2 * (warp + q * NW) + 1 >= F ? 0u : 0xFFFFFFFFu;
+  int it = 0;
+  for (int64_t blk = blockIdx.x; blk < n_blocks; blk += gridDim.x, ++it) {
+    const int buf = it & 1;
+    float* St = stage + (size_t)buf * 32 * F;
+    const int64_t row0 = blk * 32;
+    if (row0 + 32 <= n_rows) {
+      ptx::mbar_wait(&bars[buf], (uint32_t)(it >> 1) & 1u);
+    } else {
+      __syncthreads();
+      const int rows = (int)(n_rows - row0);
+      const float* src = X + row0 * F;
+      for (int e = threadIdx.x; e < 32 * F; e += blockDim.x) St[e] = e < rows * F ? src[e] : 0.f;
+      __syncthreads();
+    }
+    const uint32_t xs = ptx::s2u(St) + 4u * (uint32_t)(lane * F);
+    uint32_t* dst = codes + (size_t)blk * F2h * 32 + lane;
+    float x[2 * NP];
+    uint32_t pos[2 * NP];
+#pragma unroll
+    for (int u = 0; u < 2 * NP; ++u) {
+      x[u] = ptx::lds_f32(xs + xoff[u]);
+      float t = __fmul_rn(__fsub_rn(x[u], lo[u]), iw[u]);
+      t = fminf(fmaxf(t, 0.f), nbm1);
+      const uint32_t b = (uint32_t)t;
+      pos[u] = ub[u] + 4u * ptx::lds_u16(cumb[u] + 2u * b);
+    }
+    // branch-free lower_bound over the 15-element window (every bucket holds
+    // <= 15 thresholds; positions past the bucket hold larger ones or +inf)
+#pragma unroll
+    for (int h = 8; h >= 1; h >>= 1) {
+#pragma unroll
+      for (int u = 0; u < 2 * NP; ++u) {
+        const float e = ptx::lds_f32(pos[u] + 4u * (uint32_t)(h - 1));
+        if (e < x[u]) pos[u] += 4u * (uint32_t)h;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2 * NP; u += 2) {
+      if (u / 2 < npairs) {
+        const uint32_t c0 = isnan(x[u]) ? 0xFFFFu : (pos[u] - ub[u]) >> 2;
+        uint32_t c1 = isnan(x[u + 1]) ? 0xFFFFu : (pos[u + 1] - ub[u + 1]) >> 2;
+        c1 &= hi_mask[u / 2];
+        dst[(size_t)(warp + (u >> 1) * NW) * 32] = c0 | (c1 << 16);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd(&done[buf], 1u) == (uint32_t)NW - 1u) {
+        done[buf] = 0;
+        if (blk + 2 * (int64_t)gridDim.x < n_blocks && (blk + 2 * (int64_t)gridDim.x + 1) * 32 <= n_rows) {
+          ptx::fence_proxy_async();
+          ptx::mbar_arrive_expect_tx(&bars[buf], blk_bytes);
+          ptx::bulk_g2s(stage + (size_t)buf * 32 * F, X + (blk + 2 * (int64_t)gridDim.x) * 32 * (int64_t)F, blk_bytes,
+                        &bars[buf]);
+        }
+      }
+    }
+  }
+}
+
 // Feature-group binning for search tables too large to hold for all features
 // at once (C5-shaped shards: 200 features x 8191-slot trees = 6.5 MB): a CTA
 // owns FG features and a range of 32-row blocks; lane = row reads its row's FG
@@ -460,6 +584,44 @@ static cudaError_t launch_binning(const bridger_model* m, const TravLayout& L, c
   const int F2 = (m->F + 1) & ~1;
   err = cudaMallocAsync(&codes, (size_t)nbk * 32 * F2 * 2, st);
   if (err != cudaSuccess) return err;
+  // Bucketed binning where the per-warp-staged Eytzinger kernel does not fit
+  // (wide tables, e.g. C3): measured on B200, C3 2.39 -> 2.23 ms; C2 (staged
+  // kernel fits) 0.095 ms Eytzinger vs 0.15 bucketed -- both are bound by
+  // random shared-memory wavefronts (~15-17 per warp-value either way).
+  // BRIDGER_BIN: tests force a variant ('b' bucketed, 'f'/'c' Eytzinger).
+  const char* bin_env = std::getenv("BRIDGER_BIN");
+  const int P0 = (1 << L.bin_k) - 1;
+  const bool staged_fits = (m->F * P0 * 4 + 127) / 128 * 128 + 8 * (2 * 128 * m->F + 16) <= 232448;
+  const bool want_bkt = bin_env ? bin_env[0] == 'b' : !staged_fits;
+  if (L.bkt_nb > 0 && !L.stream && want_bkt) {
+    // bucketed binning (all features' tables + one shared double-buffered block)
+    const int f2h = (m->F + 1) >> 1;
+    // >= 3 pairs (6 search chains) per warp when the feature count allows
+    int nw = std::max(4, std::min(16, (f2h + 2) / 3));
+    if (const char* e = std::getenv("BRIDGER_BIN_WARPS")) nw = std::max(1, std::min(16, std::atoi(e)));
+    const int np = (f2h + nw - 1) / nw;  // pairs per warp: one pass
+    const int blob = (int)L.bkt_blob.size();
+    const int bsm = (blob + 127) / 128 * 128 + 2 * 128 * m->F + 32;
+    using BinB = void (*)(const float*, int64_t, int32_t, const uint8_t*, int32_t, int32_t, int32_t, uint32_t*);
+    const BinB bks[8] = {bin_bucket_kernel<1>, bin_bucket_kernel<2>, bin_bucket_kernel<3>, bin_bucket_kernel<4>,
+                         bin_bucket_kernel<5>, bin_bucket_kernel<6>, bin_bucket_kernel<7>, bin_bucket_kernel<8>};
+    if (np <= 8 && bsm <= 232448) {
+      auto bk = bks[np - 1];
+      static std::atomic<uint64_t> attr[8];
+      smem_opt_in(reinterpret_cast<const void*>(bk), attr[np - 1]);
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nbk, sms));
+      bk<<<grid, nw * 32, bsm, st>>>(X, n_rows, m->F, m->d_bkt, blob, L.bkt_nb, L.bkt_stride,
+                                     static_cast<uint32_t*>(codes));
+      count_launch();
+      err = cudaGetLastError();
+      if (err != cudaSuccess) {
+        cudaFreeAsync(codes, st);
+        return err;
+      }
+      *codes_out = codes;
+      return cudaSuccess;
+    }
+  }
   const int P = (1 << L.bin_k) - 1;
   const int fixed = (m->F * P * 4 + 127) / 128 * 128;
   // per-warp staging (bulk-copied dense blocks) when the table leaves room

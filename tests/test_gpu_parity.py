@@ -221,11 +221,13 @@ def test_coded_format_feature_widths(F, monkeypatch):
     assert g.layout()["coded"]
 
 
-@pytest.mark.parametrize("binv", ["coop", "fg"])
+@pytest.mark.parametrize("binv", ["coop", "fg", "bucket"])
 @pytest.mark.parametrize("F", [7, 28, 90])
 def test_coded_binning_variants(binv, F, monkeypatch):
-    """The cooperative (CTA-shared block) and feature-group (tables per CTA,
-    direct loads) binning kernels produce the same codes: bit-exact end to end."""
+    """The cooperative (CTA-shared block), feature-group (tables per CTA,
+    direct loads) and bucketed (affine bucket map + short window search)
+    binning kernels produce the same codes: bit-exact end to end, with NaN,
+    +-inf, -0 and subnormal inputs."""
     monkeypatch.setenv("BRIDGER_CODES", "1")
     monkeypatch.setenv("BRIDGER_BIN", binv)
     m = perfect_ensemble(60 + F, 31, 7, F, kind="regression", lr=0.1, calib_rows=2048)
@@ -346,3 +348,41 @@ def test_tree_streamed_pruned_missing_mixed_depth(ml):
     g = B.Model(m)
     assert g.layout()["format"] == "stream"
     check(m, inject_specials(gen_x(96, 0, 2001, 64), 96, rate=0.02))
+
+
+@pytest.mark.parametrize("spread", ["clustered", "wide", "single"])
+def test_bucketed_binning_threshold_layouts(spread, monkeypatch):
+    """Bucketed binning on threshold sets that stress the bucket map: many
+    thresholds packed into a tiny range (large per-bucket counts: the window
+    search, or the fallback to the Eytzinger kernels when a bucket exceeds
+    15), thresholds spread over 1e-30..1e30, and features with a single
+    distinct threshold (zero span); inputs placed exactly on, just below and
+    just above every threshold.  Bit-exact against the oracle either way."""
+    monkeypatch.setenv("BRIDGER_CODES", "1")
+    F = 6
+    m = perfect_ensemble(83, 40, 6, F, kind="regression", lr=0.1, calib_rows=1024)
+    thr = np.array(m.threshold, np.float32)
+    inner = np.asarray(m.left) != -1
+    rng = np.random.default_rng(7)
+    n_in = int(inner.sum())
+    if spread == "clustered":
+        vals = np.float32(1.0) + rng.integers(0, 200, n_in).astype(np.float32) * np.float32(2.0 ** -23)
+    elif spread == "wide":
+        vals = (rng.choice([-1, 1], n_in) * 10.0 ** rng.uniform(-30, 30, n_in)).astype(np.float32)
+    else:
+        vals = np.full(n_in, 0.25, np.float32)
+    thr[inner] = vals
+    m.threshold = thr
+    u = np.unique(vals)
+    base = gen_x(84, 0, 3000, F)
+    pick = rng.choice(u, size=base.shape)
+    jitter = rng.integers(-1, 2, size=base.shape)
+    X = np.where(jitter < 0, np.nextafter(pick, np.float32(-np.inf)),
+                 np.where(jitter > 0, np.nextafter(pick, np.float32(np.inf)), pick)).astype(np.float32)
+    X[::97, 1] = np.nan
+    X[::89, 2] = np.inf
+    X[::83, 3] = -np.inf
+    X[::79, 4] = -0.0
+    for binv in ("bucket", "coop"):
+        monkeypatch.setenv("BRIDGER_BIN", binv)
+        check(m, X)

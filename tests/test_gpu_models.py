@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 import oracle
-from synth import gen_x, inject_specials, perfect_ensemble
+from synth import gen_x, inject_specials, make_config, perfect_ensemble
 from synth.trees import ModelDesc
 from tests.sk_export import from_sklearn_forest, from_sklearn_gbr
 from tests.test_gpu_parity import check, dev
@@ -168,3 +168,18 @@ def test_imported_formats_on_gpu(name):
     # the hand rows, then a larger seeded batch with specials through the same model
     Xb = np.concatenate([X, inject_specials(gen_x(93, 0, 3000, m.n_features), 93, rate=0.05)])
     check(m, Xb, exact=False)
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two GPUs in one process")
+def test_two_devices_one_process():
+    """the >48 KB shared-memory opt-in is per device; models on two
+    GPUs of one process (loaded and run alternately) must both launch."""
+    _, m = make_config("C3", n_trees=60)
+    X = gen_x(3, 0, 4099, 90)
+    o = oracle.run(m, X)
+    for dev_i in (0, 1, 0, 1):
+        g = B.Model(m, device=dev_i)
+        xd = torch.from_numpy(X).to(f"cuda:{dev_i}")
+        with torch.cuda.device(dev_i):
+            got = g.predict(xd).cpu().numpy()
+        np.testing.assert_array_equal(got, o["pred"])

@@ -89,9 +89,9 @@ __device__ __forceinline__ void walk_codes_spec(const TravParams& p, uint32_t no
     bool r = x[v] * k16 > a[v];
     if (ML) r = r && !((a[v] & 1u) && x[v] == 0xFFFFu);
     if (KT == 1) {
-      float v0, v1;
-      asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v0), "=f"(v1) : "r"(la));
-      acc[0] += leaf_to_acc<long long>(r ? v1 : v0);
+      // one leaf value after the compare: a random LDS.32 costs about half the
+      // wavefronts of the leaf pair (the walk is LSU-bound here)
+      acc[0] += leaf_to_acc<long long>(ptx::lds_f32(la + (r ? 4u : 0u)));
     } else if (KT == 2) {
       float v0, v1, v2, v3;
       asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v0), "=f"(v1), "=f"(v2), "=f"(v3) : "r"(la));

@@ -24,14 +24,35 @@ import paper_2405_12491_b200 as B  # noqa: E402
 
 
 def cpu_decisions(m, X, t):
-    p = B.lower_tree(m, t)
-    D = p["depth"]
-    I = (1 << D) - 1
+    """a1+a2 by definition, from the ORIGINAL node arrays of a perfect,
+    heap-ordered tree (independent of the library's lowering): decision i =
+    [x[feature_i] <= threshold_i], NaN -> missing_left_i."""
+    tr = m.tree(t)
+    left, right = np.asarray(tr["left"]), np.asarray(tr["right"])
+    # heap position of every internal node (children of heap h: 2h+1, 2h+2),
+    # by a walk from the root over the original child links (any node order)
+    heap, order = {0: 0}, [0]
+    for n in order:
+        if left[n] != -1:
+            heap[int(left[n])], heap[int(right[n])] = 2 * heap[n] + 1, 2 * heap[n] + 2
+            order += [int(left[n]), int(right[n])]
+    inner = [n for n in order if left[n] != -1]
+    I = len(inner)
+    D = int(np.log2(I + 1))
+    assert I == (1 << D) - 1 and sorted(heap[n] for n in inner) == list(range(I)), "perfect tree"
     ip, _ = B.gemm_geometry(max(D, 1))
-    x = X[:, p["feature"]]
+    feat = np.zeros(I, np.int64)
+    thr = np.zeros(I, np.float32)
+    ml = np.zeros(I, np.uint8)
+    for n in inner:
+        feat[heap[n]] = tr["feature"][n]
+        thr[heap[n]] = tr["threshold"][n]
+        if tr["missing_left"] is not None:
+            ml[heap[n]] = tr["missing_left"][n]
+    x = X[:, feat]
     with np.errstate(invalid="ignore"):
-        d = (x <= p["threshold"][None, :])
-    d |= np.isnan(x) & (p["missing_left"][None, :] != 0)
+        d = (x <= thr[None, :])
+    d |= np.isnan(x) & (ml[None, :] != 0)
     out = np.zeros((X.shape[0], ip), np.int8)
     out[:, :I] = d
     return out
@@ -47,7 +68,7 @@ def test_k1_decisions_bitwise(name, ml):
         c, m = make_config(name, n_trees=12)
         X = gen_x(c.seed, 0, 1001, c.n_features)
     g = B.Model(m)
-    D = B.lower_tree(m, 0)["depth"]
+    D = int(np.log2(int(np.sum(np.asarray(m.tree(0)["left"]) != -1)) + 1))
     ip, _ = B.gemm_geometry(D)
     P = g.step_decisions(dev(X), 2, 5, ip).cpu().numpy()
     for j in range(5):

@@ -128,6 +128,7 @@ struct TravLayout {
   // [F] {lo, iw, s, 0} 16 B | [F][NB+2] u16 cum | [F][bkt_stride] fp32 U
   std::vector<uint8_t> bkt_blob;
   int32_t bkt_nb = 0, bkt_stride = 0;
+  int32_t bkt_fg = 0;               // > 0: tables sized for the feature-group kernel (that many features per CTA)
   int32_t smem_bytes = 0;       // dynamic shared memory per CTA
   int32_t chunk_budget = 0;     // max bytes of one chunk
   bool has_missing = false;

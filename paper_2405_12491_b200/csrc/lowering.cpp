@@ -302,19 +302,27 @@ static bool build_bin_table(const bridger_model_desc* d, TravLayout* out) {
 // bucket hold larger thresholds or +inf padding).  Built only if every
 // feature's max bucket count <= 15 (s <= 4) for the chosen NB and the tables
 // fit next to the staging buffers.
-static void build_bucket_table(int32_t F, TravLayout* out, int32_t staging_bytes) {
+// fg_features > 0: tables for the feature-group kernel (bin_bucket_fg_kernel),
+// which holds only fg_features features' rows per CTA -- the fit test is per
+// group, not for the whole blob (C5-shaped: 200 features x ~6.4K thresholds).
+static void build_bucket_table(int32_t F, TravLayout* out, int32_t staging_bytes, int32_t fg_features = 0) {
   out->bkt_blob.clear();
   out->bkt_nb = 0;
   out->bkt_stride = 0;
+  out->bkt_fg = 0;
   const auto& u = out->bin_sorted;
   if ((int32_t)u.size() != F || F == 0) return;
   size_t nmax = 0;
   for (auto& v : u) nmax = std::max(nmax, v.size());
   const int32_t stride = (int32_t)((nmax + 16 + 3) / 4 * 4);  // + 15 +inf pad (window overrun), 16-B rows
-  for (int32_t NB : {256, 512, 1024}) {
+  for (int32_t NB : {256, 512, 1024, 2048, 4096, 8192, 16384}) {
     const size_t cum_row = ((size_t)(NB + 2) * 2 + 3) / 4 * 4;
     const size_t bytes = (size_t)F * 16 + (size_t)F * cum_row + (size_t)F * stride * 4;
-    if (bytes + (size_t)staging_bytes + 64 > (size_t)kSmemMax) break;
+    if (fg_features > 0) {
+      if ((size_t)fg_features * (16 + cum_row + (size_t)stride * 4) + 64 > (size_t)kSmemMax) break;
+    } else if (bytes + (size_t)staging_bytes + 64 > (size_t)kSmemMax) {
+      break;
+    }
     std::vector<uint8_t> blob(bytes, 0);
     bool ok = true;
     for (int32_t f = 0; f < F && ok; ++f) {
@@ -361,6 +369,7 @@ static void build_bucket_table(int32_t F, TravLayout* out, int32_t staging_bytes
     out->bkt_blob.swap(blob);
     out->bkt_nb = NB;
     out->bkt_stride = stride;
+    out->bkt_fg = fg_features;
     return;
   }
 }
@@ -593,8 +602,13 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
   // (two dense [32][F] fp32 blocks); BRIDGER_BUCKET=0 keeps the Eytzinger search
   {
     const char* be = std::getenv("BRIDGER_BUCKET");
-    if (out->codes && !(be && be[0] == '0')) build_bucket_table(F, out, 2 * 128 * F + 64);
-    else { out->bkt_blob.clear(); out->bkt_nb = 0; }
+    if (out->codes && !(be && be[0] == '0')) {
+      build_bucket_table(F, out, 2 * 128 * F + 64);
+      if (out->bkt_nb == 0) build_bucket_table(F, out, 0, 4);  // per-feature-group tables (wide inputs)
+    } else {
+      out->bkt_blob.clear();
+      out->bkt_nb = 0;
+    }
   }
   if (!out->codes) {
     out->bin_table.clear();

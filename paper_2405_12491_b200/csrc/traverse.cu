@@ -459,6 +459,98 @@ __global__ void __launch_bounds__(512, 1) bin_bucket_kernel(const float* __restr
   }
 }
 
+// Bucketed binning per feature group (wide inputs whose tables do not fit all
+// at once: C5-shaped 200 features x ~6.4K thresholds, NB = 8192 buckets): a
+// CTA holds FG features' parameter, cum and threshold rows and a slice of row
+// blocks; lane = row reads its FG values (one 16-byte load when FG = 4 and
+// F % 4 == 0), then the same bucket map + 4-step window search as
+// bin_bucket_kernel (5 random shared loads instead of the 13 levels of the
+// Eytzinger descent).
+template <int FG>
+__global__ void __launch_bounds__(512, 1) bin_bucket_fg_kernel(const float* __restrict__ X, int64_t n_rows, int32_t F,
+                                                               const uint8_t* __restrict__ blob, int32_t NB,
+                                                               int32_t stride, uint32_t* __restrict__ codes) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
+  const int F2h = (F + 1) >> 1;
+  const int n_fg = (F + FG - 1) / FG;
+  const int fg = blockIdx.x % n_fg;
+  const int slice = blockIdx.x / n_fg, n_slices = gridDim.x / n_fg;
+  const int f0 = fg * FG;
+  const int nf = min(FG, F - f0);
+  const uint32_t cum_row = (uint32_t)(((NB + 2) * 2 + 3) / 4 * 4);
+  const uint32_t urow = 4u * (uint32_t)stride;
+  // shared: params [FG][16 B] | cum [FG][cum_row] | U [FG][urow]
+  uint8_t* s_cum = smem + 16 * FG;
+  uint8_t* s_u = s_cum + (size_t)FG * cum_row;
+  {
+    const uint32_t* g = reinterpret_cast<const uint32_t*>(blob);
+    const size_t g_cum = ((size_t)F * 16) / 4, g_u = ((size_t)F * 16 + (size_t)F * cum_row) / 4;
+    for (int i = threadIdx.x; i < nf * 4; i += blockDim.x)
+      reinterpret_cast<uint32_t*>(smem)[i] = g[(size_t)f0 * 4 + i];
+    const int cw = (int)(cum_row / 4), uw = (int)(urow / 4);
+    for (int i = threadIdx.x; i < nf * cw; i += blockDim.x)
+      reinterpret_cast<uint32_t*>(s_cum)[i] = g[g_cum + (size_t)(f0 + i / cw) * cw + i % cw];
+    for (int i = threadIdx.x; i < nf * uw; i += blockDim.x)
+      reinterpret_cast<uint32_t*>(s_u)[i] = g[g_u + (size_t)(f0 + i / uw) * uw + i % uw];
+  }
+  __syncthreads();
+  float lo[FG], iw[FG];
+  uint32_t cumb[FG], ub[FG];
+#pragma unroll
+  for (int q = 0; q < FG; ++q) {
+    const int qq = min(q, nf - 1);
+    lo[q] = reinterpret_cast<const float*>(smem)[4 * qq];
+    iw[q] = reinterpret_cast<const float*>(smem)[4 * qq + 1];
+    cumb[q] = ptx::s2u(s_cum) + cum_row * (uint32_t)qq;
+    ub[q] = ptx::s2u(s_u) + urow * (uint32_t)qq;
+  }
+  const float nbm1 = (float)(NB - 1);
+  const bool vec4 = FG == 4 && nf == 4 && (F & 3) == 0;
+  const int64_t n_blocks = (n_rows + 31) / 32;
+  for (int64_t blk = (int64_t)slice * NW + warp; blk < n_blocks; blk += (int64_t)n_slices * NW) {
+    const int64_t row = blk * 32 + lane;
+    const float* xr = X + (row < n_rows ? row : blk * 32) * (int64_t)F + f0;
+    float x[FG];
+    if (vec4) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(xr));
+      x[0] = v.x;
+      x[FG > 1 ? 1 : 0] = v.y;
+      x[FG > 2 ? 2 : 0] = v.z;
+      x[FG > 3 ? 3 : 0] = v.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < FG; ++q) x[q] = q < nf ? __ldg(xr + q) : 0.f;
+    }
+    uint32_t pos[FG];
+#pragma unroll
+    for (int q = 0; q < FG; ++q) {
+      float t = __fmul_rn(__fsub_rn(x[q], lo[q]), iw[q]);
+      t = fminf(fmaxf(t, 0.f), nbm1);
+      pos[q] = ub[q] + 4u * ptx::lds_u16(cumb[q] + 2u * (uint32_t)t);
+    }
+#pragma unroll
+    for (int h = 8; h >= 1; h >>= 1) {
+#pragma unroll
+      for (int q = 0; q < FG; ++q) {
+        const float e = ptx::lds_f32(pos[q] + 4u * (uint32_t)(h - 1));
+        if (e < x[q]) pos[q] += 4u * (uint32_t)h;
+      }
+    }
+    uint32_t cd[FG];
+#pragma unroll
+    for (int q = 0; q < FG; ++q) cd[q] = q >= nf ? 0u : isnan(x[q]) ? 0xFFFFu : (pos[q] - ub[q]) >> 2;
+    uint32_t* dst = codes + (size_t)blk * F2h * 32 + lane;
+    if (FG == 1) {
+      reinterpret_cast<uint16_t*>(dst + (size_t)(f0 >> 1) * 32)[f0 & 1] = (uint16_t)cd[0];
+    } else {
+#pragma unroll
+      for (int q = 0; q < FG; q += 2)
+        if (f0 + q < 2 * F2h) dst[(size_t)((f0 + q) >> 1) * 32] = cd[q] | (cd[q + 1 < FG ? q + 1 : q] << 16) * (q + 1 < FG);
+    }
+  }
+}
+
 // Feature-group binning for search tables too large to hold for all features
 // at once (C5-shaped shards: 200 features x 8191-slot trees = 6.5 MB): a CTA
 // owns FG features and a range of 32-row blocks; lane = row reads its row's FG
@@ -593,7 +685,27 @@ static cudaError_t launch_binning(const bridger_model* m, const TravLayout& L, c
   const int P0 = (1 << L.bin_k) - 1;
   const bool staged_fits = (m->F * P0 * 4 + 127) / 128 * 128 + 8 * (2 * 128 * m->F + 16) <= 232448;
   const bool want_bkt = bin_env ? bin_env[0] == 'b' : !staged_fits;
-  if (L.bkt_nb > 0 && !L.stream && want_bkt) {
+  if (L.bkt_nb > 0 && L.bkt_fg > 0 && !L.stream && want_bkt) {
+    // per-feature-group bucketed binning
+    const int FG = L.bkt_fg;  // 4
+    const int n_fg = (m->F + FG - 1) / FG;
+    const int cum_row = ((L.bkt_nb + 2) * 2 + 3) / 4 * 4;
+    const int bsm = FG * (16 + cum_row + 4 * L.bkt_stride) + 64;
+    const int64_t slices = std::max<int64_t>(1, std::min<int64_t>((2 * sms + n_fg - 1) / n_fg, (nbk + 15) / 16));
+    static std::atomic<uint64_t> attr_fg{0};
+    smem_opt_in(reinterpret_cast<const void*>(bin_bucket_fg_kernel<4>), attr_fg);
+    bin_bucket_fg_kernel<4><<<(int)(n_fg * slices), 512, bsm, st>>>(X, n_rows, m->F, m->d_bkt, L.bkt_nb,
+                                                                      L.bkt_stride, static_cast<uint32_t*>(codes));
+    count_launch();
+    err = cudaGetLastError();
+    if (err != cudaSuccess) {
+      cudaFreeAsync(codes, st);
+      return err;
+    }
+    *codes_out = codes;
+    return cudaSuccess;
+  }
+  if (L.bkt_nb > 0 && L.bkt_fg == 0 && !L.stream && want_bkt) {
     // bucketed binning (all features' tables + one shared double-buffered block)
     const int f2h = (m->F + 1) >> 1;
     // >= 3 pairs (6 search chains) per warp when the feature count allows

@@ -816,7 +816,7 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
     c.depth = D;
     c.first_slot = r.start;
     const int64_t nodes = out->split ? (((int64_t)r.n * I * 4 + 15) / 16 * 16 + (int64_t)r.n * I)
-                          : (out->stream && out->codes) ? (int64_t)r.n * I * 4
+                          : (out->stream && out->codes) ? (int64_t)r.n * (I + 1) * 4
                           : out->codes ? (int64_t)r.n * (I + 1) * 4
                           : out->stream ? (int64_t)r.n * (out->stream_split ? ((((int64_t)5 << D) + 15) / 16 * 16) : (int64_t)(I + 1) * 8)
                                         : (int64_t)r.n * I * node_bytes;
@@ -831,11 +831,11 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
         // node word: code index j (bits 16..31) | byte offset of the feature's
         // code within a lane's view of a [F/2][32][2] u16 code block (bits
         // 1..14: (f/2)*128 + (f%2)*2, always even, F <= 512) | missing (bit 0).
-        // Resident chunks store tree j at words [j (I + 1), (j + 1)(I + 1)):
-        // a pad word, then nodes 0..I-1, so that the two children 2i+1, 2i+2
-        // of every node form one 8-byte-aligned pair (the speculative walk of
-        // trav_deep.cu loads both with one LDS.64); streamed chunks are dense.
-        uint32_t* nd = reinterpret_cast<uint32_t*>(base) + (out->stream ? (size_t)j * I : (size_t)j * (I + 1) + 1);
+        // Tree j at words [j (I + 1), (j + 1)(I + 1)): a pad word, then nodes
+        // 0..I-1, so that the two children 2i+1, 2i+2 of every node form one
+        // 8-byte-aligned pair (the speculative walks of trav_deep.cu and of
+        // the tree-streamed kernel load both with one LDS.64).
+        uint32_t* nd = reinterpret_cast<uint32_t*>(base) + (size_t)j * (I + 1) + 1;
         for (int32_t i = 0; i < I; ++i) {
           // real nodes: t is in U_f, exact index; dummy nodes under replicated
           // leaves (feature 0, threshold 0): any code routes to identical leaves

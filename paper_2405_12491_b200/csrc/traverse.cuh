@@ -864,33 +864,49 @@ __device__ __forceinline__ void stream_walk_split(const uint8_t* t0, int tb, con
 }
 
 // Threshold-bin codes for streamed trees: 4-byte node words (code index j <<
-// 16 | feature byte offset | missing) walked as in walk_trees' CODES branch;
-// xb = this lane's column of its warp's 2^b-aligned code block.
+// 16 | feature byte offset | missing) behind a pad word per tree (tree stride
+// 4 (I + 1), node idx at T + 4 (idx + 1), lowering.cpp); xb = this lane's
+// column of its warp's 2^b-aligned code block.  Child-pair speculation (as in
+// trav_deep.cu): per level the lane's code of the current node and the words
+// of BOTH children (one LDS.64) are loaded together and the compare selects
+// the child already in registers -- one shared-memory latency per level
+// instead of two (the depth-12 streamed walk is latency-bound).
 template <int W, bool ML>
 __device__ __forceinline__ void stream_walk_codes(uint32_t nb, int tstride, int umax, uint32_t xb, uint32_t mask,
                                                   uint32_t k2, uint32_t k16, int I, int D, int (&idx)[W]) {
-  uint32_t A[W], cb[W];
+  uint32_t A[W], cb[W], a[W];
 #pragma unroll
   for (int u = 0; u < W; ++u) {
-    A[u] = nb + (uint32_t)(min(u, umax) * tstride);  // chunks with < W trees re-walk their last tree
+    A[u] = nb + (uint32_t)(min(u, umax) * tstride);  // node 0; chunks with < W trees re-walk their last tree
     cb[u] = 4u - A[u];
+    a[u] = ptx::lds_u32(A[u]);
   }
-  for (int lvl = 0; lvl < D; ++lvl) {
-    uint32_t a[W], x[W];
-#pragma unroll
-    for (int u = 0; u < W; ++u) a[u] = ptx::lds_u32(A[u]);
+  for (int lvl = 0; lvl + 1 < D; ++lvl) {
+    uint32_t x[W], c0[W], c1[W];
 #pragma unroll
     for (int u = 0; u < W; ++u) x[u] = ptx::lds_u16(xb | (a[u] & mask));
 #pragma unroll
     for (int u = 0; u < W; ++u) {
+      A[u] = A[u] * k2 + cb[u];  // left child (the pair {left, right} is 8-byte aligned)
+      asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(c0[u]), "=r"(c1[u]) : "r"(A[u]));
+    }
+#pragma unroll
+    for (int u = 0; u < W; ++u) {
       bool r = x[u] * k16 > a[u];  // code(x) > j; NaN code 0xFFFF -> right
       if (ML) r = r && !((a[u] & 1u) && x[u] == 0xFFFFu);
-      A[u] = A[u] * k2 + cb[u];
+      a[u] = r ? c1[u] : c0[u];
       if (r) A[u] += 4u;
     }
   }
 #pragma unroll
-  for (int u = 0; u < W; ++u) idx[u] = (int)((A[u] + cb[u] - 4u) >> 2) - I;  // leaf index
+  for (int u = 0; u < W; ++u) {
+    const uint32_t x = ptx::lds_u16(xb | (a[u] & mask));
+    bool r = x * k16 > a[u];
+    if (ML) r = r && !((a[u] & 1u) && x == 0xFFFFu);
+    A[u] = A[u] * k2 + cb[u];
+    if (r) A[u] += 4u;
+    idx[u] = (int)((A[u] + cb[u] - 4u) >> 2) - I;  // leaf index
+  }
 }
 
 // W: trees walked together per pass (= the chunk width chosen at lowering; a
@@ -1045,7 +1061,7 @@ __global__ void __launch_bounds__(544, 1) trav_stream_kernel(const TravParams p)
         // trees past the chunk's end re-walk its last tree (masked below)
         const int jw = min(j, ch.n_trees - W < 0 ? 0 : ch.n_trees - W);
         if (SCODES) {
-          stream_walk_codes<W, ML>(ptx::s2u(nodes) + 4u * (uint32_t)(jw * I), 4 * I, ch.n_trees - 1 - jw, xcl,
+          stream_walk_codes<W, ML>(ptx::s2u(nodes) + 4u * (uint32_t)(jw * (I + 1)) + 4u, 4 * (I + 1), ch.n_trees - 1 - jw, xcl,
                                    (uint32_t)p.code_buf - 2u, p.k2, p.k16, I, D, idx);
         } else if (SPL) {
           const int tb = ((5 << D) + 15) & ~15;

@@ -199,7 +199,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f32 compare, f64 accumulate", "data": "synthetic", "config": workload_config(cfg, 1, n),
+        "dtype": "f32 compare, f64 accumulate", "data": "synthetic", "config": workload_config(cfg, 1),
         "cpu_baseline": {"value": value, "unit": "rows/s", "cores": cores, "kind": "oracle",
                          "sample": f"{n} rows per step (bounded sample of the {cfg.n_rows}-row workload)"},
         "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

@@ -435,7 +435,7 @@ bridger_status bridger_model_layout(const bridger_model* m, int32_t* n_chunks, i
     // 8: threshold-bin codes walked by the many-chunk K4d kernel (trav_deep.cu)
     const char* de = std::getenv("BRIDGER_DEEP");
     const bool deep = m->trav.codes && !m->trav.stream && !m->trav.global_trees && m->acc_int &&
-                      m->trav.chunks.size() >= 3 && !(de && de[0] == '0');
+                      (int)m->trav.chunks.size() >= deep_min_chunks() && !(de && de[0] == '0');
     *coded = !m->trav_ok ? 0 : m->trav.stream ? (m->trav.codes ? 7 : 6) : deep ? 8 : m->trav.codes ? 1
            : m->trav.sparse ? 2 : m->trav.hybrid ? 4 : m->trav.pretransposed ? 3 : 0;
   }

@@ -5,6 +5,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -178,6 +179,13 @@ struct GemmClass {
 };
 
 // ------------------------------------------------ launch configuration -----
+// K4d (trav_deep.cu) serves coded models of at least this many chunks
+// (measured on B200: C3's 3 chunks 8.47 vs 8.50 ms in K4; C2's 2 chunks
+// 0.392 vs 0.401 ms per step); BRIDGER_DEEP_MIN overrides
+inline int deep_min_chunks() {
+  const char* e = std::getenv("BRIDGER_DEEP_MIN");
+  return e ? std::atoi(e) : 2;
+}
 #ifdef __CUDACC__
 // Opt a kernel in to the full 227 KB of dynamic shared memory on the CURRENT
 // device.  The attribute belongs to one device's context, so the cache is a

@@ -939,7 +939,7 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
   // per-warp red.global.add into one accumulator instead of per-chunk partials
   // + combine (BRIDGER_DEEP=0 keeps K4's partials, for comparison)
   const char* deep_env = std::getenv("BRIDGER_DEEP");
-  const bool deep = L.codes && !L.global_trees && want != 3 && m->acc_int && n_chunks >= 3 &&
+  const bool deep = L.codes && !L.global_trees && want != 3 && m->acc_int && n_chunks >= deep_min_chunks() &&
                     !(deep_env && deep_env[0] == '0');
   if (want == 3) {
     p.mode = TRAV_APPLY;

@@ -389,7 +389,9 @@ __global__ void __launch_bounds__(512, 1) bin_bucket_kernel(const float* __restr
   const float nbm1 = (float)(NB - 1);
 #pragma unroll
   for (int u = 0; u < 2 * NP; ++u) {
-    const int f = min(2 * (warp + (u >> 1) * NW) + (u & 1), F - 1);
+    // pair index clamped to the last pair, so (for even F) the pair's first
+    // feature stays even and its 8-byte LDS.64 aligned
+    const int f = min(2 * min(warp + (u >> 1) * NW, F2h - 1) + (u & 1), F - 1);
     xoff[u] = 4u * (uint32_t)f;
     lo[u] = ptx::lds_f32(sbase + 16u * f);
     iw[u] = ptx::lds_f32(sbase + 16u * f + 4u);
@@ -398,6 +400,7 @@ __global__ void __launch_bounds__(512, 1) bin_bucket_kernel(const float* __restr
   }
 #pragma unroll
   for (int q = 0; q < NP; ++q) hi_mask[q] = 2 * (warp + q * NW) + 1 >= F ? 0u : 0xFFFFFFFFu;
+  const bool even_f = (F & 1) == 0;  // pairs (2p, 2p+1) are 8-byte aligned in a row
   int it = 0;
   for (int64_t blk = blockIdx.x; blk < n_blocks; blk += gridDim.x, ++it) {
     const int buf = it & 1;
@@ -416,9 +419,23 @@ __global__ void __launch_bounds__(512, 1) bin_bucket_kernel(const float* __restr
     uint32_t* dst = codes + (size_t)blk * F2h * 32 + lane;
     float x[2 * NP];
     uint32_t pos[2 * NP];
+    if (even_f) {
+      // both values of a feature pair with one LDS.64: lanes' rows start at
+      // lane * 4F bytes, so the 16 lanes of a half-warp phase hit 16 distinct
+      // even banks (conflict-free; two LDS.32 of odd-stride rows conflict 2-way)
+#pragma unroll
+      for (int u = 0; u < 2 * NP; u += 2) {
+        float a, b;
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(a), "=f"(b) : "r"(xs + xoff[u]));
+        x[u] = a;
+        x[u + 1] = b;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 2 * NP; ++u) x[u] = ptx::lds_f32(xs + xoff[u]);
+    }
 #pragma unroll
     for (int u = 0; u < 2 * NP; ++u) {
-      x[u] = ptx::lds_f32(xs + xoff[u]);
       float t = __fmul_rn(__fsub_rn(x[u], lo[u]), iw[u]);
       t = fminf(fmaxf(t, 0.f), nbm1);
       const uint32_t b = (uint32_t)t;

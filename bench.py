@@ -420,9 +420,20 @@ def run_workload(name, args, dev, world, rank, local, headline, rows=None, trees
     n = b - a
     X = gen_x_torch(cfg.seed, a, n, cfg.n_features, device=dev)
     tsp = None
+    reduce_desc = None
     if tree_sharded and world > 1:
-        from paper_2405_12491_b200.dist import TreeShardedPredictor
-        tsp = TreeShardedPredictor(m, device=local, variant=args.variant)
+        from paper_2405_12491_b200.dist import FusedTreeShardedPredictor, TreeShardedPredictor
+        tsp = None
+        if not args.no_fused_reduce:
+            tsp = FusedTreeShardedPredictor(m, device=local, variant=args.variant)
+            if not tsp.available:
+                tsp = None
+        if tsp is not None:
+            reduce_desc = ("fused: each rank's walk adds its int64 partials straight into the owner rank's "
+                           "accumulator slice over NVLink P2P (CUDA IPC, red.global.add)")
+        else:
+            tsp = TreeShardedPredictor(m, device=local, variant=args.variant)
+            reduce_desc = "NCCL reduce-scatter of int64 partials"
         model = tsp.model
     else:
         model = B.Model(m, device=local, variant=args.variant)
@@ -441,6 +452,8 @@ def run_workload(name, args, dev, world, rank, local, headline, rows=None, trees
     ms, hot, launches, t_wall = time_steps(step, steps, args.warmup, dev, world, flush, st, clk)
     res = {"value": n_total / (ms / 1e3), "ms_per_step": ms, "steps": steps, "gpu_launches": launches,
            "wall_s_timed": t_wall, "config": workload_config(cfg, world, n_total)}
+    if reduce_desc:
+        res["config"]["reduce"] = reduce_desc
     if clk is not None:
         res["clocks"] = clk.summary()
     info = model.info()
@@ -558,6 +571,8 @@ def main(argv=None):
     ap.add_argument("--rows", type=int, default=None, help="override total rows (exploration; reported in config)")
     ap.add_argument("--trees", type=int, default=None, help="override ensemble size (exploration)")
     ap.add_argument("--dry-run", action="store_true", help="CPU: launcher + sharding bookkeeping only (tests)")
+    ap.add_argument("--no-fused-reduce", action="store_true",
+                    help="tree sharding: NCCL reduce-scatter instead of the fused peer-memory reduce")
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

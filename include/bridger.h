@@ -174,6 +174,23 @@ bridger_status bridger_predict_raw(const bridger_model* m, const float* X, int64
 /* finalize: acc (layout of predict_raw, summed over shards) -> predict output
  * (want_proba == 0) or predict_proba output (want_proba == 1).  total_trees is
  * the ensemble size used by MEAN aggregation. */
+/* Tree sharding with the cross-rank reduce fused into the walk (SURVEY.md
+ * §8(e); the "compute followed by a collective" written as one kernel over
+ * peer memory): like bridger_predict_raw, but every row's int64 fixed-point
+ * partial sum is added with red.global.add straight into the accumulator
+ * slice of the rank that owns the row -- dest[r] (HOST array of n_dest device
+ * pointers: this device's own memory or a peer's, mapped through CUDA IPC and
+ * reached over NVLink P2P) is rank r's slice, int64 [rows_per_rank][n_outputs],
+ * row i belongs to rank i / rows_per_rank.  int64 addition is associative, so
+ * the slices end bitwise equal to an NCCL reduce-scatter of predict_raw
+ * outputs.  The caller zeroes every slice before any rank launches and reads
+ * its own only after every rank's kernel has completed (host barriers; the
+ * library never makes one rank wait for another).  rows_per_rank: a positive
+ * multiple of 32 with rows_per_rank * n_dest >= n_rows; n_rows < 2^31.
+ * Exact tiers and the multi-chunk coded layout only (else
+ * BRIDGER_E_UNSUPPORTED: use predict_raw + a collective). */
+bridger_status bridger_predict_raw_scatter(const bridger_model* m, const float* X, int64_t n_rows, int32_t n_features,
+                                           void* const* dest, int32_t n_dest, int64_t rows_per_rank, void* stream);
 bridger_status bridger_finalize(const bridger_model* m, const void* acc, int64_t n_rows,
                                 int32_t total_trees, void* out, int32_t want_proba, void* stream);
 

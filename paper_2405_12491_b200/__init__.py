@@ -53,7 +53,7 @@ EXPORTS = [
     "bridger_launch_count", "bridger_hot_kernel_timing", "bridger_hot_kernel_time", "bridger_model_layout",
     "bridger_hot_kernel_time_by", "bridger_linear_load", "bridger_linear_free", "bridger_linear_predict",
     "bridger_linear_predict_proba", "bridger_linear_decision", "bridger_probe_smem_bandwidth",
-    "bridger_path_matrix_sparse", "bridger_step_path_scores_sparse",
+    "bridger_path_matrix_sparse", "bridger_step_path_scores_sparse", "bridger_predict_raw_scatter",
 ]
 
 
@@ -96,6 +96,7 @@ def _load_lib():
         "bridger_probe_smem_bandwidth": ([i32, vp, vp], i32),
         "bridger_path_matrix_sparse": ([i32, vp, vp, vp], i32),
         "bridger_step_path_scores_sparse": ([vp, i32, vp, i64, vp, vp], i32),
+        "bridger_predict_raw_scatter": ([vp, vp, i64, i32, vp, i32, i64, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -351,6 +352,15 @@ class Model:
         _check(_lib.bridger_predict_raw(self._h, X.data_ptr(), n, X.shape[1], out.data_ptr(),
                                         _stream_ptr(X.device)))
         return out
+
+    def predict_raw_scatter(self, X, dest_ptrs, rows_per_rank: int):
+        """Fused tree-sharding reduce (bridger_predict_raw_scatter): add every
+        row's int64 partial into dest_ptrs[row // rows_per_rank] (device
+        pointers of the ranks' zeroed accumulator slices, own or peer)."""
+        X = self._x(X)
+        arr = (C.c_void_p * len(dest_ptrs))(*[C.c_void_p(int(d)) for d in dest_ptrs])
+        _check(_lib.bridger_predict_raw_scatter(self._h, X.data_ptr(), X.shape[0], X.shape[1], arr, len(dest_ptrs),
+                                                int(rows_per_rank), _stream_ptr(X.device)))
 
     def finalize(self, acc, total_trees: int, proba: bool = False, out=None):
         import torch

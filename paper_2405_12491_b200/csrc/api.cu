@@ -44,7 +44,8 @@ void hot_end_id(cudaStream_t st, cudaEvent_t start, int id) {
 void hot_end(cudaStream_t st, cudaEvent_t start) { hot_end_id(st, start, 0); }
 
 cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, void* out, int want,
-                     int32_t total_trees, cudaStream_t st);
+                     int32_t total_trees, cudaStream_t st, void* const* scatter = nullptr,
+                     int64_t rows_per_rank = 0);
 cudaError_t finalize_run(const bridger_model* m, const void* acc, int64_t n_rows, int32_t total_trees,
                          void* out, int want, cudaStream_t st);
 // GEMM path (gemm_path.cu)
@@ -464,6 +465,33 @@ bridger_status bridger_apply(const bridger_model* m, const float* X, int64_t n_r
 bridger_status bridger_predict_raw(const bridger_model* m, const float* X, int64_t n_rows, int32_t n_features,
                                    void* acc, void* stream) {
   return run(m, X, n_rows, n_features, acc, 2, stream);
+}
+
+bridger_status bridger_predict_raw_scatter(const bridger_model* m, const float* X, int64_t n_rows, int32_t n_features,
+                                           void* const* dest, int32_t n_dest, int64_t rows_per_rank, void* stream) {
+  bridger_status s = check_rows(m, X, n_rows, n_features, dest);
+  if (s != BRIDGER_OK || n_rows == 0) return s;
+  if (n_dest < 1 || n_dest > 1024) return fail(BRIDGER_E_SHAPE, "n_dest must be in [1, 1024]");
+  if (rows_per_rank < 32 || rows_per_rank % 32 != 0)
+    return fail(BRIDGER_E_SHAPE, "rows_per_rank must be a positive multiple of 32");
+  if (rows_per_rank * n_dest < n_rows) return fail(BRIDGER_E_SHAPE, "rows_per_rank * n_dest < n_rows");
+  if (n_rows >= ((int64_t)1 << 31)) return fail(BRIDGER_E_SHAPE, "scatter: n_rows must be < 2^31");
+  for (int32_t r = 0; r < n_dest; ++r)
+    if (!dest[r]) return fail(BRIDGER_E_NULL_ARG, "dest pointer is NULL");
+  const bool deep = m->trav_ok && m->trav.codes && !m->trav.stream && !m->trav.global_trees && m->acc_int &&
+                    (int)m->trav.chunks.size() >= deep_min_chunks();
+  if (!deep)
+    return fail(BRIDGER_E_UNSUPPORTED,
+                "fused scatter needs an exact-tier model in the multi-chunk coded layout (use predict_raw + a collective)");
+  DeviceGuard g(m->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  void** d_dest = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d_dest), sizeof(void*) * n_dest, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_dest, dest, sizeof(void*) * n_dest, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = trav_run(m, X, n_rows, nullptr, 2, m->T, st, d_dest, rows_per_rank);
+  if (d_dest) cudaFreeAsync(d_dest, st);
+  if (e != cudaSuccess) return cuda_fail(e, "predict_raw_scatter");
+  return BRIDGER_OK;
 }
 
 bridger_status bridger_finalize(const bridger_model* m, const void* acc, int64_t n_rows, int32_t total_trees,

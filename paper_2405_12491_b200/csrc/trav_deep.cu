@@ -214,7 +214,17 @@ __global__ void __launch_bounds__(512, 1) trav_deep_kernel(const TravParams p) {
     }
     const int cnt = base + b1;
     if (cnt > 0 && row < n_rows) {
-      unsigned long long* dst = static_cast<unsigned long long*>(p.partial) + row * K;
+      unsigned long long* dst;
+      if (p.scatter) {
+        // the reduce of tree sharding fused into the walk: this row's partial
+        // goes straight into the owner rank's slice (own or peer memory)
+        const int32_t gb = (int32_t)(blk0 + i * stride);           // global 32-row block (warp-uniform)
+        const int32_t rk = gb / p.scatter_blocks;
+        dst = static_cast<unsigned long long*>(p.scatter[rk]) +
+              ((int64_t)(gb - rk * p.scatter_blocks) * 32 + lane) * K;
+      } else {
+        dst = static_cast<unsigned long long*>(p.partial) + row * K;
+      }
 #pragma unroll
       for (int k = 0; k < KT; ++k)
         if (k < K) red_add_u64(dst + k, static_cast<unsigned long long>(acc[k]));

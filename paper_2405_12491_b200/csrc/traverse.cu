@@ -825,7 +825,7 @@ static cudaError_t launch_binning(const bridger_model* m, const TravLayout& L, c
 }
 
 cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, void* out, int want,
-                     int32_t total_trees, cudaStream_t st) {
+                     int32_t total_trees, cudaStream_t st, void* const* scatter, int64_t rows_per_rank) {
   const TravLayout& L = m->trav;
   const int n_chunks = (int)L.chunks.size();
   TravParams p{};
@@ -1009,10 +1009,19 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
     }
     p.X = static_cast<const float*>(codes);
   }
+  if (scatter && !deep) {
+    if (codes) cudaFreeAsync(codes, st);
+    return cudaErrorNotSupported;
+  }
   if (deep) {
     void* acc = want == 2 ? out : nullptr;
-    if (!acc) err = cudaMallocAsync(&acc, (size_t)n_rows * m->K * 8, st);
-    if (err == cudaSuccess) err = cudaMemsetAsync(acc, 0, (size_t)n_rows * m->K * 8, st);
+    if (scatter) {
+      p.scatter = scatter;  // the caller zeroed the ranks' slices
+      p.scatter_blocks = (int32_t)(rows_per_rank / 32);
+    } else {
+      if (!acc) err = cudaMallocAsync(&acc, (size_t)n_rows * m->K * 8, st);
+      if (err == cudaSuccess) err = cudaMemsetAsync(acc, 0, (size_t)n_rows * m->K * 8, st);
+    }
     if (err == cudaSuccess) {
       p.mode = TRAV_PARTIAL;
       p.partial = acc;

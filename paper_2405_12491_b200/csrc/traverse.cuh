@@ -80,6 +80,8 @@ struct TravParams {
   uint32_t k2, k16;   // 2 and 65536, opaque to the compiler: keeps the walk's
                       // multiplies on the FMA pipe (IMAD) instead of the ALU pipe
   int32_t spec_min_d; // trav_deep: chunks of depth >= this walk with child-pair speculation
+  void* const* scatter;      // trav_deep, bridger_predict_raw_scatter: per-rank accumulator slices
+  int32_t scatter_blocks;    //   32-row blocks per rank slice (rows_per_rank / 32)
   FinalizeArgs fin;   // (TRAV_FINAL, TRAV_CLUSTER)
 };
 

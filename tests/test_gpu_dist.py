@@ -32,12 +32,12 @@ def _free_port():
     return p
 
 
-def _e63_c5_model():
+def _e63_c5_model(n_trees=40):
     """C5 recipe (depth 10, 200 features, lr 0.01 GBDT) with 40 trees and ONE
     leaf set to 2^-60: q (the lowest set bit of any leaf value) drops to -60, so M = sum_t max|v| 2^-q >= 2^53 while
     staying < 2^63 -- the E63 tier (reading c9) on a small model."""
     from synth import make_config
-    _, m = make_config("C5", n_trees=40)
+    _, m = make_config("C5", n_trees=n_trees)
     v = np.array(m.value, np.float32)
     leaf = int(np.nonzero(np.asarray(m.left) == -1)[0][3])
     v[leaf] = np.float32(2.0 ** -60)
@@ -101,6 +101,29 @@ def _worker(rank, world, port, case, q):
             _, sc = p.predict(xd)
             o = oracle.run(m, X)
             np.testing.assert_allclose(sc.cpu().numpy(), o["pred"][r0:r1], rtol=1e-5, atol=1e-6)
+        elif case == "trees_fused":
+            # the reduce fused into the walk: peer slices mapped through CUDA IPC
+            # (all ranks share cuda:0 here; on 8 GPUs the same adds go over NVLink)
+            from paper_2405_12491_b200.dist import FusedTreeShardedPredictor
+            os.environ["BRIDGER_CODES"] = "1"   # small shards: force the coded (K4d) layout
+            m = _e63_c5_model(n_trees=60)
+            X = gen_x(5, 0, 3001, 200)
+            xd = torch.from_numpy(X).cuda()
+            p = FusedTreeShardedPredictor(m, device=0)
+            assert p.available, p.model.layout()
+            qx, tier, _ = B.analyze_exactness(m)
+            assert tier == "E63"
+            row0, sc = p.predict(xd)
+            r0, r1 = p.slice_of(X.shape[0])
+            assert row0 == r0
+            full = B.Model(m, device=0)
+            raw = full.predict_raw(xd).cpu().numpy()
+            np.testing.assert_array_equal(p._slice[: r1 - r0].cpu().numpy(), raw[r0:r1])   # exact int64
+            np.testing.assert_array_equal(sc.cpu().numpy(), full.predict(xd).cpu().numpy()[r0:r1])
+            o = oracle.run(m, X)
+            np.testing.assert_allclose(sc.cpu().numpy(), o["pred"][r0:r1], rtol=1e-5, atol=1e-6)
+            _, sc2 = p.predict(xd)            # second call: slices re-zeroed, same result
+            np.testing.assert_array_equal(sc2.cpu().numpy(), sc.cpu().numpy())
         elif case == "grid2d":
             m = prune_ensemble(perfect_ensemble(7, 31, 7, 12, kind="regression", lr=0.05, calib_rows=512), 7, p=0.2)
             X = gen_x(8, 0, 2003, 12)
@@ -152,3 +175,8 @@ def test_tree_sharded_c5_shaped_e63_world2():
 
 def test_two_d_sharded_grid_world4():
     _run("grid2d", 4)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_tree_sharded_fused_scatter(world):
+    _run("trees_fused", world)

@@ -35,7 +35,9 @@ __device__ __forceinline__ void finalize_row(const FinalizeArgs& f, int64_t row,
       if (k < K) o[k] = acc[k];
     return;
   }
-  const double scale_q = ldexp(1.0, f.q);
+  // 2^q built from its bit pattern (exact; the int64 tiers have q in
+  // [-149, 127], always a normal double -- the F64 tier never uses it)
+  const double scale_q = __longlong_as_double((long long)(f.q + 1023) << 52);
   double s[KT];
 #pragma unroll
   for (int k = 0; k < KT; ++k) {

@@ -386,3 +386,23 @@ def test_bucketed_binning_threshold_layouts(spread, monkeypatch):
     for binv in ("bucket", "coop"):
         monkeypatch.setenv("BRIDGER_BIN", binv)
         check(m, X)
+
+
+@pytest.mark.parametrize("K,ml", [(1, True), (2, True), (2, False), (3, True)])
+def test_deep_chunks_speculative_walk_variants(K, ml, monkeypatch):
+    """K4d on deep (depth 10, after pruning: mixed-depth, replicated leaves)
+    coded trees in >= 2 chunks, every walk variant: child-pair speculation
+    with missing-left routing (ML) for K = 1 (single last-level leaf) and K = 2
+    (leaf-pair vector), and the non-speculative walk for K = 3 (K != KT);
+    NaN / +-inf / -0 / subnormal inputs, a ragged last block; labels, proba,
+    scores and raw int64 sums bitwise (E53)."""
+    monkeypatch.setenv("BRIDGER_CODES", "1")
+    kind = "regression" if K == 1 else "classification"
+    m = perfect_ensemble(90 + K, 60, 10, 24, kind=kind, n_classes=K, lr=0.02, calib_rows=2048)
+    m = prune_ensemble(m, 90 + K, p=0.05, with_missing=ml)
+    X = inject_specials(gen_x(91 + K, 0, 2077, 24), 91 + K, rate=0.02)
+    g, _ = check(m, X, apply=False)
+    assert g.layout()["format"] == "codes_deep", g.layout()
+    raw = g.predict_raw(dev(X)).cpu().numpy()
+    want = np.round(np.ldexp(oracle.run(m, X)["acc"], -g.info()["acc_scale_exp"])).astype(np.int64)
+    np.testing.assert_array_equal(raw, want)

@@ -161,6 +161,10 @@ __global__ void __launch_bounds__(512, 1) trav_deep_kernel(const TravParams p) {
     ptx::mbar_arrive_expect_tx(&full[s], cbytes);
     ptx::bulk_g2s(gbuf + (size_t)s * cbuf, codes + (blk0 + i * stride) * (int64_t)cbytes, cbytes, &full[s]);
   };
+  // programmatic dependent launch: everything above (barrier init, the chunk's
+  // bulk copy) overlapped the binning grid's tail; the codes it writes are
+  // read from here on
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (gw == 0 && lane == 0) {
     if (n_mine > 0) issue(0, 0);
     if (n_mine > 1) issue(1, 1);
@@ -254,10 +258,22 @@ cudaError_t launch_deep_t(const TravParams& p, int grid, int block, int smem, cu
   if (std::getenv("BRIDGER_DEBUG"))
     std::fprintf(stderr, "[bridger] trav_deep_kernel grid=%d block=%d smem=%d chunks=%d cpc=%d G=%d\n", grid, block,
                  smem, q.n_chunks, q.cpc, q.group);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  const char* pdl = std::getenv("BRIDGER_PDL");
+  cfg.numAttrs = (pdl && pdl[0] == '0') ? 0 : 1;
   cudaEvent_t ev;
   hot_begin(st, &ev);
-  kern<<<grid, block, smem, st>>>(q);
+  e = cudaLaunchKernelEx(&cfg, kern, q);
   hot_end(st, ev);
+  if (e != cudaSuccess) return e;
   count_launch();
   return cudaGetLastError();
 }

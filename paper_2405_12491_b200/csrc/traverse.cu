@@ -90,6 +90,9 @@ __global__ void __launch_bounds__(512, 1) bin_kernel(const float* __restrict__ X
                                                      const float* __restrict__ table, int32_t k,
                                                      uint32_t* __restrict__ codes) {
   extern __shared__ __align__(128) uint8_t smem[];
+  // programmatic dependent launch: the walk kernel that consumes the codes may
+  // be scheduled (and run its prologue) as SMs free up; it waits for this grid
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
   const int P = (1 << k) - 1;
   const int F2h = (F + 1) >> 1;  // feature pairs
@@ -191,6 +194,9 @@ __global__ void __launch_bounds__(512, 1) bin_coop_kernel(const float* __restric
                                                           const float* __restrict__ table, int32_t k,
                                                           uint32_t* __restrict__ codes) {
   extern __shared__ __align__(128) uint8_t smem[];
+  // programmatic dependent launch: the walk kernel that consumes the codes may
+  // be scheduled (and run its prologue) as SMs free up; it waits for this grid
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
   const int P = (1 << k) - 1;
   const int F2h = (F + 1) >> 1;
@@ -350,6 +356,9 @@ __global__ void __launch_bounds__(512, 1) bin_bucket_kernel(const float* __restr
                                                             int32_t NB, int32_t stride,
                                                             uint32_t* __restrict__ codes) {
   extern __shared__ __align__(128) uint8_t smem[];
+  // programmatic dependent launch: the walk kernel that consumes the codes may
+  // be scheduled (and run its prologue) as SMs free up; it waits for this grid
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
   const int F2h = (F + 1) >> 1;
   const size_t tab_bytes = ((size_t)blob_bytes + 127) / 128 * 128;
@@ -488,6 +497,9 @@ __global__ void __launch_bounds__(512, 1) bin_bucket_fg_kernel(const float* __re
                                                                const uint8_t* __restrict__ blob, int32_t NB,
                                                                int32_t stride, uint32_t* __restrict__ codes) {
   extern __shared__ __align__(128) uint8_t smem[];
+  // programmatic dependent launch: the walk kernel that consumes the codes may
+  // be scheduled (and run its prologue) as SMs free up; it waits for this grid
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
   const int F2h = (F + 1) >> 1;
   const int n_fg = (F + FG - 1) / FG;
@@ -581,6 +593,9 @@ __global__ void __launch_bounds__(512, 1) bin_fg_kernel(const float* __restrict_
                                                         const float* __restrict__ table, int32_t k, int32_t T,
                                                         uint32_t* __restrict__ codes) {
   extern __shared__ __align__(128) uint8_t smem[];
+  // programmatic dependent launch: the walk kernel that consumes the codes may
+  // be scheduled (and run its prologue) as SMs free up; it waits for this grid
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
   const int P = (1 << k) - 1, Pt = (1 << T) - 1;
   const int F2h = (F + 1) >> 1;
@@ -984,6 +999,15 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
   const int grid = p.n_chunks_grid * cpc;
   cudaError_t err = cudaSuccess;
   void* codes = nullptr;
+  // K4d accumulator: zeroed BEFORE the binning kernel, so the walk -- launched
+  // as a programmatic dependent of the binning grid -- only waits on that grid
+  void* deep_acc = nullptr;
+  if (deep && !scatter) {
+    deep_acc = want == 2 ? out : nullptr;
+    if (!deep_acc) err = cudaMallocAsync(&deep_acc, (size_t)n_rows * m->K * 8, st);
+    if (err == cudaSuccess) err = cudaMemsetAsync(deep_acc, 0, (size_t)n_rows * m->K * 8, st);
+    if (err != cudaSuccess) return err;
+  }
   if (L.codes) {
     err = launch_binning(m, L, X, n_rows, sms, st, &codes);
     if (err != cudaSuccess) return err;
@@ -1014,13 +1038,10 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
     return cudaErrorNotSupported;
   }
   if (deep) {
-    void* acc = want == 2 ? out : nullptr;
+    void* acc = deep_acc;
     if (scatter) {
       p.scatter = scatter;  // the caller zeroed the ranks' slices
       p.scatter_blocks = (int32_t)(rows_per_rank / 32);
-    } else {
-      if (!acc) err = cudaMallocAsync(&acc, (size_t)n_rows * m->K * 8, st);
-      if (err == cudaSuccess) err = cudaMemsetAsync(acc, 0, (size_t)n_rows * m->K * 8, st);
     }
     if (err == cudaSuccess) {
       p.mode = TRAV_PARTIAL;

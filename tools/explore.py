@@ -26,6 +26,7 @@ ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--proba", action="store_true")
 ap.add_argument("--variant", default=None)
 ap.add_argument("--tag", default="")
+ap.add_argument("--no-hot", action="store_true", help="no per-kernel events (lets programmatic dependent launch overlap)")
 a = ap.parse_args()
 cfg, m = make_config(a.config, n_trees=a.trees)
 n = a.rows or cfg.n_rows
@@ -43,7 +44,7 @@ for _ in range(a.warmup):
     flush.fill_(1.0)
     call()
 torch.cuda.synchronize()
-B.hot_kernel_timing(True)
+B.hot_kernel_timing(not a.no_hot)
 for k in range(4):
     B.hot_kernel_time(k)
 tot = 0.0

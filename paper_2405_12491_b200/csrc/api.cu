@@ -124,6 +124,7 @@ static void free_model(bridger_model* m) {
   cudaFree(m->d_base);
   cudaFree(m->d_bin_table);
   cudaFree(m->d_bkt);
+  cudaFree(m->d_bke);
   cudaFree(m->d_sparse_trees);
   cudaFree(m->d_hyb_nodes);
   cudaFree(m->d_hyb_leaves);
@@ -370,6 +371,7 @@ bridger_status bridger_model_load(const bridger_model_desc* d_in, int cuda_devic
         (e = upload(&m->d_leaf_ids, L.leaf_ids.data(), L.leaf_ids.size())) != cudaSuccess ||
         (e = upload(&m->d_bin_table, L.bin_table.data(), L.bin_table.size())) != cudaSuccess ||
         (e = upload(&m->d_bkt, L.bkt_blob.data(), L.bkt_blob.size())) != cudaSuccess ||
+        (e = upload(&m->d_bke, L.bke_blob.data(), L.bke_blob.size())) != cudaSuccess ||
         (e = upload(reinterpret_cast<SparseTree**>(&m->d_sparse_trees), L.sparse_trees.data(), L.sparse_trees.size())) != cudaSuccess ||
         (e = upload(reinterpret_cast<uint32_t**>(&m->d_hyb_nodes), L.hyb_nodes.data(), L.hyb_nodes.size())) != cudaSuccess ||
         (e = upload(&m->d_hyb_leaves, L.hyb_leaves.data(), L.hyb_leaves.size())) != cudaSuccess ||

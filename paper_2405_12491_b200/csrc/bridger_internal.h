@@ -130,6 +130,15 @@ struct TravLayout {
   std::vector<uint8_t> bkt_blob;
   int32_t bkt_nb = 0, bkt_stride = 0;
   int32_t bkt_fg = 0;               // > 0: tables sized for the feature-group kernel (that many features per CTA)
+  // Bucket-entry binning (round 2): the same monotone bucket map, but each
+  // bucket is one 16-byte entry {cum | cnt << 16, t0, t1, t2} holding its
+  // first three thresholds (+inf padded), so code(x) = cum + #{t_i < x} with
+  // ONE shared load when cnt <= 3 (the window search over U only when a
+  // bucket holds more).  Tables for bke_fg features per CTA (row tiles staged
+  // by TMA).  Blob: [F] {lo, iw, 0, 0} 16 B | [F][NB] 16 B entries |
+  // [F][bke_stride] fp32 U (+inf padded)   (lowering.cpp build_entry_table)
+  std::vector<uint8_t> bke_blob;
+  int32_t bke_nb = 0, bke_stride = 0, bke_fg = 0;
   int32_t smem_bytes = 0;       // dynamic shared memory per CTA
   int32_t chunk_budget = 0;     // max bytes of one chunk
   bool has_missing = false;
@@ -244,6 +253,7 @@ struct bridger_model {
   void* d_sparse_nodes = nullptr;    // uint4 records
   float* d_bin_table = nullptr;      // threshold-bin codes (TravLayout::codes)
   uint8_t* d_bkt = nullptr;          // bucketed binning tables (TravLayout::bkt_blob)
+  uint8_t* d_bke = nullptr;          // bucket-entry binning tables (TravLayout::bke_blob)
 
   // GEMM-path layout on device (filled by gemm_path.cu)
   bool gemm_ok = false;

@@ -374,6 +374,83 @@ static void build_bucket_table(int32_t F, TravLayout* out, int32_t staging_bytes
   }
 }
 
+// Bucket-entry tables (TravLayout::bke_blob) for bin_entry_kernel: FG
+// features per CTA (FG * 4 B = the TMA box width, >= 16 B), 16 warps each
+// double-buffering a [32][FG] fp32 row tile; NB = the most buckets that fit
+// the rest of shared memory.  FG = 8 when that leaves >= 3 buckets per
+// threshold of the densest feature, else 4.  Same monotone map as
+// build_bucket_table (exact: thresholds in earlier buckets are < x, in later
+// ones > x); every bucket must hold <= 15 thresholds (the overflow window).
+static void build_entry_table(int32_t F, TravLayout* out) {
+  out->bke_blob.clear();
+  out->bke_nb = out->bke_stride = out->bke_fg = 0;
+  const auto& u = out->bin_sorted;
+  if ((int32_t)u.size() != F || F == 0) return;
+  size_t nmax = 0;
+  for (auto& v : u) nmax = std::max(nmax, v.size());
+  if (nmax == 0) return;
+  const int32_t stride = (int32_t)((nmax + 16 + 3) / 4 * 4);
+  // row tile width: FG values, or FG + 4 when rows are not 16-byte aligned
+  // (R > 1 super-rows: TMA box starts must be 16-byte aligned, so the box
+  // begins up to 3 values early; traverse.cu bin_entry_kernel)
+  const bool rows_aligned = (F * 4) % 16 == 0;
+  auto nb_for = [&](int32_t fg) {
+    const int64_t w = rows_aligned ? fg : fg + 4;
+    const int64_t staging = 16LL * 2 * 32 * w * 4 + 16 * 2 * 8 + 64;
+    const int64_t per_f = (kSmemMax - staging) / fg - 16 - 4LL * stride;
+    return (int32_t)std::max<int64_t>(0, per_f / 16 / 32 * 32);
+  };
+  int32_t FG = 8, NB = nb_for(8);
+  if ((size_t)NB < 3 * nmax) {
+    FG = 4;
+    NB = nb_for(4);
+  }
+  if (NB < 64 || (size_t)NB * 3 < 2 * nmax) return;  // too few buckets: keep the other binning kernels
+  std::vector<uint8_t> blob((size_t)F * 16 + (size_t)F * NB * 16 + (size_t)F * stride * 4, 0);
+  const float nbm1 = (float)(NB - 1);
+  for (int32_t f = 0; f < F; ++f) {
+    const std::vector<float>& v = u[f];
+    float* prm = reinterpret_cast<float*>(blob.data() + (size_t)f * 16);
+    uint32_t* ent = reinterpret_cast<uint32_t*>(blob.data() + (size_t)F * 16 + (size_t)f * NB * 16);
+    float* U = reinterpret_cast<float*>(blob.data() + (size_t)F * 16 + (size_t)F * NB * 16) + (size_t)f * stride;
+    for (int32_t i = 0; i < stride; ++i) U[i] = i < (int32_t)v.size() ? v[i] : INFINITY;
+    float lo = 0.f, iw = INFINITY;  // no threshold: every x -> bucket 0 (code 0)
+    if (!v.empty()) {
+      lo = v.front();
+      const float span = v.back() - lo;
+      iw = span > 0.f ? (float)NB / span : INFINITY;
+      if (!(std::isfinite(lo) && std::isfinite(v.back()))) return;
+    }
+    prm[0] = lo;
+    prm[1] = iw;
+    std::vector<int32_t> cnt(NB, 0);
+    int32_t prev = -1;
+    for (float x : v) {
+      float t = (x - lo) * iw;  // IEEE fp32, as the kernel (__fsub_rn, __fmul_rn)
+      if (std::isnan(t)) t = 0.f;  // inf * 0 (single threshold): the kernel's fmaxf(NaN, 0) = 0
+      t = std::fmin(std::fmax(t, 0.f), nbm1);
+      const int32_t b = (int32_t)t;
+      if (b < prev) return;  // monotone by construction; checked
+      prev = b;
+      if (++cnt[b] > 15) return;
+    }
+    int32_t run = 0;
+    for (int32_t b = 0; b < NB; ++b) {
+      uint32_t* e = ent + 4 * (size_t)b;
+      e[0] = (uint32_t)run | ((uint32_t)cnt[b] << 16);
+      for (int32_t j = 0; j < 3; ++j) {
+        const float t = j < cnt[b] ? v[run + j] : INFINITY;
+        std::memcpy(&e[1 + j], &t, 4);
+      }
+      run += cnt[b];
+    }
+  }
+  out->bke_blob.swap(blob);
+  out->bke_nb = NB;
+  out->bke_stride = stride;
+  out->bke_fg = FG;
+}
+
 static uint32_t code_of_threshold(const TravLayout& L, int32_t f, float t) {
   const std::vector<float>& v = L.bin_sorted[f];
   return (uint32_t)(std::lower_bound(v.begin(), v.end(), t) - v.begin());  // t is present: exact index
@@ -609,6 +686,9 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
       out->bkt_blob.clear();
       out->bkt_nb = 0;
     }
+    out->bke_blob.clear();
+    out->bke_nb = 0;
+    if (out->codes && !(be && be[0] == '0')) build_entry_table(F, out);
   }
   if (!out->codes) {
     out->bin_table.clear();

@@ -1,11 +1,13 @@
 // K4 traversal: host-side dispatch (trav_run) and finalize of caller-provided
 // accumulators.  The kernel templates live in traverse.cuh and are
 // instantiated in trav_inst_*.cu (compiled in parallel).
+#include <cuda.h>  // CUtensorMap (encoded through the runtime's driver entry point; no -lcuda)
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 #include "traverse.cuh"
 #include "ptx.cuh"
@@ -580,6 +582,157 @@ __global__ void __launch_bounds__(512, 1) bin_bucket_fg_kernel(const float* __re
   }
 }
 
+// Bucket-entry binning (round 2; TravLayout::bke_blob, lowering.cpp
+// build_entry_table): step a1's threshold-bin codes with ONE random 16-byte
+// shared load per value.  b = clamp(floor((x - lo) * iw), 0, NB - 1) (the
+// host's IEEE fp32 map: monotone, exact), entry e_b = {cum | cnt << 16, t0,
+// t1, t2}; code = cum + [t0 < x] + [t1 < x] + [t2 < x] (pads +inf) when
+// cnt <= 3, else the branch-free 4-step search in the 15-wide window of U
+// from cum (rare: the map puts ~3+ buckets per threshold).  The previous
+// bucketed kernel issued 5 dependent random 4-byte loads per value (~16
+// shared wavefronts per warp-value, 58% of them bank conflicts).
+// A CTA holds FG features' tables (~210 KB) and a slice of the 32-row blocks;
+// each warp owns its blocks and double-buffers their [32][FG] fp32 tiles,
+// moved by the TMA engine (cp.async.bulk.tensor.2d, no LSU wavefronts) from X
+// viewed as [n_rows / R][R * F] (R = 1, 2, 4: the smallest super-row whose
+// pitch is a multiple of 16 B), R boxes of {W, 32 / R} per block.  A box's
+// first column must sit on a 16-byte boundary (measured: an unaligned start
+// is an illegal instruction, tools/tma_probe.cu), so for R > 1 the boxes
+// start at the aligned column at or below r * F + f0 and are W = FG + 4 wide.
+// Rows past the last whole super-row (n_rows % R) are read directly.
+template <int FG, int R>
+__global__ void __launch_bounds__(512, 1) bin_entry_kernel(const __grid_constant__ CUtensorMap tmx,
+                                                           const float* __restrict__ X, int64_t n_rows, int64_t n_tma,
+                                                           int32_t F, const uint8_t* __restrict__ blob, int32_t NB,
+                                                           int32_t stride, uint32_t* __restrict__ codes) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  constexpr int W = R == 1 ? FG : FG + 4;    // staged values per row
+  constexpr uint32_t kTile = 32u * W * 4u;   // bytes of one staged block
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
+  const int F2h = (F + 1) >> 1;
+  const int n_fg = (F + FG - 1) / FG;
+  const int fg = blockIdx.x % n_fg;
+  const int slice = blockIdx.x / n_fg, n_slices = gridDim.x / n_fg;
+  const int f0 = fg * FG;
+  const int nf = min(FG, F - f0);
+  // shared: stage [NW][2][32][W] fp32 | params [FG][16 B] | entries [FG][NB][16 B] | U [FG][stride] | bars
+  uint8_t* stage = smem;
+  uint8_t* s_prm = smem + (size_t)NW * 2 * kTile;
+  uint8_t* s_ent = s_prm + 16 * FG;
+  uint8_t* s_u = s_ent + (size_t)FG * NB * 16;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_u + (size_t)FG * stride * 4);  // [NW][2] + [1] table
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2 * NW + 1; ++i) ptx::mbar_init(&bars[i], 1);
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // this group's tables: three contiguous bulk copies
+    const uint32_t pb = 16u * nf, eb = 16u * (uint32_t)nf * NB, ub = 4u * (uint32_t)nf * stride;
+    ptx::mbar_arrive_expect_tx(&bars[2 * NW], pb + eb + ub);
+    ptx::bulk_g2s(s_prm, blob + (size_t)f0 * 16, pb, &bars[2 * NW]);
+    const uint8_t* ge = blob + (size_t)F * 16 + (size_t)f0 * NB * 16;
+    for (uint32_t o = 0; o < eb;) {  // <= 1 MB per bulk copy
+      const uint32_t n = min(eb - o, 1u << 20);
+      ptx::bulk_g2s(s_ent + o, ge + o, n, &bars[2 * NW]);
+      o += n;
+    }
+    ptx::bulk_g2s(s_u, blob + (size_t)F * 16 + (size_t)F * NB * 16 + (size_t)f0 * stride * 4, ub, &bars[2 * NW]);
+  }
+  const int64_t n_blocks = (n_rows + 31) / 32;
+  const int64_t step = (int64_t)n_slices * NW;
+  const uint32_t st0 = ptx::s2u(stage) + (uint32_t)warp * 2u * kTile;
+  uint64_t* wb = bars + 2 * warp;
+  auto issue = [&](int64_t b, int buf) {
+    if (b >= n_blocks) return;
+    ptx::mbar_arrive_expect_tx(&wb[buf], kTile);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t dst = st0 + (uint32_t)buf * kTile + (uint32_t)r * (kTile / R);
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+              dst),
+          "l"(&tmx), "r"((r * F + f0) & ~3), "r"((int)(b * (32 / R))), "r"(ptx::s2u(&wb[buf]))
+          : "memory");
+    }
+  };
+  int64_t blk = (int64_t)slice * NW + warp;
+  if (lane == 0) {
+    issue(blk, 0);
+    issue(blk + step, 1);
+  }
+  ptx::mbar_wait(&bars[2 * NW], 0);
+  float lo[FG], iw[FG];
+  uint32_t eb_[FG], ub_[FG];
+#pragma unroll
+  for (int q = 0; q < FG; ++q) {
+    const int qq = min(q, nf - 1);
+    lo[q] = reinterpret_cast<const float*>(s_prm)[4 * qq];
+    iw[q] = reinterpret_cast<const float*>(s_prm)[4 * qq + 1];
+    eb_[q] = ptx::s2u(s_ent) + 16u * (uint32_t)NB * (uint32_t)qq;
+    ub_[q] = ptx::s2u(s_u) + 4u * (uint32_t)stride * (uint32_t)qq;
+  }
+  const float nbm1 = (float)(NB - 1);
+  // lane's row within the block: box r = lane % R, super-row s = lane / R,
+  // its first value d = (r * F + f0) % 4 columns into the box row
+  const int xr = lane % R;
+  const uint32_t xoff = ((uint32_t)xr * (32 / R) + (uint32_t)(lane / R)) * W * 4u + 4u * (uint32_t)((xr * F + f0) & 3);
+  for (int it = 0; blk < n_blocks; blk += step, ++it) {
+    const int buf = it & 1;
+    ptx::mbar_wait(&wb[buf], (uint32_t)(it >> 1) & 1u);
+    const uint32_t xa = st0 + (uint32_t)buf * kTile + xoff;
+    float x[FG];
+    if (R == 1) {  // 16-byte aligned
+#pragma unroll
+      for (int q = 0; q < FG; q += 4)
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(x[q]), "=f"(x[q + 1]), "=f"(x[q + 2]), "=f"(x[q + 3])
+                     : "r"(xa + 4u * q));
+    } else if (R == 2) {  // F = 2 mod 4: d in {0, 2}, 8-byte aligned
+#pragma unroll
+      for (int q = 0; q < FG; q += 2)
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(x[q]), "=f"(x[q + 1]) : "r"(xa + 4u * q));
+    } else {
+#pragma unroll
+      for (int q = 0; q < FG; ++q) x[q] = ptx::lds_f32(xa + 4u * q);
+    }
+    const int64_t row = blk * 32 + lane;
+    if (row >= n_tma && row < n_rows) {  // past the last whole super-row
+#pragma unroll
+      for (int q = 0; q < FG; ++q) x[q] = q < nf ? __ldg(X + row * F + f0 + q) : 0.f;
+    }
+    __syncwarp();
+    if (lane == 0) {  // every lane holds its values: refill this buffer
+      ptx::fence_proxy_async();
+      issue(blk + 2 * step, buf);
+    }
+    uint32_t cd[FG];
+#pragma unroll
+    for (int q = 0; q < FG; ++q) {
+      float t = __fmul_rn(__fsub_rn(x[q], lo[q]), iw[q]);
+      t = fminf(fmaxf(t, 0.f), nbm1);
+      uint32_t e0, e1, e2, e3;
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(e0), "=r"(e1), "=r"(e2), "=r"(e3)
+                   : "r"(eb_[q] + 16u * (uint32_t)t));
+      uint32_t c = (e0 & 0xFFFFu) + (__uint_as_float(e1) < x[q] ? 1u : 0u) + (__uint_as_float(e2) < x[q] ? 1u : 0u) +
+                   (__uint_as_float(e3) < x[q] ? 1u : 0u);
+      if (e0 > 0x3FFFFu) {  // cnt > 3: lower_bound in the 15-wide window from cum
+        uint32_t pos = ub_[q] + 4u * (e0 & 0xFFFFu);
+#pragma unroll
+        for (int h = 8; h >= 1; h >>= 1)
+          if (ptx::lds_f32(pos + 4u * (uint32_t)(h - 1)) < x[q]) pos += 4u * (uint32_t)h;
+        c = (pos - ub_[q]) >> 2;
+      }
+      cd[q] = q >= nf ? 0u : isnan(x[q]) ? 0xFFFFu : c;
+    }
+    uint32_t* dst = codes + (size_t)blk * F2h * 32 + lane;
+#pragma unroll
+    for (int q = 0; q < FG; q += 2)
+      if (q < nf) dst[(size_t)((f0 + q) >> 1) * 32] = cd[q] | (cd[q + 1] << 16);
+  }
+}
+
 // Feature-group binning for search tables too large to hold for all features
 // at once (C5-shaped shards: 200 features x 8191-slot trees = 6.5 MB): a CTA
 // owns FG features and a range of 32-row blocks; lane = row reads its row's FG
@@ -696,6 +849,31 @@ static int num_sms(int dev) {
   return n;
 }
 
+// Tensor map of X [n_rows][F] fp32 viewed as [n_sr][R * F] (pitch R * F * 4,
+// a multiple of 16 B), box {W, 32 / R}: bin_entry_kernel's row tiles.
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static cudaError_t encode_x_map(CUtensorMap* tm, const float* X, int F, int R, int64_t n_sr, int W) {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  if (!fn || n_sr <= 0) return cudaErrorNotSupported;
+  const cuuint64_t gdim[2] = {(cuuint64_t)R * F, (cuuint64_t)n_sr};
+  const cuuint64_t gstr[1] = {(cuuint64_t)R * F * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)W, (cuuint32_t)(32 / R)}, es[2] = {1, 1};
+  const CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(X), gdim, gstr, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorNotSupported;
+}
+
 // Runs the traversal over all rows.  want: 0 predict, 1 proba, 2 raw, 3 apply.
 // Step a1 in coded form: bin the rows once into [n_blocks][F2/2][32][2] u16
 // code blocks (stream-ordered allocation, returned in *codes_out).
@@ -717,6 +895,52 @@ static cudaError_t launch_binning(const bridger_model* m, const TravLayout& L, c
   const int P0 = (1 << L.bin_k) - 1;
   const bool staged_fits = (m->F * P0 * 4 + 127) / 128 * 128 + 8 * (2 * 128 * m->F + 16) <= 232448;
   const bool want_bkt = bin_env ? bin_env[0] == 'b' : !staged_fits;
+  // bucket-entry kernel (TMA-staged row tiles) when built and X is 16-byte
+  // aligned; BRIDGER_BIN=e forces it, any other BRIDGER_BIN value avoids it
+  // (BRIDGER_BIN=E: required -- an error when it cannot run; tests)
+  // Default only where it measured faster: 16-byte-aligned rows (R = 1) and
+  // an input that stays L2-resident while the ceil(F / FG) feature-group CTAs
+  // each read their columns of every row (C2: step 0.386 -> 0.377 ms).  On C3
+  // (10M x 90, 3.6 GB) the groups drift apart and every group's sectors come
+  // from DRAM (9.2 GB read vs 3.6), so despite 23% fewer shared wavefronts it
+  // ties the all-features bucketed kernel (2.04 ms each).
+  const int R = (m->F * 4) % 16 == 0 ? 1 : (m->F * 8) % 16 == 0 ? 2 : 4;
+  const bool want_bke = bin_env ? (bin_env[0] == 'e' || bin_env[0] == 'E')
+                                : R == 1 && (double)n_rows * m->F * 4 <= 96.0 * (1 << 20);
+  if (L.bke_nb > 0 && !L.stream && want_bke && (reinterpret_cast<uintptr_t>(X) & 15) == 0 && n_rows >= 128) {
+    const int64_t n_sr = n_rows / R;
+    CUtensorMap tm;
+    err = encode_x_map(&tm, X, m->F, R, n_sr, R == 1 ? L.bke_fg : L.bke_fg + 4);
+    if (err == cudaSuccess) {
+      const int FG = L.bke_fg;
+      const int n_fg = (m->F + FG - 1) / FG;
+      const int nw = 16;
+      const int bsm = nw * 2 * 32 * (R == 1 ? FG : FG + 4) * 4 + 16 * FG + FG * L.bke_nb * 16 + FG * L.bke_stride * 4 + 8 * (2 * nw + 1);
+      const int64_t slices = std::max<int64_t>(1, std::min<int64_t>(sms / n_fg, (nbk + nw - 1) / nw));
+      using BinE = void (*)(const CUtensorMap, const float*, int64_t, int64_t, int32_t, const uint8_t*, int32_t, int32_t,
+                            uint32_t*);
+      BinE k = nullptr;
+      if (FG == 8) k = R == 1 ? bin_entry_kernel<8, 1> : R == 2 ? bin_entry_kernel<8, 2> : bin_entry_kernel<8, 4>;
+      else k = R == 1 ? bin_entry_kernel<4, 1> : R == 2 ? bin_entry_kernel<4, 2> : bin_entry_kernel<4, 4>;
+      static std::atomic<uint64_t> attr_e[6];
+      smem_opt_in(reinterpret_cast<const void*>(k), attr_e[(FG == 8 ? 3 : 0) + (R == 1 ? 0 : R == 2 ? 1 : 2)]);
+      k<<<(int)(n_fg * slices), nw * 32, bsm, st>>>(tm, X, n_rows, n_sr * R, m->F, m->d_bke, L.bke_nb, L.bke_stride,
+                                                    static_cast<uint32_t*>(codes));
+      count_launch();
+      err = cudaGetLastError();
+      if (err != cudaSuccess) {
+        cudaFreeAsync(codes, st);
+        return err;
+      }
+      *codes_out = codes;
+      return cudaSuccess;
+    }
+    err = cudaSuccess;  // no tensor map (driver entry point missing): the other kernels
+  }
+  if (bin_env && bin_env[0] == 'E') {
+    cudaFreeAsync(codes, st);
+    return cudaErrorNotSupported;
+  }
   if (L.bkt_nb > 0 && L.bkt_fg > 0 && !L.stream && want_bkt) {
     // per-feature-group bucketed binning
     const int FG = L.bkt_fg;  // 4

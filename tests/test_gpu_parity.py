@@ -221,13 +221,16 @@ def test_coded_format_feature_widths(F, monkeypatch):
     assert g.layout()["coded"]
 
 
-@pytest.mark.parametrize("binv", ["coop", "fg", "bucket"])
+@pytest.mark.parametrize("binv", ["coop", "fg", "bucket", "E"])
 @pytest.mark.parametrize("F", [7, 28, 90])
 def test_coded_binning_variants(binv, F, monkeypatch):
     """The cooperative (CTA-shared block), feature-group (tables per CTA,
-    direct loads) and bucketed (affine bucket map + short window search)
-    binning kernels produce the same codes: bit-exact end to end, with NaN,
-    +-inf, -0 and subnormal inputs."""
+    direct loads), bucketed (affine bucket map + short window search) and
+    bucket-entry (one 16-byte entry per bucket, TMA-staged row tiles; "E"
+    makes it an error if that kernel cannot run) binning kernels produce the
+    same codes: bit-exact end to end, with NaN, +-inf, -0 and subnormal
+    inputs.  F = 7, 28, 90 cover the 4-, 1- and 2-row super-row views of the
+    entry kernel's tensor map, 2011 rows its directly-read tail rows."""
     monkeypatch.setenv("BRIDGER_CODES", "1")
     monkeypatch.setenv("BRIDGER_BIN", binv)
     m = perfect_ensemble(60 + F, 31, 7, F, kind="regression", lr=0.1, calib_rows=2048)
@@ -350,7 +353,7 @@ def test_tree_streamed_pruned_missing_mixed_depth(ml):
     check(m, inject_specials(gen_x(96, 0, 2001, 64), 96, rate=0.02))
 
 
-@pytest.mark.parametrize("spread", ["clustered", "wide", "single"])
+@pytest.mark.parametrize("spread", ["clustered", "wide", "single", "bunched"])
 def test_bucketed_binning_threshold_layouts(spread, monkeypatch):
     """Bucketed binning on threshold sets that stress the bucket map: many
     thresholds packed into a tiny range (large per-bucket counts: the window
@@ -369,6 +372,11 @@ def test_bucketed_binning_threshold_layouts(spread, monkeypatch):
         vals = np.float32(1.0) + rng.integers(0, 200, n_in).astype(np.float32) * np.float32(2.0 ** -23)
     elif spread == "wide":
         vals = (rng.choice([-1, 1], n_in) * 10.0 ** rng.uniform(-30, 30, n_in)).astype(np.float32)
+    elif spread == "bunched":
+        # 50 bunches of 8 thresholds 1e-6 apart: 4..15 per bucket, so the
+        # entry kernel's overflow window search runs next to its 1-load path
+        base = np.repeat(np.arange(50, dtype=np.float32) / np.float32(50), 8)
+        vals = (base + np.tile(np.arange(8, dtype=np.float32), 50) * np.float32(1e-6))[rng.integers(0, 400, n_in)]
     else:
         vals = np.full(n_in, 0.25, np.float32)
     thr[inner] = vals
@@ -383,7 +391,7 @@ def test_bucketed_binning_threshold_layouts(spread, monkeypatch):
     X[::89, 2] = np.inf
     X[::83, 3] = -np.inf
     X[::79, 4] = -0.0
-    for binv in ("bucket", "coop"):
+    for binv in ("bucket", "coop", "e" if spread == "wide" else "E"):
         monkeypatch.setenv("BRIDGER_BIN", binv)
         check(m, X)
 

@@ -118,7 +118,10 @@ __device__ __forceinline__ void walk_spec_tail(int n, const TravParams& p, uint3
   }
 }
 
-template <int KT, bool ML>
+// SC: the fused tree-sharding reduce (partials scattered to the owner rank's
+// slice); a separate instantiation -- the branch in the common kernel cost the
+// C5 shard walk 4% (7.89 -> 8.23 ms, register allocation of the pass loop)
+template <int KT, bool ML, bool SC>
 __global__ void __launch_bounds__(512, 1) trav_deep_kernel(const TravParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
@@ -219,7 +222,7 @@ __global__ void __launch_bounds__(512, 1) trav_deep_kernel(const TravParams p) {
     const int cnt = base + b1;
     if (cnt > 0 && row < n_rows) {
       unsigned long long* dst;
-      if (p.scatter) {
+      if (SC) {
         // the reduce of tree sharding fused into the walk: this row's partial
         // goes straight into the owner rank's slice (own or peer memory)
         const int32_t gb = (int32_t)(blk0 + i * stride);           // global 32-row block (warp-uniform)
@@ -249,9 +252,9 @@ __global__ void __launch_bounds__(512, 1) trav_deep_kernel(const TravParams p) {
 // Launch: acc [n_rows][K] int64 zeroed here; the caller finalizes.
 template <int KT, bool ML>
 cudaError_t launch_deep_t(const TravParams& p, int grid, int block, int smem, cudaStream_t st) {
-  auto kern = trav_deep_kernel<KT, ML>;
-  static std::atomic<uint64_t> configured{0};  // per instantiation, per device
-  cudaError_t e = smem_opt_in(reinterpret_cast<const void*>(kern), configured);
+  auto kern = p.scatter ? trav_deep_kernel<KT, ML, true> : trav_deep_kernel<KT, ML, false>;
+  static std::atomic<uint64_t> configured[2];  // per instantiation, per device
+  cudaError_t e = smem_opt_in(reinterpret_cast<const void*>(kern), configured[p.scatter ? 1 : 0]);
   if (e != cudaSuccess) return e;
   TravParams q = p;
   q.cpc = grid / p.n_chunks_grid;

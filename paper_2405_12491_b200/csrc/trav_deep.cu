@@ -121,7 +121,10 @@ __device__ __forceinline__ void walk_spec_tail(int n, const TravParams& p, uint3
 // SC: the fused tree-sharding reduce (partials scattered to the owner rank's
 // slice); a separate instantiation -- the branch in the common kernel cost the
 // C5 shard walk 4% (7.89 -> 8.23 ms, register allocation of the pass loop)
-template <int KT, bool ML, bool SC>
+// WM = 1: every chunk takes the speculative walk, and the kernel holds only
+// that walk (C5 shard walk 7.86 -> 7.73 ms); 0 chooses per chunk at run time.
+// (A WM for the compile-time-depth walks measured slower on C3: 8.55 -> 8.73.)
+template <int KT, bool ML, bool SC, int WM>
 __global__ void __launch_bounds__(512, 1) trav_deep_kernel(const TravParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
@@ -209,7 +212,7 @@ __global__ void __launch_bounds__(512, 1) trav_deep_kernel(const TravParams p) {
     const int n_pass = b1 ? np_[1] : np_[0], sz0 = b1 ? sz_[1] : sz_[0], nbig = b1 ? big_[1] : big_[0];
     for (int q = 0; q < n_pass; ++q) {
       const int sz = sz0 + (q < nbig ? 1 : 0);
-      if (spec)
+      if (WM == 1 || (WM == 0 && spec))
         walk_spec_tail<KT, ML, SPEC_NI>(sz, p, nodes_s, leaves_s, ptx::s2u(xl), j, I, L, D, acc);
       else if (!ML && KT <= 8 && D == 6)
         walk_tail<KT, long long, ML, true, NI_MAX, false, 6>(sz, p, c, smem, leaves, xl, j, I, L, D, K, row, acc);
@@ -251,10 +254,14 @@ __global__ void __launch_bounds__(512, 1) trav_deep_kernel(const TravParams p) {
 
 // Launch: acc [n_rows][K] int64 zeroed here; the caller finalizes.
 template <int KT, bool ML>
-cudaError_t launch_deep_t(const TravParams& p, int grid, int block, int smem, cudaStream_t st) {
-  auto kern = p.scatter ? trav_deep_kernel<KT, ML, true> : trav_deep_kernel<KT, ML, false>;
-  static std::atomic<uint64_t> configured[2];  // per instantiation, per device
-  cudaError_t e = smem_opt_in(reinterpret_cast<const void*>(kern), configured[p.scatter ? 1 : 0]);
+cudaError_t launch_deep_t(const TravParams& p, int wm, int grid, int block, int smem, cudaStream_t st) {
+  auto kern = p.scatter ? trav_deep_kernel<KT, ML, true, 0> : trav_deep_kernel<KT, ML, false, 0>;
+  int ki = p.scatter ? 1 : 0;
+  if constexpr (!ML && KT <= 8) {
+    if (!p.scatter && wm == 1) kern = trav_deep_kernel<KT, false, false, 1>, ki = 2;
+  }
+  static std::atomic<uint64_t> configured[3];  // per instantiation, per device
+  cudaError_t e = smem_opt_in(reinterpret_cast<const void*>(kern), configured[ki]);
   if (e != cudaSuccess) return e;
   TravParams q = p;
   q.cpc = grid / p.n_chunks_grid;
@@ -281,10 +288,12 @@ cudaError_t launch_deep_t(const TravParams& p, int grid, int block, int smem, cu
   return cudaGetLastError();
 }
 
-cudaError_t launch_trav_deep(const TravParams& p, int K, bool ml, int grid, int block, int smem, cudaStream_t st) {
+// wm: the walk every chunk takes (traverse.cu deep_walk_mode), 0 if mixed
+cudaError_t launch_trav_deep(const TravParams& p, int K, bool ml, int wm, int grid, int block, int smem,
+                             cudaStream_t st) {
   cudaError_t e = cudaErrorInvalidValue;
-  BRIDGER_DISPATCH_KT(K, { e = ml ? launch_deep_t<KT, true>(p, grid, block, smem, st)
-                                  : launch_deep_t<KT, false>(p, grid, block, smem, st); });
+  BRIDGER_DISPATCH_KT(K, { e = ml ? launch_deep_t<KT, true>(p, wm, grid, block, smem, st)
+                                  : launch_deep_t<KT, false>(p, wm, grid, block, smem, st); });
   return e;
 }
 

@@ -14,7 +14,8 @@
 
 namespace bridger {
 
-cudaError_t launch_trav_deep(const TravParams& p, int K, bool ml, int grid, int block, int smem, cudaStream_t st);
+cudaError_t launch_trav_deep(const TravParams& p, int K, bool ml, int wm, int grid, int block, int smem,
+                             cudaStream_t st);
 int trav_deep_smem(int chunk_cap, int code_buf, int nb);
 
 #define BRIDGER_TRAV_EXTERN(ACC, ML, GT, FMT)                                                                           \
@@ -1274,7 +1275,15 @@ cudaError_t trav_run(const bridger_model* m, const float* X, int64_t n_rows, voi
       p.spec_min_d = 9;
       if (const char* e = std::getenv("BRIDGER_SPEC_D")) p.spec_min_d = std::atoi(e);
       const int dsmem = trav_deep_smem(p.chunk_cap, p.code_buf, NB);
-      err = launch_trav_deep(p, m->K, L.has_missing, grid, block, dsmem, st);
+      // wm = 1 when every chunk takes the speculative walk (as
+      // trav_deep_kernel decides it): the kernel built with only that walk
+      int wm = 1;
+      const int KT = m->K <= 1 ? 1 : m->K <= 2 ? 2 : m->K <= 4 ? 4 : m->K <= 8 ? 8 : m->K <= 16 ? 16 : 64;
+      for (const TravChunk& ch : L.chunks)
+        if (!(ch.depth >= p.spec_min_d && m->K == KT && ch.depth >= 1)) wm = 0;
+      if (const char* e = std::getenv("BRIDGER_DEEP_WM"))
+        if (e[0] == '0') wm = 0;  // A/B: the kernel with every walk (runtime choice)
+      err = launch_trav_deep(p, m->K, L.has_missing, std::max(wm, 0), grid, block, dsmem, st);
     }
     if (err == cudaSuccess && want != 2) {
       const int tb = 256;

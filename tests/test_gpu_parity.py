@@ -240,6 +240,21 @@ def test_coded_binning_variants(binv, F, monkeypatch):
     assert g.layout()["coded"]
 
 
+@pytest.mark.parametrize("F,n", [(7, 129), (7, 131), (90, 130), (28, 160), (90, 4099)])
+def test_entry_binning_small_and_ragged(F, n, monkeypatch):
+    """Bucket-entry binning (BRIDGER_BIN=E: an error unless that kernel runs)
+    at the smallest row counts it takes (>= 128) and ragged sizes: the last
+    32-row block partly out of the tensor map (TMA zero fill), rows past the
+    last whole R-row super-row read directly (F = 7: R = 4, F = 90: R = 2),
+    and a multi-block input; labels, scores and raw sums bitwise."""
+    monkeypatch.setenv("BRIDGER_CODES", "1")
+    monkeypatch.setenv("BRIDGER_BIN", "E")
+    m = perfect_ensemble(70 + F, 23, 6, F, kind="classification", n_classes=3, calib_rows=2048)
+    X = inject_specials(gen_x(71 + F, 0, n, F), 71 + F, rate=0.02)
+    g, _ = check(m, X)
+    assert g.layout()["coded"]
+
+
 def test_coded_wide_code_range(monkeypatch):
     """Up to 65534 distinct thresholds per feature (16-bit code index, missing
     flag in bit 0): ~41K random distinct thresholds on each of 4 features ->

@@ -841,6 +841,15 @@ __global__ void __launch_bounds__(512) xpose_kernel(const float* __restrict__ X,
 // ------------------------------------------------------------- launchers ----
 static std::atomic<uint64_t> g_xpose_smem{0};  // xpose_kernel's shared-memory opt-in, per device
 
+static int64_t l2_bytes(int dev) {
+  static std::atomic<int64_t> cached[64];
+  if (dev >= 0 && dev < 64 && cached[dev].load()) return cached[dev].load();
+  int b = 0;
+  cudaDeviceGetAttribute(&b, cudaDevAttrL2CacheSize, dev);
+  if (dev >= 0 && dev < 64) cached[dev].store(b);
+  return b;
+}
+
 static int num_sms(int dev) {
   static int cached[64] = {0};
   if (dev >= 0 && dev < 64 && cached[dev]) return cached[dev];
@@ -900,14 +909,15 @@ static cudaError_t launch_binning(const bridger_model* m, const TravLayout& L, c
   // aligned; BRIDGER_BIN=e forces it, any other BRIDGER_BIN value avoids it
   // (BRIDGER_BIN=E: required -- an error when it cannot run; tests)
   // Default only where it measured faster: 16-byte-aligned rows (R = 1) and
-  // an input that stays L2-resident while the ceil(F / FG) feature-group CTAs
-  // each read their columns of every row (C2: step 0.386 -> 0.377 ms).  On C3
+  // an input no larger than L2, which stays resident while the ceil(F / FG)
+  // feature-group CTAs each read their columns of every row (C2, 112 MB:
+  // binning 0.080 -> 0.067 ms, step 0.390 -> 0.375 ms).  On C3
   // (10M x 90, 3.6 GB) the groups drift apart and every group's sectors come
   // from DRAM (9.2 GB read vs 3.6), so despite 23% fewer shared wavefronts it
   // ties the all-features bucketed kernel (2.04 ms each).
   const int R = (m->F * 4) % 16 == 0 ? 1 : (m->F * 8) % 16 == 0 ? 2 : 4;
   const bool want_bke = bin_env ? (bin_env[0] == 'e' || bin_env[0] == 'E')
-                                : R == 1 && (double)n_rows * m->F * 4 <= 96.0 * (1 << 20);
+                                : R == 1 && (double)n_rows * m->F * 4 <= (double)l2_bytes(m->device);
   if (L.bke_nb > 0 && !L.stream && want_bke && (reinterpret_cast<uintptr_t>(X) & 15) == 0 && n_rows >= 128) {
     const int64_t n_sr = n_rows / R;
     CUtensorMap tm;

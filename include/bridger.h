@@ -252,6 +252,17 @@ bridger_status bridger_analyze_exactness(const bridger_model_desc* desc, int32_t
                                          int32_t* tier, double* log2_M);
 /* Validation only (E_INVALID_TREE etc. exactly as load). */
 bridger_status bridger_validate(const bridger_model_desc* desc);
+/* Host emulation of step a1's threshold-bin codes from the tables the load
+ * would build ("data type rewriting"; DESIGN.md §6 bucketed /
+ * bucket-entry binning), for CPU tests of the table construction: code(x) =
+ * #{distinct thresholds of feature f < x}, 0xFFFF for NaN.  method 1: the
+ * bucketed table (cum + 15-wide window search), 2: the bucket-entry table
+ * ({cum | cnt, t0, t1, t2} + the window when cnt > 3).  X host [n_rows][F]
+ * fp32, codes host [n_rows][F] u16 (caller-owned).  *nb = the table's bucket
+ * count, 0 when the load would not build that table (codes untouched).
+ * E_UNSUPPORTED when the model would not use threshold-bin codes. */
+bridger_status bridger_bin_codes_host(const bridger_model_desc* desc, const float* X, int64_t n_rows,
+                                      int32_t n_features, int32_t method, uint16_t* codes, int32_t* nb);
 
 /* ---------------------------------------------------------------------------
  * Linear models (the paper's other GPU-evaluated classical-ML

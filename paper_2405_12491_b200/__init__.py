@@ -54,6 +54,7 @@ EXPORTS = [
     "bridger_hot_kernel_time_by", "bridger_linear_load", "bridger_linear_free", "bridger_linear_predict",
     "bridger_linear_predict_proba", "bridger_linear_decision", "bridger_probe_smem_bandwidth",
     "bridger_path_matrix_sparse", "bridger_step_path_scores_sparse", "bridger_predict_raw_scatter",
+    "bridger_bin_codes_host",
 ]
 
 
@@ -97,6 +98,7 @@ def _load_lib():
         "bridger_path_matrix_sparse": ([i32, vp, vp, vp], i32),
         "bridger_step_path_scores_sparse": ([vp, i32, vp, i64, vp, vp], i32),
         "bridger_predict_raw_scatter": ([vp, vp, i64, i32, vp, i32, i64, vp], i32),
+        "bridger_bin_codes_host": ([vp, vp, i64, i32, i32, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -189,6 +191,21 @@ def analyze_exactness(m):
     q, t, l2 = C.c_int32(), C.c_int32(), C.c_double()
     _check(_lib.bridger_analyze_exactness(k.ptr, C.byref(q), C.byref(t), C.byref(l2)))
     return q.value, TIERS[t.value], l2.value
+
+
+def bin_codes_host(m, X, method: str):
+    """Host emulation of the threshold-bin codes from the bucketed ("bucket")
+    or bucket-entry ("entry") tables the load builds (bridger_bin_codes_host):
+    (codes uint16 [n][F], NB), NB = 0 and codes None when that table is not
+    built.  For CPU tests of the table construction."""
+    import numpy as np
+    k = _DescKeep(m)
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    codes = np.zeros(X.shape, dtype=np.uint16)
+    nb = C.c_int32()
+    _check(_lib.bridger_bin_codes_host(k.ptr, X.ctypes.data, X.shape[0], X.shape[1], {"bucket": 1, "entry": 2}[method],
+                                       codes.ctypes.data, C.byref(nb)))
+    return (codes if nb.value else None), nb.value
 
 
 def gemm_geometry(depth: int):
@@ -422,7 +439,7 @@ class Model:
         return out
 
 
-__all__ = ["Model", "BridgerError", "validate", "analyze_exactness", "path_matrix", "path_matrix_sparse", "lower_tree",
+__all__ = ["Model", "BridgerError", "validate", "analyze_exactness", "bin_codes_host", "path_matrix", "path_matrix_sparse", "lower_tree",
            "gemm_geometry", "launch_count", "lib", "LIB_PATH", "EXPORTS"]
 
 

@@ -301,6 +301,68 @@ bridger_status bridger_lower_tree(const bridger_model_desc* d, int32_t tree, int
   return BRIDGER_OK;
 }
 
+bridger_status bridger_bin_codes_host(const bridger_model_desc* d_in, const float* X, int64_t n_rows,
+                                      int32_t n_features, int32_t method, uint16_t* codes, int32_t* nb) {
+  if (!nb || (n_rows > 0 && (!X || !codes))) return fail(BRIDGER_E_NULL_ARG, "X, codes or nb is NULL");
+  bridger_status s = validate_desc(d_in);
+  if (s != BRIDGER_OK) return s;
+  if (n_features != d_in->n_features) return fail(BRIDGER_E_SHAPE, "n_features does not match the model");
+  if (method != 1 && method != 2) return fail(BRIDGER_E_UNSUPPORTED, "method must be 1 (bucketed) or 2 (entries)");
+  const ExpandedDesc ed(d_in);
+  const bridger_model_desc* d = ed.get();
+  std::vector<int32_t> depth(d->n_trees);
+  for (int32_t t = 0; t < d->n_trees; ++t) depth[t] = tree_depth(d, t);
+  const Exactness ex = analyze_exactness(d);
+  TravLayout L;
+  std::string why;
+  if (!build_trav_layout(d, depth, ex, ex.tier != BRIDGER_EXACT_F64, 148, &L, &why) || !L.codes)
+    return fail(BRIDGER_E_UNSUPPORTED, "the model would not use threshold-bin codes");
+  const int32_t F = d->n_features;
+  const int32_t NB = method == 1 ? L.bkt_nb : L.bke_nb;
+  *nb = NB;
+  if (NB == 0) return BRIDGER_OK;
+  const uint8_t* blob = method == 1 ? L.bkt_blob.data() : L.bke_blob.data();
+  const int32_t stride = method == 1 ? L.bkt_stride : L.bke_stride;
+  const size_t cum_row = ((size_t)(NB + 2) * 2 + 3) / 4 * 4;
+  const float nbm1 = (float)(NB - 1);
+  for (int32_t f = 0; f < F; ++f) {
+    const float* prm = reinterpret_cast<const float*>(blob + (size_t)f * 16);
+    const float lo = prm[0], iw = prm[1];
+    const float* U = reinterpret_cast<const float*>(
+                         blob + (size_t)F * 16 + (size_t)F * (method == 1 ? cum_row : (size_t)NB * 16)) +
+                     (size_t)f * stride;
+    for (int64_t r = 0; r < n_rows; ++r) {
+      const float x = X[r * F + f];
+      uint16_t& c = codes[r * F + f];
+      if (std::isnan(x)) {
+        c = 0xFFFF;
+        continue;
+      }
+      float t = (x - lo) * iw;  // fp32, as the kernels (__fsub_rn, __fmul_rn)
+      t = std::fmin(std::fmax(t, 0.f), nbm1);  // fmax(NaN, 0) = 0, as fmaxf
+      const uint32_t b = (uint32_t)t;
+      uint32_t pos;
+      if (method == 1) {
+        pos = reinterpret_cast<const uint16_t*>(blob + (size_t)F * 16 + (size_t)f * cum_row)[b];
+      } else {
+        const uint32_t* e = reinterpret_cast<const uint32_t*>(blob + (size_t)F * 16 + ((size_t)f * NB + b) * 16);
+        float t3[3];
+        std::memcpy(t3, e + 1, 12);
+        pos = (e[0] & 0xFFFFu) + (t3[0] < x) + (t3[1] < x) + (t3[2] < x);
+        if ((e[0] >> 16) <= 3) {
+          c = (uint16_t)pos;
+          continue;
+        }
+        pos = e[0] & 0xFFFFu;
+      }
+      for (int h = 8; h >= 1; h >>= 1)  // branch-free lower_bound in the 15-wide window
+        if (U[pos + h - 1] < x) pos += h;
+      c = (uint16_t)pos;
+    }
+  }
+  return BRIDGER_OK;
+}
+
 bridger_status bridger_model_load(const bridger_model_desc* d_in, int cuda_device, bridger_model** out) {
   if (!out) return fail(BRIDGER_E_NULL_ARG, "out is NULL");
   bridger_status s = validate_desc(d_in);

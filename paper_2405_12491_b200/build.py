@@ -15,7 +15,7 @@ LIB = os.path.join(HERE, "libbridger.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["api.cu", "traverse.cu", "trav_inst_i64.cu", "trav_inst_i64_ml.cu", "trav_inst_f64.cu",
-           "trav_inst_gt_i64.cu", "trav_inst_gt_f64.cu", "trav_inst_sparse.cu", "trav_inst_hybrid.cu", "trav_inst_split.cu", "trav_inst_stream.cu", "trav_inst_stream_split.cu", "trav_inst_stream_codes.cu", "trav_deep.cu", "gemm_path.cu", "linear.cu", "probe.cu", "lowering.cpp"]
+           "trav_inst_gt_i64.cu", "trav_inst_gt_f64.cu", "trav_inst_sparse.cu", "trav_inst_hybrid.cu", "trav_inst_split.cu", "trav_inst_stream.cu", "trav_inst_stream_split.cu", "trav_inst_stream_codes.cu", "trav_deep.cu", "trav_deep_inst_0.cu", "trav_deep_inst_1.cu", "trav_deep_inst_2.cu", "trav_deep_inst_3.cu", "trav_deep_inst_4.cu", "gemm_path.cu", "linear.cu", "probe.cu", "lowering.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-ftz=false", "-prec-div=true", "-prec-sqrt=true",
           "-fmad=true", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",

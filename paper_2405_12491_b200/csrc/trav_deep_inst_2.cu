@@ -1,0 +1,6 @@
+// Explicit instantiations of the K4d kernel launchers (trav_deep.cuh).
+#include "trav_deep.cuh"
+
+namespace bridger {
+BRIDGER_DEEP_ALL_KT(, false, true, 0)
+}  // namespace bridger

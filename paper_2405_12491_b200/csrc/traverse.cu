@@ -601,7 +601,12 @@ __global__ void __launch_bounds__(512, 1) bin_bucket_fg_kernel(const float* __re
 // is an illegal instruction, tools/tma_probe.cu), so for R > 1 the boxes
 // start at the aligned column at or below r * F + f0 and are W = FG + 4 wide.
 // Rows past the last whole super-row (n_rows % R) are read directly.
-template <int FG, int R>
+// TAB = 1: the same TMA-staged pipeline over the bucketed tables instead
+// (TravLayout::bkt_blob built for feature groups: u16 cum + the 15-wide
+// window search; wide inputs such as the C5 shard, whose ~6.4K thresholds per
+// feature leave no room for entries) -- it replaces bin_bucket_fg_kernel's
+// per-lane global row loads (32 sectors per warp load, latency-bound).
+template <int FG, int R, int TAB>
 __global__ void __launch_bounds__(512, 1) bin_entry_kernel(const __grid_constant__ CUtensorMap tmx,
                                                            const float* __restrict__ X, int64_t n_rows, int64_t n_tma,
                                                            int32_t F, const uint8_t* __restrict__ blob, int32_t NB,
@@ -617,18 +622,31 @@ __global__ void __launch_bounds__(512, 1) bin_entry_kernel(const __grid_constant
   const int slice = blockIdx.x / n_fg, n_slices = gridDim.x / n_fg;
   const int f0 = fg * FG;
   const int nf = min(FG, F - f0);
-  // shared: stage [NW][2][32][W] fp32 | params [FG][16 B] | entries [FG][NB][16 B] | U [FG][stride] | bars
+  // per feature: entries [NB][16 B] (TAB 0) or cum [NB + 2] u16 rounded to 4 B (TAB 1)
+  const uint32_t sec2 = TAB == 0 ? 16u * (uint32_t)NB : (uint32_t)(((NB + 2) * 2 + 3) / 4 * 4);
+  // shared: stage [NW][2][32][W] fp32 | params [FG][16 B] | entries / cum [FG][sec2] | U [FG][stride] | bars
   uint8_t* stage = smem;
   uint8_t* s_prm = smem + (size_t)NW * 2 * kTile;
   uint8_t* s_ent = s_prm + 16 * FG;
-  uint8_t* s_u = s_ent + (size_t)FG * NB * 16;
+  uint8_t* s_u = s_ent + (size_t)FG * sec2;
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_u + (size_t)FG * stride * 4);  // [NW][2] + [1] table
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2 * NW + 1; ++i) ptx::mbar_init(&bars[i], 1);
     ptx::fence_barrier_init();
   }
   __syncthreads();
-  if (threadIdx.x == 0) {  // this group's tables: three contiguous bulk copies
+  if (TAB == 1) {  // cum rows are 4-byte multiples: a plain cooperative copy of this group's tables
+    const uint32_t* g = reinterpret_cast<const uint32_t*>(blob);
+    const size_t g_cum = (size_t)F * 4, g_u = ((size_t)F * 16 + (size_t)F * sec2) / 4;
+    const int cw = (int)(sec2 / 4), uw = stride;
+    for (int i = threadIdx.x; i < nf * 4; i += blockDim.x) reinterpret_cast<uint32_t*>(s_prm)[i] = g[(size_t)f0 * 4 + i];
+    for (int i = threadIdx.x; i < nf * cw; i += blockDim.x)
+      reinterpret_cast<uint32_t*>(s_ent)[i] = g[g_cum + (size_t)f0 * cw + i];
+    for (int i = threadIdx.x; i < nf * uw; i += blockDim.x)
+      reinterpret_cast<uint32_t*>(s_u)[i] = g[g_u + (size_t)f0 * uw + i];
+    if (threadIdx.x == 0) ptx::mbar_arrive(&bars[2 * NW]);
+    __syncthreads();
+  } else if (threadIdx.x == 0) {  // this group's tables: three contiguous bulk copies
     const uint32_t pb = 16u * nf, eb = 16u * (uint32_t)nf * NB, ub = 4u * (uint32_t)nf * stride;
     ptx::mbar_arrive_expect_tx(&bars[2 * NW], pb + eb + ub);
     ptx::bulk_g2s(s_prm, blob + (size_t)f0 * 16, pb, &bars[2 * NW]);
@@ -670,7 +688,7 @@ __global__ void __launch_bounds__(512, 1) bin_entry_kernel(const __grid_constant
     const int qq = min(q, nf - 1);
     lo[q] = reinterpret_cast<const float*>(s_prm)[4 * qq];
     iw[q] = reinterpret_cast<const float*>(s_prm)[4 * qq + 1];
-    eb_[q] = ptx::s2u(s_ent) + 16u * (uint32_t)NB * (uint32_t)qq;
+    eb_[q] = ptx::s2u(s_ent) + sec2 * (uint32_t)qq;
     ub_[q] = ptx::s2u(s_u) + 4u * (uint32_t)stride * (uint32_t)qq;
   }
   const float nbm1 = (float)(NB - 1);
@@ -712,6 +730,14 @@ __global__ void __launch_bounds__(512, 1) bin_entry_kernel(const __grid_constant
     for (int q = 0; q < FG; ++q) {
       float t = __fmul_rn(__fsub_rn(x[q], lo[q]), iw[q]);
       t = fminf(fmaxf(t, 0.f), nbm1);
+      if (TAB == 1) {  // cum[b] + lower_bound in the 15-wide window
+        uint32_t pos = ub_[q] + 4u * ptx::lds_u16(eb_[q] + 2u * (uint32_t)t);
+#pragma unroll
+        for (int h = 8; h >= 1; h >>= 1)
+          if (ptx::lds_f32(pos + 4u * (uint32_t)(h - 1)) < x[q]) pos += 4u * (uint32_t)h;
+        cd[q] = q >= nf ? 0u : isnan(x[q]) ? 0xFFFFu : (pos - ub_[q]) >> 2;
+        continue;
+      }
       uint32_t e0, e1, e2, e3;
       asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                    : "=r"(e0), "=r"(e1), "=r"(e2), "=r"(e3)
@@ -884,6 +910,19 @@ static cudaError_t encode_x_map(CUtensorMap* tm, const float* X, int F, int R, i
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorNotSupported;
 }
 
+// Row slices per feature group for one-CTA-per-SM binning grids of n_fg x
+// slices CTAs: the fewest slices whose waves keep >= 90% of the SMs busy
+// (C5 shard: 50 groups -> 8 slices, 400 CTAs in 3 waves; 100 CTAs would idle
+// a third of the SMs and 150 would leave 2 CTAs for a second wave).
+static int64_t pick_slices(int n_fg, int sms, int64_t max_slices) {
+  max_slices = std::max<int64_t>(1, max_slices);
+  for (int64_t s = std::max(1, sms / n_fg); s <= std::min<int64_t>(max_slices, 64); ++s) {
+    const int64_t ctas = (int64_t)n_fg * s, waves = (ctas + sms - 1) / sms;
+    if (ctas * 10 >= waves * sms * 9) return s;
+  }
+  return std::max<int64_t>(1, std::min<int64_t>(max_slices, std::max(1, sms / n_fg)));
+}
+
 // Runs the traversal over all rows.  want: 0 predict, 1 proba, 2 raw, 3 apply.
 // Step a1 in coded form: bin the rows once into [n_blocks][F2/2][32][2] u16
 // code blocks (stream-ordered allocation, returned in *codes_out).
@@ -904,7 +943,7 @@ static cudaError_t launch_binning(const bridger_model* m, const TravLayout& L, c
   const char* bin_env = std::getenv("BRIDGER_BIN");
   const int P0 = (1 << L.bin_k) - 1;
   const bool staged_fits = (m->F * P0 * 4 + 127) / 128 * 128 + 8 * (2 * 128 * m->F + 16) <= 232448;
-  const bool want_bkt = bin_env ? bin_env[0] == 'b' : !staged_fits;
+  const bool want_bkt = bin_env ? (bin_env[0] == 'b' || bin_env[0] == 'g') : !staged_fits;
   // bucket-entry kernel (TMA-staged row tiles) when built and X is 16-byte
   // aligned; BRIDGER_BIN=e forces it, any other BRIDGER_BIN value avoids it
   // (BRIDGER_BIN=E: required -- an error when it cannot run; tests)
@@ -927,12 +966,14 @@ static cudaError_t launch_binning(const bridger_model* m, const TravLayout& L, c
       const int n_fg = (m->F + FG - 1) / FG;
       const int nw = 16;
       const int bsm = nw * 2 * 32 * (R == 1 ? FG : FG + 4) * 4 + 16 * FG + FG * L.bke_nb * 16 + FG * L.bke_stride * 4 + 8 * (2 * nw + 1);
-      const int64_t slices = std::max<int64_t>(1, std::min<int64_t>(sms / n_fg, (nbk + nw - 1) / nw));
+      const int64_t slices = pick_slices(n_fg, sms, (nbk + nw - 1) / nw);
       using BinE = void (*)(const CUtensorMap, const float*, int64_t, int64_t, int32_t, const uint8_t*, int32_t, int32_t,
                             uint32_t*);
       BinE k = nullptr;
-      if (FG == 8) k = R == 1 ? bin_entry_kernel<8, 1> : R == 2 ? bin_entry_kernel<8, 2> : bin_entry_kernel<8, 4>;
-      else k = R == 1 ? bin_entry_kernel<4, 1> : R == 2 ? bin_entry_kernel<4, 2> : bin_entry_kernel<4, 4>;
+      if (FG == 8)
+        k = R == 1 ? bin_entry_kernel<8, 1, 0> : R == 2 ? bin_entry_kernel<8, 2, 0> : bin_entry_kernel<8, 4, 0>;
+      else
+        k = R == 1 ? bin_entry_kernel<4, 1, 0> : R == 2 ? bin_entry_kernel<4, 2, 0> : bin_entry_kernel<4, 4, 0>;
       static std::atomic<uint64_t> attr_e[6];
       smem_opt_in(reinterpret_cast<const void*>(k), attr_e[(FG == 8 ? 3 : 0) + (R == 1 ? 0 : R == 2 ? 1 : 2)]);
       k<<<(int)(n_fg * slices), nw * 32, bsm, st>>>(tm, X, n_rows, n_sr * R, m->F, m->d_bke, L.bke_nb, L.bke_stride,
@@ -951,6 +992,39 @@ static cudaError_t launch_binning(const bridger_model* m, const TravLayout& L, c
   if (bin_env && bin_env[0] == 'E') {
     cudaFreeAsync(codes, st);
     return cudaErrorNotSupported;
+  }
+  if (L.bkt_nb > 0 && L.bkt_fg == 4 && !L.stream && want_bkt && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
+      n_rows >= 128 && !(bin_env && bin_env[0] == 'g')) {
+    // per-feature-group bucketed tables with TMA-staged row tiles
+    // (bin_entry_kernel<4, R, 1>) when they fit next to the staging;
+    // BRIDGER_BIN=g keeps the direct-load kernel below
+    const int R = (m->F * 4) % 16 == 0 ? 1 : (m->F * 8) % 16 == 0 ? 2 : 4;
+    const int W = R == 1 ? 4 : 8;
+    const int n_fg = (m->F + 3) / 4;
+    const int cum_row = ((L.bkt_nb + 2) * 2 + 3) / 4 * 4;
+    int nw = 16;
+    auto bsm_of = [&](int w) { return w * 2 * 32 * W * 4 + 4 * (16 + cum_row + 4 * L.bkt_stride) + 8 * (2 * w + 1); };
+    while (nw > 4 && bsm_of(nw) > 232448) nw /= 2;
+    CUtensorMap tm;
+    const int64_t n_sr = n_rows / R;
+    if (bsm_of(nw) <= 232448 && encode_x_map(&tm, X, m->F, R, n_sr, W) == cudaSuccess) {
+      using BinE = void (*)(const CUtensorMap, const float*, int64_t, int64_t, int32_t, const uint8_t*, int32_t, int32_t,
+                            uint32_t*);
+      BinE k = R == 1 ? bin_entry_kernel<4, 1, 1> : R == 2 ? bin_entry_kernel<4, 2, 1> : bin_entry_kernel<4, 4, 1>;
+      static std::atomic<uint64_t> attr_t[3];
+      smem_opt_in(reinterpret_cast<const void*>(k), attr_t[R == 1 ? 0 : R == 2 ? 1 : 2]);
+      const int64_t slices = pick_slices(n_fg, sms, (nbk + nw - 1) / nw);
+      k<<<(int)(n_fg * slices), nw * 32, bsm_of(nw), st>>>(
+          tm, X, n_rows, n_sr * R, m->F, m->d_bkt, L.bkt_nb, L.bkt_stride, static_cast<uint32_t*>(codes));
+      count_launch();
+      err = cudaGetLastError();
+      if (err != cudaSuccess) {
+        cudaFreeAsync(codes, st);
+        return err;
+      }
+      *codes_out = codes;
+      return cudaSuccess;
+    }
   }
   if (L.bkt_nb > 0 && L.bkt_fg > 0 && !L.stream && want_bkt) {
     // per-feature-group bucketed binning

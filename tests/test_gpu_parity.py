@@ -274,13 +274,29 @@ def test_coded_wide_code_range(monkeypatch):
     assert g.layout()["coded"]
 
 
-def test_c5_shard_coded(monkeypatch):
+@pytest.mark.parametrize("binv", [None, "g"])
+def test_c5_shard_coded(binv, monkeypatch):
     """C5-shaped tree shard (1250 trees would take minutes in the oracle: 120
     trees of depth 10 over 200 features) in threshold-bin codes with
-    feature-group binning (6K+ thresholds per feature at full size)."""
+    feature-group bucketed binning (6K+ thresholds per feature at full size):
+    the TMA-staged kernel (default) and the direct-load one (BRIDGER_BIN=g)."""
     monkeypatch.setenv("BRIDGER_CODES", "1")
+    if binv:
+        monkeypatch.setenv("BRIDGER_BIN", binv)
     c, m = make_config("C5", n_trees=120)
     g, _ = check(m, gen_x(5, 0, 3001, 200), apply=False)
+
+
+@pytest.mark.parametrize("F", [202, 199])
+def test_wide_feature_group_binning_unaligned_rows(F, monkeypatch):
+    """Feature-group bucketed tables with TMA row tiles when rows are not
+    16-byte aligned (F = 202: 2-row super-rows, F = 199: 4-row), boxes
+    starting at the aligned column below each group; NaN / inf / -0 inputs
+    and a ragged tail; raw sums bitwise."""
+    monkeypatch.setenv("BRIDGER_CODES", "1")
+    m = perfect_ensemble(120 + F, 60, 10, F, kind="regression", lr=0.01, calib_rows=2048)
+    X = inject_specials(gen_x(121 + F, 0, 2003, F), 121 + F, rate=0.02)
+    check(m, X, apply=False)
 
 
 @pytest.mark.parametrize("pret", ["1", "0"])

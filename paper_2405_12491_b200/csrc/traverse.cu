@@ -601,6 +601,17 @@ __global__ void __launch_bounds__(512, 1) bin_bucket_fg_kernel(const float* __re
 // is an illegal instruction, tools/tma_probe.cu), so for R > 1 the boxes
 // start at the aligned column at or below r * F + f0 and are W = FG + 4 wide.
 // Rows past the last whole super-row (n_rows % R) are read directly.
+// Row-tile width W (values staged per row): a box must start on a 16-byte
+// column, so it begins d = (r F + f0) mod 4 values before the group when
+// that is not 0 (R > 1, or FG = 2) and is rounded up to 4 values.
+__host__ __device__ constexpr int bin_tile_w(int FG, int R) {
+  return R == 1 ? (FG < 4 ? 4 : FG) : ((FG + (R == 2 ? 2 : 3) + 3) / 4) * 4;
+}
+
+// TAB = 2: the Eytzinger search trees (TravLayout::bin_table, 2^k - 1 slots
+// per feature) for tables too large for any bucket form (C4: up to 63K
+// thresholds per feature, k = 16): the top T levels of FG features' trees in
+// shared memory, the k - T deeper ones read from L2 (NB := k, stride := T).
 // TAB = 1: the same TMA-staged pipeline over the bucketed tables instead
 // (TravLayout::bkt_blob built for feature groups: u16 cum + the 15-wide
 // window search; wide inputs such as the C5 shard, whose ~6.4K thresholds per
@@ -613,7 +624,7 @@ __global__ void __launch_bounds__(512, 1) bin_entry_kernel(const __grid_constant
                                                            int32_t stride, uint32_t* __restrict__ codes) {
   extern __shared__ __align__(128) uint8_t smem[];
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  constexpr int W = R == 1 ? FG : FG + 4;    // staged values per row
+  constexpr int W = bin_tile_w(FG, R);       // staged values per row
   constexpr uint32_t kTile = 32u * W * 4u;   // bytes of one staged block
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
   const int F2h = (F + 1) >> 1;
@@ -622,20 +633,31 @@ __global__ void __launch_bounds__(512, 1) bin_entry_kernel(const __grid_constant
   const int slice = blockIdx.x / n_fg, n_slices = gridDim.x / n_fg;
   const int f0 = fg * FG;
   const int nf = min(FG, F - f0);
-  // per feature: entries [NB][16 B] (TAB 0) or cum [NB + 2] u16 rounded to 4 B (TAB 1)
-  const uint32_t sec2 = TAB == 0 ? 16u * (uint32_t)NB : (uint32_t)(((NB + 2) * 2 + 3) / 4 * 4);
+  // per feature: entries [NB][16 B] (TAB 0), cum [NB + 2] u16 rounded to 4 B
+  // (TAB 1), or the top T levels of the search tree (TAB 2; no U: stride = T)
+  const int P = TAB == 2 ? (1 << NB) - 1 : 1, Pt = TAB == 2 ? (1 << stride) - 1 : 1;
+  const uint32_t sec2 = TAB == 0 ? 16u * (uint32_t)NB
+                        : TAB == 1 ? (uint32_t)(((NB + 2) * 2 + 3) / 4 * 4)
+                                   : 4u * (uint32_t)Pt;
+  const int ustride = TAB == 2 ? 0 : stride;
   // shared: stage [NW][2][32][W] fp32 | params [FG][16 B] | entries / cum [FG][sec2] | U [FG][stride] | bars
   uint8_t* stage = smem;
   uint8_t* s_prm = smem + (size_t)NW * 2 * kTile;
   uint8_t* s_ent = s_prm + 16 * FG;
   uint8_t* s_u = s_ent + (size_t)FG * sec2;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_u + (size_t)FG * stride * 4);  // [NW][2] + [1] table
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_u + (size_t)FG * ustride * 4);  // [NW][2] + [1] table
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2 * NW + 1; ++i) ptx::mbar_init(&bars[i], 1);
     ptx::fence_barrier_init();
   }
   __syncthreads();
-  if (TAB == 1) {  // cum rows are 4-byte multiples: a plain cooperative copy of this group's tables
+  if (TAB == 2) {  // top T levels of this group's search trees
+    const float* tab = reinterpret_cast<const float*>(blob);
+    float* dst = reinterpret_cast<float*>(s_ent);
+    for (int i = threadIdx.x; i < nf * Pt; i += blockDim.x) dst[i] = tab[(size_t)(f0 + i / Pt) * P + i % Pt];
+    if (threadIdx.x == 0) ptx::mbar_arrive(&bars[2 * NW]);
+    __syncthreads();
+  } else if (TAB == 1) {  // cum rows are 4-byte multiples: a plain cooperative copy of this group's tables
     const uint32_t* g = reinterpret_cast<const uint32_t*>(blob);
     const size_t g_cum = (size_t)F * 4, g_u = ((size_t)F * 16 + (size_t)F * sec2) / 4;
     const int cw = (int)(sec2 / 4), uw = stride;
@@ -686,8 +708,8 @@ __global__ void __launch_bounds__(512, 1) bin_entry_kernel(const __grid_constant
 #pragma unroll
   for (int q = 0; q < FG; ++q) {
     const int qq = min(q, nf - 1);
-    lo[q] = reinterpret_cast<const float*>(s_prm)[4 * qq];
-    iw[q] = reinterpret_cast<const float*>(s_prm)[4 * qq + 1];
+    lo[q] = TAB == 2 ? 0.f : reinterpret_cast<const float*>(s_prm)[4 * qq];
+    iw[q] = TAB == 2 ? 0.f : reinterpret_cast<const float*>(s_prm)[4 * qq + 1];
     eb_[q] = ptx::s2u(s_ent) + sec2 * (uint32_t)qq;
     ub_[q] = ptx::s2u(s_u) + 4u * (uint32_t)stride * (uint32_t)qq;
   }
@@ -701,13 +723,14 @@ __global__ void __launch_bounds__(512, 1) bin_entry_kernel(const __grid_constant
     ptx::mbar_wait(&wb[buf], (uint32_t)(it >> 1) & 1u);
     const uint32_t xa = st0 + (uint32_t)buf * kTile + xoff;
     float x[FG];
-    if (R == 1) {  // 16-byte aligned
+    if (R == 1 && FG % 4 == 0) {  // 16-byte aligned
 #pragma unroll
       for (int q = 0; q < FG; q += 4)
         asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                     : "=f"(x[q]), "=f"(x[q + 1]), "=f"(x[q + 2]), "=f"(x[q + 3])
+                     : "=f"(x[q]), "=f"(x[q + (FG > 1 ? 1 : 0)]), "=f"(x[q + (FG > 2 ? 2 : 0)]),
+                       "=f"(x[q + (FG > 3 ? 3 : 0)])
                      : "r"(xa + 4u * q));
-    } else if (R == 2) {  // F = 2 mod 4: d in {0, 2}, 8-byte aligned
+    } else if (R <= 2 && FG % 2 == 0) {  // d in {0, 2}: 8-byte aligned
 #pragma unroll
       for (int q = 0; q < FG; q += 2)
         asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(x[q]), "=f"(x[q + 1]) : "r"(xa + 4u * q));
@@ -726,8 +749,38 @@ __global__ void __launch_bounds__(512, 1) bin_entry_kernel(const __grid_constant
       issue(blk + 2 * step, buf);
     }
     uint32_t cd[FG];
+    if (TAB == 2) {  // Eytzinger descents, the FG chains interleaved: T levels in shared memory, then L2
+      uint32_t A[FG], c4[FG];
+#pragma unroll
+      for (int q = 0; q < FG; ++q) {
+        A[q] = eb_[q];
+        c4[q] = 4u - eb_[q];
+      }
+      for (int l = 0; l < stride; ++l) {
+#pragma unroll
+        for (int q = 0; q < FG; ++q) {
+          const float e = ptx::lds_f32(A[q]);
+          A[q] = 2u * A[q] + c4[q];
+          if (e < x[q]) A[q] += 4u;
+        }
+      }
+      uint32_t i[FG];
+      const float* tg[FG];
+#pragma unroll
+      for (int q = 0; q < FG; ++q) {
+        i[q] = (A[q] + c4[q] - 4u) >> 2;
+        tg[q] = reinterpret_cast<const float*>(blob) + (size_t)(f0 + min(q, nf - 1)) * P;
+      }
+      for (int l = stride; l < NB; ++l) {
+#pragma unroll
+        for (int q = 0; q < FG; ++q) i[q] = 2u * i[q] + 1u + (__ldg(tg[q] + i[q]) < x[q] ? 1u : 0u);
+      }
+#pragma unroll
+      for (int q = 0; q < FG; ++q) cd[q] = q >= nf ? 0u : isnan(x[q]) ? 0xFFFFu : i[q] - (uint32_t)P;
+    }
 #pragma unroll
     for (int q = 0; q < FG; ++q) {
+      if (TAB == 2) continue;
       float t = __fmul_rn(__fsub_rn(x[q], lo[q]), iw[q]);
       t = fminf(fmaxf(t, 0.f), nbm1);
       if (TAB == 1) {  // cum[b] + lower_bound in the 15-wide window
@@ -960,12 +1013,12 @@ static cudaError_t launch_binning(const bridger_model* m, const TravLayout& L, c
   if (L.bke_nb > 0 && !L.stream && want_bke && (reinterpret_cast<uintptr_t>(X) & 15) == 0 && n_rows >= 128) {
     const int64_t n_sr = n_rows / R;
     CUtensorMap tm;
-    err = encode_x_map(&tm, X, m->F, R, n_sr, R == 1 ? L.bke_fg : L.bke_fg + 4);
+    err = encode_x_map(&tm, X, m->F, R, n_sr, bin_tile_w(L.bke_fg, R));
     if (err == cudaSuccess) {
       const int FG = L.bke_fg;
       const int n_fg = (m->F + FG - 1) / FG;
       const int nw = 16;
-      const int bsm = nw * 2 * 32 * (R == 1 ? FG : FG + 4) * 4 + 16 * FG + FG * L.bke_nb * 16 + FG * L.bke_stride * 4 + 8 * (2 * nw + 1);
+      const int bsm = nw * 2 * 32 * bin_tile_w(FG, R) * 4 + 16 * FG + FG * L.bke_nb * 16 + FG * L.bke_stride * 4 + 8 * (2 * nw + 1);
       const int64_t slices = pick_slices(n_fg, sms, (nbk + nw - 1) / nw);
       using BinE = void (*)(const CUtensorMap, const float*, int64_t, int64_t, int32_t, const uint8_t*, int32_t, int32_t,
                             uint32_t*);
@@ -999,7 +1052,7 @@ static cudaError_t launch_binning(const bridger_model* m, const TravLayout& L, c
     // (bin_entry_kernel<4, R, 1>) when they fit next to the staging;
     // BRIDGER_BIN=g keeps the direct-load kernel below
     const int R = (m->F * 4) % 16 == 0 ? 1 : (m->F * 8) % 16 == 0 ? 2 : 4;
-    const int W = R == 1 ? 4 : 8;
+    const int W = bin_tile_w(4, R);
     const int n_fg = (m->F + 3) / 4;
     const int cum_row = ((L.bkt_nb + 2) * 2 + 3) / 4 * 4;
     int nw = 16;
@@ -1130,6 +1183,36 @@ static cudaError_t launch_binning(const bridger_model* m, const TravLayout& L, c
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bk, nwb * 32, bsm);
   const int bgrid = fgsz ? (int)want_ctas
                          : (int)std::max<int64_t>(1, std::min<int64_t>(want_ctas, (int64_t)sms * std::max(1, occ)));
+  if (fgsz == 2 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 && n_rows >= 128 && !(bin_env && bin_env[0] == 'g')) {
+    // the same feature groups with TMA-staged row tiles (bin_entry_kernel<2, R, 2>)
+    const int R = (m->F * 4) % 16 == 0 ? 1 : (m->F * 8) % 16 == 0 ? 2 : 4;
+    const int W = bin_tile_w(2, R);
+    const int n_fg = (m->F + 1) / 2;
+    int nw = 16;
+    auto bsm_of = [&](int w) { return w * 2 * 32 * W * 4 + 2 * 16 + bsm + 8 * (2 * w + 1); };
+    while (nw > 4 && bsm_of(nw) > 232448) nw /= 2;
+    CUtensorMap tm;
+    const int64_t n_sr = n_rows / R;
+    if (bsm_of(nw) <= 232448 && encode_x_map(&tm, X, m->F, R, n_sr, W) == cudaSuccess) {
+      using BinE = void (*)(const CUtensorMap, const float*, int64_t, int64_t, int32_t, const uint8_t*, int32_t, int32_t,
+                            uint32_t*);
+      BinE k = R == 1 ? bin_entry_kernel<2, 1, 2> : R == 2 ? bin_entry_kernel<2, 2, 2> : bin_entry_kernel<2, 4, 2>;
+      static std::atomic<uint64_t> attr_y[3];
+      smem_opt_in(reinterpret_cast<const void*>(k), attr_y[R == 1 ? 0 : R == 2 ? 1 : 2]);
+      const int64_t slices = pick_slices(n_fg, sms, (nbk + nw - 1) / nw);
+      k<<<(int)(n_fg * slices), nw * 32, bsm_of(nw), st>>>(tm, X, n_rows, n_sr * R, m->F,
+                                                            reinterpret_cast<const uint8_t*>(m->d_bin_table), L.bin_k,
+                                                            fg_levels, static_cast<uint32_t*>(codes));
+      count_launch();
+      err = cudaGetLastError();
+      if (err != cudaSuccess) {
+        cudaFreeAsync(codes, st);
+        return err;
+      }
+      *codes_out = codes;
+      return cudaSuccess;
+    }
+  }
   if (fgsz) {
     auto fk = fgsz == 4 ? bin_fg_kernel<4> : fgsz == 2 ? bin_fg_kernel<2> : bin_fg_kernel<1>;
     cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);

@@ -255,20 +255,25 @@ def test_entry_binning_small_and_ragged(F, n, monkeypatch):
     assert g.layout()["coded"]
 
 
-def test_coded_wide_code_range(monkeypatch):
+@pytest.mark.parametrize("F,binv", [(4, None), (4, "g"), (5, None), (6, None)])
+def test_coded_wide_code_range(F, binv, monkeypatch):
     """Up to 65534 distinct thresholds per feature (16-bit code index, missing
-    flag in bit 0): ~41K random distinct thresholds on each of 4 features ->
+    flag in bit 0): ~164K / F random distinct thresholds per feature ->
     2^16-slot search trees, binned with their top 14 levels in shared memory
-    and the rest from global memory; NaN / missing-left routing included."""
+    and the rest from global memory -- feature pairs with TMA-staged row
+    tiles (F = 4, 5, 6: 1-, 4- and 2-row super-rows) or with direct loads
+    (BRIDGER_BIN=g); NaN / missing-left routing included."""
     monkeypatch.setenv("BRIDGER_CODES", "1")
-    m = perfect_ensemble(80, 40, 12, 4, kind="regression", lr=0.1, calib_rows=512)
+    if binv:
+        monkeypatch.setenv("BRIDGER_BIN", binv)
+    m = perfect_ensemble(80, 40, 12, F, kind="regression", lr=0.1, calib_rows=512)
     rng = np.random.default_rng(81)
     th = m.threshold.copy()
     internal = m.left != -1
     th[internal] = rng.standard_normal(int(internal.sum())).astype(np.float32)
     ml = (rng.random(len(th)) < 0.3).astype(np.uint8)
     m = ModelDesc(**{**m.__dict__, "threshold": th, "missing_left": ml})
-    X = inject_specials(gen_x(82, 0, 3001, 4), 82, rate=0.02)
+    X = inject_specials(gen_x(82, 0, 3001, F), 82, rate=0.02)
     X[::53, 1] = th[internal][m.feature[internal] == 1][:57].repeat(1)[: len(X[::53])]
     g, _ = check(m, X, apply=False)
     assert g.layout()["coded"]

@@ -175,7 +175,14 @@ class _DescKeep:
 
 
 def _stream_ptr(device):
+    """The caller's current CUDA stream on `device` (raw handle).  torch's
+    private raw-stream getter costs ~0.2 us against ~2.3 us for
+    torch.cuda.current_stream() -- a quarter of a small predict's host time."""
     import torch
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        return C.c_void_p(raw(idx))
     return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 

@@ -183,3 +183,25 @@ def test_two_devices_one_process():
         with torch.cuda.device(dev_i):
             got = g.predict(xd).cpu().numpy()
         np.testing.assert_array_equal(got, o["pred"])
+
+
+def test_predict_on_caller_stream():
+    """Kernels are enqueued on the caller's current stream (the boundary's
+    stream argument, filled by the binding from torch's current stream): a
+    predict issued on a side stream behind a long kernel on that stream sees
+    the input that kernel wrote, and the default stream is not used."""
+    c, m = make_config("C2", n_trees=20)
+    g = B.Model(m)
+    X = gen_x(2, 0, 4096, 28)
+    want = oracle.run(m, X)["label"]
+    Xd = torch.zeros((4096, 28), device="cuda")
+    src = torch.from_numpy(X).cuda()
+    big = torch.empty(64 << 20, device="cuda")
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        big.fill_(1.0)          # keeps the side stream busy
+        Xd.copy_(src)           # the input appears only after it
+        lab = g.predict(Xd)
+    s.synchronize()
+    np.testing.assert_array_equal(lab.cpu().numpy(), want)

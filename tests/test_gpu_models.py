@@ -205,3 +205,39 @@ def test_predict_on_caller_stream():
         lab = g.predict(Xd)
     s.synchronize()
     np.testing.assert_array_equal(lab.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("name,trees", [("C1", None), ("C2", 20), ("C3", 240), ("C5", 60)])
+def test_predict_captured_in_cuda_graph(name, trees):
+    """A predict call captured into a CUDA graph (serving: one graph launch per
+    batch instead of the binding + host dispatch) and replayed on new input
+    contents gives the oracle's answers: binning, the walk kernels (K4, K4d
+    with programmatic dependent launch), stream-ordered scratch and finalize
+    are all capturable."""
+    cfg, m = make_config(name, n_trees=trees)
+    n = 150 if name == "C1" else 3000
+    g = B.Model(m)
+    if name == "C3":
+        assert g.layout()["format"] == "codes_deep"  # K4d (PDL launch) inside the graph
+    Xs = [gen_x(cfg.seed + i, 0, n, cfg.n_features) for i in range(3)]
+    Xd = torch.from_numpy(Xs[0]).cuda()
+    classif = cfg.kind == "classification"
+    out = torch.empty(n, dtype=torch.int32, device="cuda") if classif else torch.empty((n, cfg.n_classes), device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        g.predict(Xd, out=out)  # warm-up (attributes, pools) outside the capture
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        g.predict(Xd, out=out)
+    for X in Xs[1:] + Xs[:1]:
+        Xd.copy_(torch.from_numpy(X))
+        graph.replay()
+        torch.cuda.synchronize()
+        o = oracle.run(m, X)
+        if classif:
+            np.testing.assert_array_equal(out.cpu().numpy(), o["label"])
+        else:
+            np.testing.assert_array_equal(out.cpu().numpy(), o["pred"].astype(np.float32).reshape(out.shape))

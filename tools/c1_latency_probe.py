@@ -45,3 +45,22 @@ for _ in range(300):
     torch.cuda.synchronize()
     ts.append(ev[0].elapsed_time(ev[1]) * 1e3)
 print("bare C call, event us median", float(np.median(ts)))
+
+# the same predict captured once into a CUDA graph (serving path)
+s = torch.cuda.Stream()
+s.wait_stream(torch.cuda.current_stream())
+with torch.cuda.stream(s):
+    g.predict(X, out=out)
+torch.cuda.current_stream().wait_stream(s)
+graph = torch.cuda.CUDAGraph()
+with torch.cuda.graph(graph):
+    g.predict(X, out=out)
+print("graph replay us/call", per_call(graph.replay))
+ts = []
+for _ in range(300):
+    ev[0].record()
+    graph.replay()
+    ev[1].record()
+    torch.cuda.synchronize()
+    ts.append(ev[0].elapsed_time(ev[1]) * 1e3)
+print("graph replay, event us median", float(np.median(ts)))

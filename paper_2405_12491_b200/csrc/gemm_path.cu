@@ -75,7 +75,9 @@ static constexpr int kSmemMax = 232448;
 // ------------------------------------------------------------------ K1 -----
 // grid (row tiles of the block, tree groups), 128 threads = 128 rows.
 // out layout TILED: P[t][rt][kc][128][16]; PLAIN: P[t][row][i_pad].
-template <bool PLAIN>
+// ML: the model has missing_left nodes (else the NaN test per decision is
+// compiled out: NaN compares false -> 0 -> right, reading c2).
+template <bool PLAIN, bool ML>
 __global__ void __launch_bounds__(128) gc_kernel(const float* __restrict__ X, int64_t row0, int32_t rows, int32_t F,
                                                  const uint8_t* __restrict__ gbase, GemmClassDev cls,
                                                  int32_t tree_begin, int32_t trees_per_cta, int32_t tree_end,
@@ -115,12 +117,17 @@ __global__ void __launch_bounds__(128) gc_kernel(const float* __restrict__ X, in
       for (int q = 0; q < 4; ++q) {
         uint32_t word = 0;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const uint2 n = ndb[kc * 16 + q * 4 + b];            // broadcast read
-          const float x = xr[(n.x & 0x7fffffffu) * S];          // exact fp32 gather (a1)
-          uint32_t d = (x <= __uint_as_float(n.y)) ? 1u : 0u;   // a2: less_equal
-          if ((int32_t)n.x < 0 && isnan(x)) d = 1u;             // missing_left
-          word |= d << (8 * b);
+        for (int b = 0; b < 4; b += 2) {
+          // two node records per broadcast read (16 B)
+          const uint4 n2 = *reinterpret_cast<const uint4*>(&ndb[kc * 16 + q * 4 + b]);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t nf = h ? n2.z : n2.x, nt = h ? n2.w : n2.y;
+            const float x = xr[(ML ? (nf & 0x7fffffffu) : nf) * S];  // exact fp32 gather (a1)
+            uint32_t d = (x <= __uint_as_float(nt)) ? 1u : 0u;      // a2: less_equal
+            if (ML && (int32_t)nf < 0 && isnan(x)) d = 1u;          // missing_left
+            word |= d << (8 * (b + h));
+          }
         }
         w[q] = word;
       }
@@ -1113,23 +1120,24 @@ void gemm_free(bridger_model* m) {
 }
 
 static cudaError_t launch_gc(const float* X, int64_t row0, int32_t rows, int32_t F, const uint8_t* gbase,
-                             const GemmClassDev& c, int32_t t_begin, int32_t t_end, int8_t* P, bool plain,
-                             cudaStream_t st) {
+                             const GemmClassDev& c, int32_t t_begin, int32_t t_end, int8_t* P, bool plain, bool ml,
+                             int sms, cudaStream_t st) {
   const int n_rt = (rows + 127) / 128;
   const int n_t = t_end - t_begin;
-  // spread trees over enough CTAs to fill the machine
-  int tpc = std::max(1, (int)((int64_t)n_t * n_rt / (4 * 148)));
+  const int smem = 129 * F * 4 + 2 * c.i_pad * 8;
+  // spread trees over enough 4-warp CTAs to keep ~12 resident per SM (round
+  // 1 aimed at 4: ncu showed 23% of the warp slots active, issue-latency
+  // bound); each tree group re-reads its 128-row X tile (from L2)
+  const int per_sm = std::max(1, std::min(12, (int)(kSmemMax / std::max(1, smem + 1024))));
+  int tpc = std::max(1, (int)((int64_t)n_t * n_rt / ((int64_t)per_sm * sms)));
   tpc = std::min(tpc, n_t);
   dim3 grid(n_rt, (n_t + tpc - 1) / tpc);
-  const int smem = 129 * F * 4 + 2 * c.i_pad * 8;
-  if (smem > 48 * 1024) {
-    cudaFuncSetAttribute(gc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
-    cudaFuncSetAttribute(gc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
-  }
+  auto k = plain ? (ml ? gc_kernel<true, true> : gc_kernel<true, false>)
+                 : (ml ? gc_kernel<false, true> : gc_kernel<false, false>);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
   cudaEvent_t ev;
   hot_begin(st, &ev);
-  if (plain) gc_kernel<true><<<grid, 128, smem, st>>>(X, row0, rows, F, gbase, c, t_begin, tpc, t_end, P);
-  else gc_kernel<false><<<grid, 128, smem, st>>>(X, row0, rows, F, gbase, c, t_begin, tpc, t_end, P);
+  k<<<grid, 128, smem, st>>>(X, row0, rows, F, gbase, c, t_begin, tpc, t_end, P);
   hot_end_id(st, ev, 1);
   count_launch();
   return cudaGetLastError();
@@ -1214,6 +1222,8 @@ static cudaError_t gemm_run_impl(const bridger_model* m, const float* X, int64_t
                                  int32_t total_trees, cudaStream_t st, bool sparse) {
   const GemmHost* h = static_cast<const GemmHost*>(m->gemm_host);
   const uint8_t* gbase = static_cast<const uint8_t*>(m->d_gemm);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device);
   // row blocks: decision scratch <= 1 GB (large blocks keep every kernel's grid
   // full); BRIDGER_GEMM_SCRATCH_MB sets it (e.g. L2-resident blocks)
   const int64_t per_row = sparse ? h->max_psp_per_row : h->max_p_per_row;
@@ -1251,10 +1261,10 @@ static cudaError_t gemm_run_impl(const bridger_model* m, const float* X, int64_t
         csp.i_pad = c.k_sp;
         csp.feat_off = c.feat_sp_off;
         csp.thr_off = c.thr_sp_off;
-        e = launch_gc(X, r0, rows, m->F, gbase, csp, 0, c.n_trees, P, false, st);
+        e = launch_gc(X, r0, rows, m->F, gbase, csp, 0, c.n_trees, P, false, h->has_missing, sms, st);
         if (e == cudaSuccess) e = launch_pcs(P, gbase, c, c.n_trees, rows, 0, leaf, nullptr, m->device, st);
       } else {
-        e = launch_gc(X, r0, rows, m->F, gbase, c, 0, c.n_trees, P, false, st);
+        e = launch_gc(X, r0, rows, m->F, gbase, c, 0, c.n_trees, P, false, h->has_missing, sms, st);
         if (e == cudaSuccess) e = launch_pc(P, gbase, c, c.n_trees, rows, 0, leaf, nullptr, m->device, st);
       }
       if (e != cudaSuccess) break;
@@ -1414,8 +1424,10 @@ cudaError_t gemm_step_decisions(const bridger_model* m, const float* X, int64_t 
     return cudaErrorInvalidValue;
   }
   const int32_t t_begin = h->tree_slot[tree0] - c.first_slot;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device);
   return launch_gc(X, 0, (int32_t)n_rows, m->F, static_cast<const uint8_t*>(m->d_gemm), c, t_begin,
-                   t_begin + n_trees, out, true, st);
+                   t_begin + n_trees, out, true, h->has_missing, sms, st);
 }
 
 cudaError_t gemm_step_scores(const bridger_model* m, int32_t depth, const int8_t* P, int64_t rows, int32_t* out,

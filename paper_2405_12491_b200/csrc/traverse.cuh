@@ -918,7 +918,11 @@ __device__ __forceinline__ void stream_walk_codes(uint32_t nb, int tstride, int 
 // SF: streamed node format -- 0: 8-byte records, 1: split (fp32 thresholds +
 // u8 features), 2: threshold-bin codes (4-byte words, u16 input codes)
 template <int KT, typename ACC, bool ML, int W, bool APPLY, int SF = 0>
-__global__ void __launch_bounds__(544, 1) trav_stream_kernel(const TravParams p) {
+// Coded walks with K <= 8: up to 20 walking warps + the loader (672 threads;
+// C4: 16 -> 20 warps, 13.27 -> 12.2 ms per 1M rows -- an 800-thread bound
+// forces spills at 72 registers); other formats keep 16 + 1 (their larger
+// per-thread state spills under the 672-thread register cap).
+__global__ void __launch_bounds__((SF == 2 && KT <= 8) ? 672 : 544, 1) trav_stream_kernel(const TravParams p) {
   constexpr bool SPL = SF == 1;
   constexpr bool SCODES = SF == 2;
   extern __shared__ __align__(128) uint8_t smem[];

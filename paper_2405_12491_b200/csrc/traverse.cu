@@ -617,11 +617,20 @@ __host__ __device__ constexpr int bin_tile_w(int FG, int R) {
 // window search; wide inputs such as the C5 shard, whose ~6.4K thresholds per
 // feature leave no room for entries) -- it replaces bin_bucket_fg_kernel's
 // per-lane global row loads (32 sectors per warp load, latency-bound).
+// Lockstep (epochs != nullptr; grid co-resident, launched cooperatively): the
+// ceil(F / FG) feature-group CTAs of one row range otherwise drift apart on
+// inputs larger than L2 and each group's sectors come from DRAM again (C3:
+// 9.2 GB read for a 3.6 GB input).  Every `ipe` block iterations a CTA
+// publishes its epoch (a counter per epoch) and waits until every CTA has
+// finished the epoch before the previous one: at most ~2 epochs (~2 x 24 MB
+// of X) are in flight, so the groups share each row's sectors through L2.
 template <int FG, int R, int TAB>
 __global__ void __launch_bounds__(512, 1) bin_entry_kernel(const __grid_constant__ CUtensorMap tmx,
                                                            const float* __restrict__ X, int64_t n_rows, int64_t n_tma,
                                                            int32_t F, const uint8_t* __restrict__ blob, int32_t NB,
-                                                           int32_t stride, uint32_t* __restrict__ codes) {
+                                                           int32_t stride, uint32_t* __restrict__ codes,
+                                                           uint32_t* __restrict__ epochs, int32_t ipe,
+                                                           int32_t n_epochs) {
   extern __shared__ __align__(128) uint8_t smem[];
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   constexpr int W = bin_tile_w(FG, R);       // staged values per row
@@ -718,7 +727,28 @@ __global__ void __launch_bounds__(512, 1) bin_entry_kernel(const __grid_constant
   // its first value d = (r * F + f0) % 4 columns into the box row
   const int xr = lane % R;
   const uint32_t xoff = ((uint32_t)xr * (32 / R) + (uint32_t)(lane / R)) * W * 4u + 4u * (uint32_t)((xr * F + f0) & 3);
-  for (int it = 0; blk < n_blocks; blk += step, ++it) {
+  // every warp of the CTA runs the same iteration count (the first warp's:
+  // the largest), so the epoch barriers below see all of them
+  const int64_t first = (int64_t)slice * NW;
+  const int64_t n_iter = first < n_blocks ? (n_blocks - 1 - first) / step + 1 : 0;
+  for (int it = 0; it < n_iter; blk += step, ++it) {
+    if (epochs != nullptr && it > 0 && it % ipe == 0) {
+      const int e = it / ipe;  // epoch e begins: this CTA finished epoch e - 1
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(epochs + (e - 1)) : "memory");
+        if (e >= 2) {  // wait until every CTA finished epoch e - 2
+          uint32_t v = 0;
+          for (;;) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(epochs + (e - 2)) : "memory");
+            if (v >= gridDim.x) break;
+            __nanosleep(64);
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (blk >= n_blocks) continue;  // this warp's blocks ran out (the CTA's last iteration)
     const int buf = it & 1;
     ptx::mbar_wait(&wb[buf], (uint32_t)(it >> 1) & 1u);
     const uint32_t xa = st0 + (uint32_t)buf * kTile + xoff;
@@ -810,6 +840,12 @@ __global__ void __launch_bounds__(512, 1) bin_entry_kernel(const __grid_constant
 #pragma unroll
     for (int q = 0; q < FG; q += 2)
       if (q < nf) dst[(size_t)((f0 + q) >> 1) * 32] = cd[q] | (cd[q + 1] << 16);
+  }
+  if (epochs != nullptr) {  // the epochs this CTA did not publish in the loop: done
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int e = n_iter > 0 ? (int)((n_iter - 1) / ipe) : 0; e < n_epochs; ++e)
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(epochs + e) : "memory");
   }
 }
 
@@ -1008,8 +1044,11 @@ static cudaError_t launch_binning(const bridger_model* m, const TravLayout& L, c
   // from DRAM (9.2 GB read vs 3.6), so despite 23% fewer shared wavefronts it
   // ties the all-features bucketed kernel (2.04 ms each).
   const int R = (m->F * 4) % 16 == 0 ? 1 : (m->F * 8) % 16 == 0 ? 2 : 4;
+  const bool fits_l2 = (double)n_rows * m->F * 4 <= (double)l2_bytes(m->device);
+  const char* lock_env = std::getenv("BRIDGER_BIN_LOCK");
+  const bool lock_ok = !fits_l2 && !(lock_env && lock_env[0] == '0');
   const bool want_bke = bin_env ? (bin_env[0] == 'e' || bin_env[0] == 'E')
-                                : R == 1 && (double)n_rows * m->F * 4 <= (double)l2_bytes(m->device);
+                                : (R == 1 && fits_l2) || (lock_ok && lock_env && lock_env[0] == '1');
   if (L.bke_nb > 0 && !L.stream && want_bke && (reinterpret_cast<uintptr_t>(X) & 15) == 0 && n_rows >= 128) {
     const int64_t n_sr = n_rows / R;
     CUtensorMap tm;
@@ -1021,7 +1060,7 @@ static cudaError_t launch_binning(const bridger_model* m, const TravLayout& L, c
       const int bsm = nw * 2 * 32 * bin_tile_w(FG, R) * 4 + 16 * FG + FG * L.bke_nb * 16 + FG * L.bke_stride * 4 + 8 * (2 * nw + 1);
       const int64_t slices = pick_slices(n_fg, sms, (nbk + nw - 1) / nw);
       using BinE = void (*)(const CUtensorMap, const float*, int64_t, int64_t, int32_t, const uint8_t*, int32_t, int32_t,
-                            uint32_t*);
+                            uint32_t*, uint32_t*, int32_t, int32_t);
       BinE k = nullptr;
       if (FG == 8)
         k = R == 1 ? bin_entry_kernel<8, 1, 0> : R == 2 ? bin_entry_kernel<8, 2, 0> : bin_entry_kernel<8, 4, 0>;
@@ -1029,10 +1068,46 @@ static cudaError_t launch_binning(const bridger_model* m, const TravLayout& L, c
         k = R == 1 ? bin_entry_kernel<4, 1, 0> : R == 2 ? bin_entry_kernel<4, 2, 0> : bin_entry_kernel<4, 4, 0>;
       static std::atomic<uint64_t> attr_e[6];
       smem_opt_in(reinterpret_cast<const void*>(k), attr_e[(FG == 8 ? 3 : 0) + (R == 1 ? 0 : R == 2 ? 1 : 2)]);
-      k<<<(int)(n_fg * slices), nw * 32, bsm, st>>>(tm, X, n_rows, n_sr * R, m->F, m->d_bke, L.bke_nb, L.bke_stride,
-                                                    static_cast<uint32_t*>(codes));
+      const int grid = (int)(n_fg * slices);
+      uint32_t* epochs = nullptr;
+      int32_t ipe = 1, n_epochs = 0;
+      if (lock_ok && grid <= sms) {
+        // lockstep epochs of ~24 MB of X (see the kernel); co-residency of
+        // every CTA is guaranteed by the cooperative launch below
+        const int64_t step = slices * nw;
+        const int64_t n_iter = (nbk + step - 1) / step;
+        ipe = (int32_t)std::max<int64_t>(1, (24LL << 20) / std::max<int64_t>(1, step * 32 * m->F * 4));
+        n_epochs = (int32_t)((n_iter + ipe - 1) / ipe);
+        if (cudaMallocAsync(reinterpret_cast<void**>(&epochs), (size_t)std::max(1, n_epochs) * 4, st) != cudaSuccess ||
+            cudaMemsetAsync(epochs, 0, (size_t)std::max(1, n_epochs) * 4, st) != cudaSuccess) {
+          cudaGetLastError();
+          if (epochs) cudaFreeAsync(epochs, st);
+          epochs = nullptr;
+        }
+      }
+      uint32_t* codes32 = static_cast<uint32_t*>(codes);
+      const uint8_t* bke = m->d_bke;
+      const int64_t n_tma_rows = n_sr * R;
+      const int32_t Fi = m->F, nbi = L.bke_nb, sti = L.bke_stride;
+      if (epochs) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(nw * 32);
+        cfg.dynamicSmemBytes = bsm;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        err = cudaLaunchKernelEx(&cfg, k, tm, X, n_rows, n_tma_rows, Fi, bke, nbi, sti, codes32, epochs, ipe, n_epochs);
+        cudaFreeAsync(epochs, st);
+      } else {
+        k<<<grid, nw * 32, bsm, st>>>(tm, X, n_rows, n_tma_rows, Fi, bke, nbi, sti, codes32, nullptr, 1, 0);
+        err = cudaSuccess;
+      }
       count_launch();
-      err = cudaGetLastError();
+      if (err == cudaSuccess) err = cudaGetLastError();
       if (err != cudaSuccess) {
         cudaFreeAsync(codes, st);
         return err;
@@ -1062,13 +1137,13 @@ static cudaError_t launch_binning(const bridger_model* m, const TravLayout& L, c
     const int64_t n_sr = n_rows / R;
     if (bsm_of(nw) <= 232448 && encode_x_map(&tm, X, m->F, R, n_sr, W) == cudaSuccess) {
       using BinE = void (*)(const CUtensorMap, const float*, int64_t, int64_t, int32_t, const uint8_t*, int32_t, int32_t,
-                            uint32_t*);
+                            uint32_t*, uint32_t*, int32_t, int32_t);
       BinE k = R == 1 ? bin_entry_kernel<4, 1, 1> : R == 2 ? bin_entry_kernel<4, 2, 1> : bin_entry_kernel<4, 4, 1>;
       static std::atomic<uint64_t> attr_t[3];
       smem_opt_in(reinterpret_cast<const void*>(k), attr_t[R == 1 ? 0 : R == 2 ? 1 : 2]);
       const int64_t slices = pick_slices(n_fg, sms, (nbk + nw - 1) / nw);
       k<<<(int)(n_fg * slices), nw * 32, bsm_of(nw), st>>>(
-          tm, X, n_rows, n_sr * R, m->F, m->d_bkt, L.bkt_nb, L.bkt_stride, static_cast<uint32_t*>(codes));
+          tm, X, n_rows, n_sr * R, m->F, m->d_bkt, L.bkt_nb, L.bkt_stride, static_cast<uint32_t*>(codes), nullptr, 1, 0);
       count_launch();
       err = cudaGetLastError();
       if (err != cudaSuccess) {
@@ -1195,14 +1270,14 @@ static cudaError_t launch_binning(const bridger_model* m, const TravLayout& L, c
     const int64_t n_sr = n_rows / R;
     if (bsm_of(nw) <= 232448 && encode_x_map(&tm, X, m->F, R, n_sr, W) == cudaSuccess) {
       using BinE = void (*)(const CUtensorMap, const float*, int64_t, int64_t, int32_t, const uint8_t*, int32_t, int32_t,
-                            uint32_t*);
+                            uint32_t*, uint32_t*, int32_t, int32_t);
       BinE k = R == 1 ? bin_entry_kernel<2, 1, 2> : R == 2 ? bin_entry_kernel<2, 2, 2> : bin_entry_kernel<2, 4, 2>;
       static std::atomic<uint64_t> attr_y[3];
       smem_opt_in(reinterpret_cast<const void*>(k), attr_y[R == 1 ? 0 : R == 2 ? 1 : 2]);
       const int64_t slices = pick_slices(n_fg, sms, (nbk + nw - 1) / nw);
       k<<<(int)(n_fg * slices), nw * 32, bsm_of(nw), st>>>(tm, X, n_rows, n_sr * R, m->F,
                                                             reinterpret_cast<const uint8_t*>(m->d_bin_table), L.bin_k,
-                                                            fg_levels, static_cast<uint32_t*>(codes));
+                                                            fg_levels, static_cast<uint32_t*>(codes), nullptr, 1, 0);
       count_launch();
       err = cudaGetLastError();
       if (err != cudaSuccess) {

@@ -25,7 +25,14 @@ def _x_rows(cfg, rows, row0=0):
     return np.concatenate([gen_x(cfg.seed, row0 + int(r), 1, cfg.n_features) for r in rows])
 
 
-def test_c3_full_size_sampled():
+@pytest.mark.parametrize("binning", [None, "entry_lockstep"])
+def test_c3_full_size_sampled(binning, monkeypatch):
+    """C3 at full size (the bench's launch configuration), and with the
+    bucket-entry binning kernel in lockstep epochs (cooperative launch, grid
+    barriers every ~24 MB of X: the path for inputs larger than L2)."""
+    if binning:
+        monkeypatch.setenv("BRIDGER_BIN", "E")
+        monkeypatch.setenv("BRIDGER_BIN_LOCK", "1")
     c, m = make_config("C3")
     g = B.Model(m)
     X = gen_x_torch(c.seed, 0, c.n_rows, c.n_features, device="cuda")

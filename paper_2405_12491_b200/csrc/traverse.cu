@@ -1102,6 +1102,11 @@ static cudaError_t launch_binning(const bridger_model* m, const TravLayout& L, c
         cfg.numAttrs = 1;
         err = cudaLaunchKernelEx(&cfg, k, tm, X, n_rows, n_tma_rows, Fi, bke, nbi, sti, codes32, epochs, ipe, n_epochs);
         cudaFreeAsync(epochs, st);
+        if (err != cudaSuccess) {  // not co-resident (e.g. a shared GPU): the free-running kernel
+          cudaGetLastError();
+          k<<<grid, nw * 32, bsm, st>>>(tm, X, n_rows, n_tma_rows, Fi, bke, nbi, sti, codes32, nullptr, 1, 0);
+          err = cudaSuccess;
+        }
       } else {
         k<<<grid, nw * 32, bsm, st>>>(tm, X, n_rows, n_tma_rows, Fi, bke, nbi, sti, codes32, nullptr, 1, 0);
         err = cudaSuccess;

@@ -328,9 +328,10 @@ bridger_status bridger_bin_codes_host(const bridger_model_desc* d_in, const floa
   for (int32_t f = 0; f < F; ++f) {
     const float* prm = reinterpret_cast<const float*>(blob + (size_t)f * 16);
     const float lo = prm[0], iw = prm[1];
+    // bucketed tables: U row at word offset prm[3]; entry tables: fixed stride
     const float* U = reinterpret_cast<const float*>(
                          blob + (size_t)F * 16 + (size_t)F * (method == 1 ? cum_row : (size_t)NB * 16)) +
-                     (size_t)f * stride;
+                     (method == 1 ? (size_t)reinterpret_cast<const uint32_t*>(prm)[3] : (size_t)f * stride);
     for (int64_t r = 0; r < n_rows; ++r) {
       const float x = X[r * F + f];
       uint16_t& c = codes[r * F + f];

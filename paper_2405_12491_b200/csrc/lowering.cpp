@@ -315,9 +315,16 @@ static void build_bucket_table(int32_t F, TravLayout* out, int32_t staging_bytes
   size_t nmax = 0;
   for (auto& v : u) nmax = std::max(nmax, v.size());
   const int32_t stride = (int32_t)((nmax + 16 + 3) / 4 * 4);  // + 15 +inf pad (window overrun), 16-B rows
+  // U rows: all-features tables give each feature a row of its own length
+  // (count + 16, 16-byte multiple; word offset in prm[3]) -- the freed bytes
+  // buy the kernel a third staged block; feature-group tables keep one stride
+  // (a group's rows are copied as one contiguous range)
+  std::vector<uint32_t> uoff(F + 1, 0);
+  for (int32_t f = 0; f < F; ++f)
+    uoff[f + 1] = uoff[f] + (fg_features > 0 ? (uint32_t)stride : (uint32_t)((u[f].size() + 16 + 3) / 4 * 4));
   for (int32_t NB : {256, 512, 1024, 2048, 4096, 8192, 16384}) {
     const size_t cum_row = ((size_t)(NB + 2) * 2 + 3) / 4 * 4;
-    const size_t bytes = (size_t)F * 16 + (size_t)F * cum_row + (size_t)F * stride * 4;
+    const size_t bytes = (size_t)F * 16 + (size_t)F * cum_row + (size_t)uoff[F] * 4;
     if (fg_features > 0) {
       if ((size_t)fg_features * (16 + cum_row + (size_t)stride * 4) + 64 > (size_t)kSmemMax) break;
     } else if (bytes + (size_t)staging_bytes + 64 > (size_t)kSmemMax) {
@@ -355,6 +362,7 @@ static void build_bucket_table(int32_t F, TravLayout* out, int32_t staging_bytes
       prm[0] = lo;
       prm[1] = iw;
       reinterpret_cast<uint32_t*>(prm)[2] = (uint32_t)sf;
+      reinterpret_cast<uint32_t*>(prm)[3] = uoff[f];
       uint16_t* cum = reinterpret_cast<uint16_t*>(blob.data() + (size_t)F * 16 + (size_t)f * cum_row);
       int32_t run = 0;
       for (int32_t b = 0; b < NB; ++b) {
@@ -362,8 +370,8 @@ static void build_bucket_table(int32_t F, TravLayout* out, int32_t staging_bytes
         run += cnt[b];
       }
       cum[NB] = (uint16_t)run;
-      float* U = reinterpret_cast<float*>(blob.data() + (size_t)F * 16 + (size_t)F * cum_row) + (size_t)f * stride;
-      for (int32_t i = 0; i < stride; ++i) U[i] = i < (int32_t)v.size() ? v[i] : INFINITY;
+      float* U = reinterpret_cast<float*>(blob.data() + (size_t)F * 16 + (size_t)F * cum_row) + uoff[f];
+      for (int32_t i = 0; i < (int32_t)(uoff[f + 1] - uoff[f]); ++i) U[i] = i < (int32_t)v.size() ? v[i] : INFINITY;
     }
     if (!ok) continue;
     out->bkt_blob.swap(blob);

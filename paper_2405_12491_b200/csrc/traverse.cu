@@ -354,9 +354,12 @@ __global__ void __launch_bounds__(512, 1) bin_coop_kernel(const float* __restric
 // double-buffered dense [32][F] block, the last warp done with a buffer
 // refills it; every warp owns fixed feature pairs (chain constants hoisted).
 template <int NP>
+// nbuf (2 or 3) staged row blocks: the DRAM reads in flight per SM are what
+// the kernel waits on once the window search is cheap; feature f's U row sits
+// at word offset prm_f[3] (rows of their own length: lowering.cpp).
 __global__ void __launch_bounds__(512, 1) bin_bucket_kernel(const float* __restrict__ X, int64_t n_rows, int32_t F,
                                                             const uint8_t* __restrict__ blob, int32_t blob_bytes,
-                                                            int32_t NB, int32_t stride,
+                                                            int32_t NB, int32_t nbuf,
                                                             uint32_t* __restrict__ codes) {
   extern __shared__ __align__(128) uint8_t smem[];
   // programmatic dependent launch: the walk kernel that consumes the codes may
@@ -367,17 +370,18 @@ __global__ void __launch_bounds__(512, 1) bin_bucket_kernel(const float* __restr
   const size_t tab_bytes = ((size_t)blob_bytes + 127) / 128 * 128;
   const uint32_t blk_bytes = 128u * (uint32_t)F;
   float* stage = reinterpret_cast<float*>(smem + tab_bytes);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + tab_bytes + 2 * (size_t)blk_bytes);
-  uint32_t* done = reinterpret_cast<uint32_t*>(bars + 2);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + tab_bytes + (size_t)nbuf * blk_bytes);
+  uint32_t* done = reinterpret_cast<uint32_t*>(bars + nbuf);
   {
     const float4* src = reinterpret_cast<const float4*>(blob);
     float4* dst = reinterpret_cast<float4*>(smem);
     for (int i = threadIdx.x; i < blob_bytes / 16; i += blockDim.x) dst[i] = src[i];
   }
   if (threadIdx.x == 0) {
-    ptx::mbar_init(&bars[0], 1);
-    ptx::mbar_init(&bars[1], 1);
-    done[0] = done[1] = 0;
+    for (int b = 0; b < nbuf; ++b) {
+      ptx::mbar_init(&bars[b], 1);
+      done[b] = 0;
+    }
     ptx::fence_barrier_init();
   }
   __syncthreads();
@@ -392,8 +396,7 @@ __global__ void __launch_bounds__(512, 1) bin_bucket_kernel(const float* __restr
       ptx::bulk_g2s(stage + (size_t)buf * 32 * F, X + b * 32 * (int64_t)F, blk_bytes, &bars[buf]);
     }
   };
-  issue(blockIdx.x, 0);
-  issue((int64_t)blockIdx.x + gridDim.x, 1);
+  for (int b = 0; b < nbuf; ++b) issue((int64_t)blockIdx.x + (int64_t)b * gridDim.x, b);
   // this warp's pairs warp, warp + NW, ... (one pass covers all: NP * NW >= F2h)
   const int npairs = warp < F2h ? min(NP, (F2h - 1 - warp) / NW + 1) : 0;
   uint32_t xoff[2 * NP], cumb[2 * NP], ub[2 * NP], hi_mask[NP];
@@ -408,18 +411,19 @@ __global__ void __launch_bounds__(512, 1) bin_bucket_kernel(const float* __restr
     lo[u] = ptx::lds_f32(sbase + 16u * f);
     iw[u] = ptx::lds_f32(sbase + 16u * f + 4u);
     cumb[u] = cum0 + cum_row * (uint32_t)f;
-    ub[u] = u0 + 4u * (uint32_t)(stride * f);
+    ub[u] = u0 + 4u * ptx::lds_u32(sbase + 16u * f + 12u);
   }
 #pragma unroll
   for (int q = 0; q < NP; ++q) hi_mask[q] = 2 * (warp + q * NW) + 1 >= F ? 0u : 0xFFFFFFFFu;
   const bool even_f = (F & 1) == 0;  // pairs (2p, 2p+1) are 8-byte aligned in a row
   int it = 0;
+  int buf = 0;
+  uint32_t par = 0;
   for (int64_t blk = blockIdx.x; blk < n_blocks; blk += gridDim.x, ++it) {
-    const int buf = it & 1;
     float* St = stage + (size_t)buf * 32 * F;
     const int64_t row0 = blk * 32;
     if (row0 + 32 <= n_rows) {
-      ptx::mbar_wait(&bars[buf], (uint32_t)(it >> 1) & 1u);
+      ptx::mbar_wait(&bars[buf], par);
     } else {
       __syncthreads();
       const int rows = (int)(n_rows - row0);
@@ -477,13 +481,17 @@ __global__ void __launch_bounds__(512, 1) bin_bucket_kernel(const float* __restr
       __threadfence_block();
       if (atomicAdd(&done[buf], 1u) == (uint32_t)NW - 1u) {
         done[buf] = 0;
-        if (blk + 2 * (int64_t)gridDim.x < n_blocks && (blk + 2 * (int64_t)gridDim.x + 1) * 32 <= n_rows) {
+        const int64_t nb2 = blk + (int64_t)nbuf * gridDim.x;
+        if (nb2 < n_blocks && (nb2 + 1) * 32 <= n_rows) {
           ptx::fence_proxy_async();
           ptx::mbar_arrive_expect_tx(&bars[buf], blk_bytes);
-          ptx::bulk_g2s(stage + (size_t)buf * 32 * F, X + (blk + 2 * (int64_t)gridDim.x) * 32 * (int64_t)F, blk_bytes,
-                        &bars[buf]);
+          ptx::bulk_g2s(stage + (size_t)buf * 32 * F, X + nb2 * 32 * (int64_t)F, blk_bytes, &bars[buf]);
         }
       }
+    }
+    if (++buf == nbuf) {
+      buf = 0;
+      par ^= 1u;
     }
   }
 }
@@ -1187,7 +1195,10 @@ static cudaError_t launch_binning(const bridger_model* m, const TravLayout& L, c
     if (const char* e = std::getenv("BRIDGER_BIN_WARPS")) nw = std::max(1, std::min(16, std::atoi(e)));
     const int np = (f2h + nw - 1) / nw;  // pairs per warp: one pass
     const int blob = (int)L.bkt_blob.size();
-    const int bsm = (blob + 127) / 128 * 128 + 2 * 128 * m->F + 32;
+    // three staged blocks when they fit (more DRAM reads in flight), else two
+    int nbuf = (blob + 127) / 128 * 128 + 3 * 128 * m->F + 48 <= 232448 ? 3 : 2;
+    if (const char* e = std::getenv("BRIDGER_BIN_NBUF")) nbuf = std::max(2, std::min(nbuf, std::atoi(e)));
+    const int bsm = (blob + 127) / 128 * 128 + nbuf * 128 * m->F + 16 * nbuf;
     using BinB = void (*)(const float*, int64_t, int32_t, const uint8_t*, int32_t, int32_t, int32_t, uint32_t*);
     const BinB bks[8] = {bin_bucket_kernel<1>, bin_bucket_kernel<2>, bin_bucket_kernel<3>, bin_bucket_kernel<4>,
                          bin_bucket_kernel<5>, bin_bucket_kernel<6>, bin_bucket_kernel<7>, bin_bucket_kernel<8>};
@@ -1196,8 +1207,7 @@ static cudaError_t launch_binning(const bridger_model* m, const TravLayout& L, c
       static std::atomic<uint64_t> attr[8];
       smem_opt_in(reinterpret_cast<const void*>(bk), attr[np - 1]);
       const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nbk, sms));
-      bk<<<grid, nw * 32, bsm, st>>>(X, n_rows, m->F, m->d_bkt, blob, L.bkt_nb, L.bkt_stride,
-                                     static_cast<uint32_t*>(codes));
+      bk<<<grid, nw * 32, bsm, st>>>(X, n_rows, m->F, m->d_bkt, blob, L.bkt_nb, nbuf, static_cast<uint32_t*>(codes));
       count_launch();
       err = cudaGetLastError();
       if (err != cudaSuccess) {

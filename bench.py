@@ -349,9 +349,12 @@ def workload_config(cfg, world, n_rows=None):
 
 
 # ------------------------------------------------------------ GPU leg ----
-def time_steps(step, steps, warmup, dev, world, flush, st, sampler=None):
+def time_steps(step, steps, warmup, dev, world, flush, st, sampler=None, hot=True):
     """W untimed warm-ups, then `steps` steps each between CUDA events on the
-    launching stream (L2 flush outside the events); max over ranks."""
+    launching stream (L2 flush outside the events); max over ranks.  hot:
+    the library also records events around its dominant kernel (the
+    roofline's launch duration) -- off for the latency-only C1 line, where the
+    two extra event records would be part of what is measured."""
     import torch
     import torch.distributed as dist
     import paper_2405_12491_b200 as B
@@ -362,7 +365,7 @@ def time_steps(step, steps, warmup, dev, world, flush, st, sampler=None):
     if world > 1:
         dist.barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-    B.hot_kernel_timing(True)
+    B.hot_kernel_timing(hot)
     for k in range(4):
         B.hot_kernel_time(k)
     l0 = B.launch_count()
@@ -453,7 +456,8 @@ def run_workload(name, args, dev, world, rank, local, headline, rows=None, trees
 
     steps = args.steps if headline else max(3, min(args.steps, 8))
     clk = ClockSampler(local) if headline else None
-    ms, hot, launches, t_wall = time_steps(step, steps, args.warmup, dev, world, flush, st, clk)
+    latency_only = name == "C1" and not headline  # the C1 extra: launch latency, no meaningful roofline
+    ms, hot, launches, t_wall = time_steps(step, steps, args.warmup, dev, world, flush, st, clk, hot=not latency_only)
     res = {"value": n_total / (ms / 1e3), "ms_per_step": ms, "steps": steps, "gpu_launches": launches,
            "wall_s_timed": t_wall, "config": workload_config(cfg, world, n_total)}
     if reduce_desc:
@@ -469,7 +473,9 @@ def run_workload(name, args, dev, world, rank, local, headline, rows=None, trees
     if hot_n == 0:
         hot_ms, hot_n = hot[3]
     hot_avg = hot_ms / max(1, hot_n)
-    if info["variant"] == "traverse":
+    if latency_only:
+        res["roofline"] = None
+    elif info["variant"] == "traverse":
         res["roofline"] = trav_roofline(B, model, cfg, n, hot_avg, local)
         res["roofline"]["kernel_share_of_step"] = hot_ms / steps / ms
     else:
@@ -483,7 +489,7 @@ def run_workload(name, args, dev, world, rank, local, headline, rows=None, trees
     if os.path.exists(tr):
         try:
             t = json.load(open(tr)).get(f"{cfg.name}:{info['variant']}:{n}")
-            if t is not None:
+            if t is not None and res["roofline"] is not None:
                 res["roofline"]["traffic"] = t
         except Exception:
             pass

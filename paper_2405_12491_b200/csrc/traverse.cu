@@ -937,7 +937,7 @@ __global__ void __launch_bounds__(512, 1) bin_fg_kernel(const float* __restrict_
 // that every chunk CTA bulk-copies blocks with no per-chunk transpose.
 __global__ void __launch_bounds__(512) xpose_kernel(const float* __restrict__ X, int64_t n_rows, int32_t F,
                                                     float* __restrict__ XT) {
-  extern __shared__ __align__(16) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
   const int S = F | 1;
   float* St = reinterpret_cast<float*>(smem) + (size_t)warp * 32 * S;

@@ -9,7 +9,7 @@ Cases (VERDICT r1 "what's weak" #9 lists the async pipelines to cover):
   tree-streamed model (K4s: loader warp ring, slot headers, cp.async landing
   slots), the fused GEMM-form kernel fz_kernel (K5) and the staged
   gc -> pc -> lg pipeline (K1/K2/K3), a linear model, and the cluster/DSMEM
-  variant of K4 (BRIDGER_CLUSTER=1).
+  variant of K4 (BRIDGER_CLUSTER=1), and round 2's binning kernels.
 """
 import os
 import sys
@@ -39,8 +39,9 @@ def check(name, m, X, variant=None, env=None):
             assert np.array_equal(got, want), name
         else:
             np.testing.assert_allclose(got, want, rtol=1e-5, atol=1e-6, err_msg=name)
+        fmt = g.layout()["format"] if variant in (None, "traverse") else variant
         g.close()
-        print(f"case {name}: ok ({g.layout()['format'] if variant in (None, 'traverse') else variant})", flush=True)
+        print(f"case {name}: ok ({fmt})", flush=True)
     finally:
         for k, v in old.items():
             if v is None:
@@ -68,6 +69,18 @@ def main():
     cases.append(("C2_staged_gc_pc_lg", make_config("C2", n_trees=12)[1], gen_x(2, 0, 1000, 28), "gemm_staged", None))
     cases.append(("C2_cluster_dsmem", make_config("C2", n_trees=100)[1], gen_x(2, 0, 4096, 28), None,
                   {"BRIDGER_CLUSTER": "1", "BRIDGER_CODES": "0"}))
+    # round-2 binning kernels: bucket entries (TMA row tiles), feature-group
+    # bucketed tables with TMA tiles, Eytzinger pairs with TMA tiles (2^16-slot
+    # trees: tests/test_gpu_parity.py test_coded_wide_code_range), the
+    # three-buffer all-features bucketed kernel, odd F (4-row views)
+    cases.append(("C2_bin_entry", m2, gen_x(2, 0, 4099, 28), None, {"BRIDGER_BIN": "E"}))
+    cases.append(("C3_bin_bucket_nbuf3", m3, gen_x(3, 0, 4099, 90), None, {"BRIDGER_BIN": "b"}))
+    cases.append(("C5_bin_fg_tma", m5, gen_x(5, 0, 2048, 200), None, None))
+    cases.append(("C4_codes_bin_fg4", make_config("C4", n_trees=40)[1], gen_x(4, 0, 2048, 64), None,
+                  {"BRIDGER_CODES": "1"}))
+    cases.append(("F21_bin_entry_R4", perfect_ensemble(27, 90, 8, 21, kind="classification", n_classes=3,
+                                                       calib_rows=2048), gen_x(28, 0, 3001, 21), None,
+                  {"BRIDGER_BIN": "E", "BRIDGER_CODES": "1"}))
     for name, m, X, variant, env in cases:
         if only and name not in only:
             continue

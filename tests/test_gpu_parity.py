@@ -240,6 +240,21 @@ def test_coded_binning_variants(binv, F, monkeypatch):
     assert g.layout()["coded"]
 
 
+@pytest.mark.parametrize("nbuf", ["2", "3"])
+def test_bucketed_binning_many_blocks_per_cta(nbuf, monkeypatch):
+    """The all-features bucketed kernel with 10+ row blocks per CTA (every
+    staging buffer reused several times: the mbarrier phases of a 2- and a
+    3-buffer ring) and a ragged last block filled by hand; C3-shaped, 50,021
+    rows, bitwise."""
+    monkeypatch.setenv("BRIDGER_CODES", "1")
+    monkeypatch.setenv("BRIDGER_BIN", "b")
+    monkeypatch.setenv("BRIDGER_BIN_NBUF", nbuf)
+    c, m = make_config("C3", n_trees=60)
+    X = inject_specials(gen_x(3, 0, 50021, 90), 33, rate=0.01)
+    g, _ = check(m, X, apply=False)
+    assert g.layout()["coded"]
+
+
 @pytest.mark.parametrize("F,n", [(7, 129), (7, 131), (90, 130), (28, 160), (90, 4099)])
 def test_entry_binning_small_and_ragged(F, n, monkeypatch):
     """Bucket-entry binning (BRIDGER_BIN=E: an error unless that kernel runs)

@@ -326,8 +326,17 @@ def gemm_roofline(B, m, cfg, X, dev, n_max=2_000_000):
               "frac": k1_bytes / (k1_ms / 1e3) / 1e9 / hbm, "ms_per_step": k1_ms / steps,
               "k3_leaf_gather_ms_per_step": k3_ms / steps}
     achieved = ops / (k2_ms / 1e3) / 1e12
+    # K2 streams every (tree, 128-row) decision tile (i_pad bytes per row-tree)
+    # from HBM once: its other roofline -- the binding one at small depths
+    # (C3: 64-byte rows, 64x64 contractions)
+    k2_bytes = steps * n * cfg.n_trees * ip
+    k2_hbm = {"bound": "hbm", "achieved": k2_bytes / (k2_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+              "frac": k2_bytes / (k2_ms / 1e3) / 1e9 / hbm,
+              "note": "decision tiles read once per contraction (the int8 frac above is low by construction when "
+                      "each 64-byte decision row feeds only 2*64*64 ops)"}
     return {"kernel": "pc_kernel (tcgen05.mma kind::i8, TMEM accumulators)", "bound": "tensor",
             "achieved": achieved, "peak": peak, "unit": "TOP/s", "frac": achieved / peak, "peak_source": src,
+            "decision_stream": k2_hbm,
             "rows": n, "k2_ms_per_step": k2_ms / steps, "k2_launches_per_step": k2_n // steps,
             "gemm_variant_ms_per_step": s_ms, "gemm_variant_rows_per_s": n / (s_ms / 1e3),
             "gather_compare": gather, "fused": fused,

@@ -67,3 +67,30 @@ def test_fuzz_shapes(seed, monkeypatch):
         np.testing.assert_array_equal(a, o["acc"], err_msg=tag)
     else:
         np.testing.assert_allclose(a, o["acc"], rtol=1e-9, atol=1e-12, err_msg=tag)
+
+
+@pytest.mark.parametrize("variant", ["gemm", "gemm_staged", "gemm_sparse"])
+@pytest.mark.parametrize("seed", list(range(12)))
+def test_fuzz_gemm_variants(seed, variant):
+    """The paper's GEMM form (fused K5, staged K1->K2->K3, 2:4-sparse K2s) on
+    randomised shapes of depth <= 8 (the path matrix's range) vs the oracle."""
+    F, D, T, K, kind, n, prune, _ = _case(100 + seed)
+    D = min(D, 8)
+    T = min(T, 120)
+    n = min(n, 6000)
+    m = perfect_ensemble(6000 + seed, T, D, F, kind=kind, n_classes=K if kind == "classification" else 1,
+                         lr=0.05, calib_rows=1024)
+    if prune:
+        m = prune_ensemble(m, 7000 + seed, p=0.08, with_missing=True)
+    X = inject_specials(gen_x(8000 + seed, 0, n, F), 9000 + seed, rate=0.01)
+    g = B.Model(m, variant=variant)
+    o = oracle.run(m, X)
+    Xd = torch.from_numpy(np.ascontiguousarray(X)).cuda()
+    tag = f"{variant} F={F} D={D} T={T} K={K} {kind} n={n} prune={prune}"
+    exact = g.info()["exact_tier"] == "E53"
+    if m.task == 1:
+        np.testing.assert_array_equal(g.predict(Xd).cpu().numpy(), o["label"], err_msg=tag)
+    elif exact:
+        np.testing.assert_array_equal(g.predict(Xd).cpu().numpy(), o["pred"], err_msg=tag)
+    else:
+        np.testing.assert_allclose(g.predict(Xd).cpu().numpy(), o["pred"], rtol=1e-5, atol=1e-6, err_msg=tag)

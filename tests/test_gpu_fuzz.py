@@ -61,6 +61,15 @@ def test_fuzz_shapes(seed, monkeypatch):
         else:
             np.testing.assert_allclose(got, o["pred"], rtol=1e-5, atol=1e-6, err_msg=tag)
     np.testing.assert_array_equal(g.apply(Xd).cpu().numpy(), o["leaf"], err_msg=tag)
+    if m.task == 1:
+        pr = g.predict_proba(Xd).cpu().numpy()
+        if exact and m.post == 0:
+            np.testing.assert_array_equal(pr, o["proba"], err_msg=tag)
+        else:
+            np.testing.assert_allclose(pr, o["proba"], rtol=1e-5, atol=1e-7, err_msg=tag)
+    # the end-to-end host-buffer API (chunked H2D / compute / D2H pipeline)
+    host = g.predict_host(X).numpy()
+    np.testing.assert_array_equal(host, g.predict(Xd).cpu().numpy(), err_msg=tag)
     raw = g.predict_raw(Xd).cpu().numpy()
     a = raw.astype(np.float64) * 2.0 ** info["acc_scale_exp"] if info["acc_is_int64"] else raw
     if exact:

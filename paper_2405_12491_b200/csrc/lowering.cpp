@@ -965,9 +965,14 @@ bool build_trav_layout(const bridger_model_desc* d, const std::vector<int32_t>& 
         }
       }
       float* lv = reinterpret_cast<float*>(base + c.leaf_offset) + (size_t)j * L * K;
+      // v * 2^-q: an integer-valued float < 2^63 (exact: a power-of-two scale
+      // of a 24-bit significand, done in double, which holds 2^-q for any q
+      // of the int64 tiers; the product is an integer, never subnormal) --
+      // one multiply instead of a std::ldexp call per leaf value (C4: 33M)
+      const double sq = std::ldexp(1.0, -ex.q);
       for (int32_t l = 0; l < L * K; ++l) {
         const float v = pt.leaf_value[l];
-        lv[l] = acc_int ? std::ldexp(v, -ex.q) : v;  // exact: integer-valued float < 2^63
+        lv[l] = acc_int ? (float)((double)v * sq) : v;
       }
       out->slot_tree[r.start + j] = t;
       out->slot_leafid_off[r.start + j] = (int64_t)out->leaf_ids.size();

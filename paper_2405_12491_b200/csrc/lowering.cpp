@@ -404,7 +404,11 @@ static void build_entry_table(int32_t F, TravLayout* out) {
   const bool rows_aligned = (F * 4) % 16 == 0;
   auto nb_for = [&](int32_t fg) {
     const int64_t w = rows_aligned ? fg : fg + 4;
-    const int64_t staging = 16LL * 2 * 32 * w * 4 + 16 * 2 * 8 + 64;
+    // 32 warps of double-buffered tiles where rows are aligned (the
+    // L2-resident default case, C2), else 16 (bin_entry_kernel's launcher
+    // falls back to 16 when 32 do not fit)
+    const int64_t nwarps = rows_aligned ? 32 : 16;
+    const int64_t staging = nwarps * 2 * 32 * w * 4 + nwarps * 2 * 8 + 64;
     const int64_t per_f = (kSmemMax - staging) / fg - 16 - 4LL * stride;
     return (int32_t)std::max<int64_t>(0, per_f / 16 / 32 * 32);
   };

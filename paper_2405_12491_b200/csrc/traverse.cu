@@ -633,7 +633,7 @@ __host__ __device__ constexpr int bin_tile_w(int FG, int R) {
 // finished the epoch before the previous one: at most ~2 epochs (~2 x 24 MB
 // of X) are in flight, so the groups share each row's sectors through L2.
 template <int FG, int R, int TAB>
-__global__ void __launch_bounds__(512, 1) bin_entry_kernel(const __grid_constant__ CUtensorMap tmx,
+__global__ void __launch_bounds__(1024, 1) bin_entry_kernel(const __grid_constant__ CUtensorMap tmx,
                                                            const float* __restrict__ X, int64_t n_rows, int64_t n_tma,
                                                            int32_t F, const uint8_t* __restrict__ blob, int32_t NB,
                                                            int32_t stride, uint32_t* __restrict__ codes,
@@ -1067,8 +1067,14 @@ static cudaError_t launch_binning(const bridger_model* m, const TravLayout& L, c
     if (err == cudaSuccess) {
       const int FG = L.bke_fg;
       const int n_fg = (m->F + FG - 1) / FG;
-      const int nw = 16;
-      const int bsm = nw * 2 * 32 * bin_tile_w(FG, R) * 4 + 16 * FG + FG * L.bke_nb * 16 + FG * L.bke_stride * 4 + 8 * (2 * nw + 1);
+      // as many warps (chains in flight) as fit next to the tables: 32, else 16
+      auto bsm_of = [&](int w) {
+        return w * 2 * 32 * bin_tile_w(FG, R) * 4 + 16 * FG + FG * L.bke_nb * 16 + FG * L.bke_stride * 4 + 8 * (2 * w + 1);
+      };
+      int nw = 32;
+      if (const char* e = std::getenv("BRIDGER_BIN_WARPS")) nw = std::atoi(e) >= 32 ? 32 : 16;
+      if (bsm_of(nw) > 232448) nw = 16;
+      const int bsm = bsm_of(nw);
       const int64_t slices = pick_slices(n_fg, sms, (nbk + nw - 1) / nw);
       using BinE = void (*)(const CUtensorMap, const float*, int64_t, int64_t, int32_t, const uint8_t*, int32_t, int32_t,
                             uint32_t*, uint32_t*, int32_t, int32_t);
@@ -1146,7 +1152,8 @@ static cudaError_t launch_binning(const bridger_model* m, const TravLayout& L, c
     const int W = bin_tile_w(4, R);
     const int n_fg = (m->F + 3) / 4;
     const int cum_row = ((L.bkt_nb + 2) * 2 + 3) / 4 * 4;
-    int nw = 16;
+    int nw = 32;
+    if (const char* e = std::getenv("BRIDGER_BIN_WARPS")) nw = std::atoi(e) >= 32 ? 32 : 16;
     auto bsm_of = [&](int w) { return w * 2 * 32 * W * 4 + 4 * (16 + cum_row + 4 * L.bkt_stride) + 8 * (2 * w + 1); };
     while (nw > 4 && bsm_of(nw) > 232448) nw /= 2;
     CUtensorMap tm;
@@ -1281,7 +1288,8 @@ static cudaError_t launch_binning(const bridger_model* m, const TravLayout& L, c
     const int R = (m->F * 4) % 16 == 0 ? 1 : (m->F * 8) % 16 == 0 ? 2 : 4;
     const int W = bin_tile_w(2, R);
     const int n_fg = (m->F + 1) / 2;
-    int nw = 16;
+    int nw = 32;
+    if (const char* e = std::getenv("BRIDGER_BIN_WARPS")) nw = std::atoi(e) >= 32 ? 32 : 16;
     auto bsm_of = [&](int w) { return w * 2 * 32 * W * 4 + 2 * 16 + bsm + 8 * (2 * w + 1); };
     while (nw > 4 && bsm_of(nw) > 232448) nw /= 2;
     CUtensorMap tm;

@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(128) gc_kernel(const float* __restrict__ X, in
                                                  const uint8_t* __restrict__ gbase, GemmClassDev cls,
                                                  int32_t tree_begin, int32_t trees_per_cta, int32_t tree_end,
                                                  int8_t* __restrict__ P) {
-  extern __shared__ __align__(16) uint8_t smem[];
+  extern __shared__ __align__(1024) uint8_t smem[];
   const int r = threadIdx.x;
   const int rt = blockIdx.x;
   const int n_rt = gridDim.x;
